@@ -1,0 +1,195 @@
+/*
+ * ls2.h — C ABI of the B200 (sm_100a) LightSeq2 training hot path.
+ *
+ * Every entry point takes plain device pointers, sizes, dtype codes and a
+ * cudaStream_t passed as void*.  All calls are asynchronous (enqueue only),
+ * allocate nothing and never synchronize, so they are CUDA-Graph capturable.
+ * Return value: LS2_OK or an LS2_ERR_* status; ls2_last_error() gives text.
+ * Status codes map 1:1 onto the reference's exception taxonomy
+ * (/root/reference/pkg/src/ftrain/errors.py:4-57).
+ *
+ * Each function cites the reference operator it replaces
+ * (F/ = /root/reference/pkg/src/ftrain/).
+ */
+#ifndef LS2_H
+#define LS2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types */
+enum {
+  LS2_F16 = 0,
+  LS2_BF16 = 1,
+  LS2_F32 = 2,
+  LS2_F64 = 3
+};
+
+/* status codes (F/errors.py) */
+enum {
+  LS2_OK = 0,
+  LS2_ERR_SHAPE = 1,          /* ShapeMismatch */
+  LS2_ERR_TOKEN = 2,          /* TokenOutOfRange */
+  LS2_ERR_SEQLEN = 3,         /* SequenceTooLong */
+  LS2_ERR_DEGENERATE = 4,     /* DegenerateRow */
+  LS2_ERR_ALLMASKED = 5,      /* AllMaskedRow */
+  LS2_ERR_TARGET = 6,         /* TargetOutOfRange */
+  LS2_ERR_DTYPE = 7,          /* unsupported dtype combination (ShapeMismatch) */
+  LS2_ERR_CUDA = 8,           /* CUDA runtime error */
+  LS2_ERR_CUBLAS = 9          /* cuBLAS error */
+};
+
+/* softmax mask kinds (F/kernels.py:113-144) */
+enum {
+  LS2_MASK_NONE = 0,
+  LS2_MASK_CAUSAL = 1,        /* keep col <= row % lq                          */
+  LS2_MASK_PADDING = 2,       /* keep col < valid_len[row / (heads * lq)]     */
+  LS2_MASK_DENSE = 3          /* uint8 keep[rows, cols]                        */
+};
+
+const char* ls2_last_error(void);
+int ls2_version(void);
+int ls2_num_kernels_launched(int64_t* out);   /* launches since load (host counter) */
+
+/* ---- counter RNG / dropout masks: F/numerics.py:139-163, F/kernels.py:155-166 ----
+ * keep bit i (byte i>>3, bit i&7) == (splitmix64(seed + i*phi) >> 11) >= thresh,
+ * thresh = ceil(p * 2^53).  Bit-identical to rand_uniform_array(seed,0,n) >= p. */
+int ls2_rand_uniform(double* out, uint64_t seed, int64_t start, int64_t n, void* stream);
+int ls2_dropout_bits(uint8_t* bits, int64_t n, uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, void* stream);
+int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream);
+int ls2_dense_to_bits(const void* dense, int dtype, uint8_t* bits, int64_t n, void* stream);
+
+/* ---- fused elementwise tails ----
+ * bias+dropout+residual  (F/kernels.py:367-382):
+ *   y = keep*(x+bias)*scale + res, keep bits generated (gen=1) or read (gen=0).
+ * x,bias,res share dtype tin; y has tout.  scale = f32/f64(1/(1-p)); p==0 -> use_drop=0. */
+int ls2_bias_dropout_residual_fwd(const void* x, const void* bias, const void* res, void* y,
+                                  uint8_t* keep_bits, int64_t rows, int64_t cols,
+                                  int use_drop, int gen, uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh,
+                                  double scale, int tin, int tout, void* stream);
+/* backward (F/gradients.py:147-159): dx = keep*dy*scale; dbias = column sums of dx
+ * (deterministic two-stage; beta=1 accumulates into dbias); dres is dy itself.
+ * ws: workspace of ls2_colsum_ws_bytes(rows, cols) bytes. */
+int ls2_bias_dropout_residual_bwd(const void* dy, const uint8_t* keep_bits, void* dx,
+                                  void* dbias, int tbias, int beta_bias, void* ws,
+                                  int64_t rows, int64_t cols, int use_drop, double scale,
+                                  int tin, int tout, void* stream);
+/* bias+relu+dropout (F/kernels.py:385-403): y = keep*relu(x+b)*scale, relu bit = (x+b)>0 */
+int ls2_bias_relu_dropout_fwd(const void* x, const void* bias, void* y, uint8_t* keep_bits,
+                              uint8_t* relu_bits, int64_t rows, int64_t cols, int use_drop,
+                              int gen, uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, double scale,
+                              int tin, int tout, void* stream);
+/* backward (F/gradients.py:162-172) */
+int ls2_bias_relu_dropout_bwd(const void* dy, const uint8_t* keep_bits, const uint8_t* relu_bits,
+                              void* dx, void* dbias, int tbias, int beta_bias, void* ws,
+                              int64_t rows, int64_t cols, int use_drop, double scale,
+                              int tin, int tout, void* stream);
+int64_t ls2_colsum_ws_bytes(int64_t rows, int64_t cols);
+/* deterministic column sums of x[rows, cols] into out[cols] (beta=1 accumulates);
+ * used for the bqkv / cross.bq / cross_kv.b gradients (F/model.py:501,726,258) */
+int ls2_colsum(const void* x, int tin, void* out, int tout, int beta, void* ws,
+               int64_t rows, int64_t cols, void* stream);
+/* y[r, c] += bias[c]  (in place; x dtype == bias dtype) */
+int ls2_bias_add(void* x, const void* bias, int64_t rows, int64_t cols, int dtype, void* stream);
+
+/* ---- LayerNorm: F/kernels.py:235-270 / F/gradients.py:103-144 ----
+ * stats (mu, sigma) have dtype tstat (F32 or F64).  degenerate: optional int*
+ * set to 1 when eps == 0 and a row has zero variance. */
+int ls2_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void* mu,
+                      void* sigma, int* degenerate, int64_t rows, int64_t cols, double eps,
+                      int tin, int tout, int tstat, void* stream);
+/* dx = LN input grad (+ dres if non-null); dw, db column sums (beta=1 accumulates),
+ * dtype tparam.  ws of ls2_layernorm_bwd_ws_bytes(rows, cols) bytes. */
+int64_t ls2_layernorm_bwd_ws_bytes(int64_t rows, int64_t cols);
+int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mu,
+                      const void* sigma, const void* dres, void* dx, void* dw, void* db,
+                      int tparam, int beta_param, void* ws, int64_t rows, int64_t cols,
+                      int tin, int tout, int tstat, void* stream);
+
+/* ---- softmax family: F/kernels.py:277-331 / F/gradients.py:77-100 ----
+ * x rows are the flattened leading dims; mask per LS2_MASK_*.  in_scale
+ * multiplies x before the softmax (folds 1/sqrt(hd)); out may alias x.
+ * all_masked: optional int* set when a row has no kept element. */
+int ls2_softmax_fwd(const void* x, void* y, int64_t rows, int64_t cols, int mask_kind,
+                    int64_t lq, int64_t heads, const int64_t* valid_lens,
+                    const uint8_t* dense_keep, double in_scale, int* all_masked,
+                    int tin, int tout, void* stream);
+/* dx = out_scale * q*(dy - sum dy*q); dx may alias dy */
+int ls2_softmax_bwd(const void* dy, const void* q, void* dx, int64_t rows, int64_t cols,
+                    double out_scale, int tin, int tout, void* stream);
+int ls2_log_softmax_fwd(const void* h, void* y, int64_t rows, int64_t cols, int tin,
+                        int tout, void* stream);
+
+/* ---- label-smoothed CE: F/kernels.py:338-360, F/gradients.py:47-74 ----
+ * row_stats (double[rows*2]) receives per-row (loss, correct) partials;
+ * out3 (double[3]) = (loss_sum, token_count, correct) after the fixed-order reduce. */
+int ls2_ls_ce_fwd(const void* logq, const int64_t* targets, double* row_stats, double* out3,
+                  int* bad_target, int64_t rows, int64_t v, double alpha, int64_t pad_id,
+                  int has_pad, int tin, void* stream);
+int ls2_ls_ce_bwd(const void* probs, const int64_t* targets, void* dh, int* bad_target,
+                  int64_t rows, int64_t v, double alpha, int64_t pad_id, int has_pad,
+                  double grad_scale, int tin, int tout, void* stream);
+/* fused criterion (F/model.py:908-932): logits -> (loss, count, correct) and, when
+ * dlogits != NULL, dlogits = (softmax - a/V - (1-a)[k]) * grad_scale written over
+ * the row (may alias logits).  logq_out (optional) receives log-softmax. */
+int ls2_criterion_fused(const void* logits, const int64_t* targets, void* dlogits,
+                        void* logq_out, double* row_stats, double* out3, int* bad_target,
+                        int64_t rows, int64_t v, double alpha, int64_t pad_id, int has_pad,
+                        double grad_scale, int t_logits, void* stream);
+
+/* ---- embedding: F/kernels.py:203-228 / F/gradients.py:20-44 ---- */
+int ls2_embedding_fwd(const void* emb, const void* pos, const int64_t* tokens, void* y,
+                      uint8_t* keep_bits, int* bad_token, int64_t batch, int64_t len,
+                      int64_t d, int64_t vocab, double emb_scale, int use_drop, int gen,
+                      uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, double drop_scale, int tin, int tout,
+                      void* stream);
+/* dE[tok] += emb_scale*keep*dy*drop_scale (atomic scatter, tgrad F32/F64);
+ * dP[l] (beta_pos: 0 write rows [0,len) and zero [len,max_len), 1 accumulate) */
+int ls2_embedding_bwd(const void* dy, const int64_t* tokens, const uint8_t* keep_bits,
+                      void* dE, void* dP, int tgrad, int beta_pos, int64_t batch,
+                      int64_t len, int64_t d, int64_t max_len, double emb_scale,
+                      int use_drop, double drop_scale, int tin, void* stream);
+
+/* ---- workspace trainer: F/trainer.py:125-181, F/engine.py:152-157 ----
+ * hyper: f32 constants precomputed on the host exactly as numpy does:
+ *   [lr, beta1, 1-beta1, beta2, 1-beta2, eps, wd, loss_scale]
+ * bc: (f32(1-beta1^t), f32(1-beta2^t)) table indexed by t; the step t is
+ *   either `t_host` (>0) or read as *applied + 1 from the device counter.
+ * skip: the update is skipped when *nonfinite != 0 or (loss && !isfinite(*loss)). */
+int ls2_adam(uint16_t* p16, const uint16_t* g16, float* m, float* v, int64_t n,
+             const float* hyper, const float* bc_table, int64_t bc_len, int64_t t_host,
+             const int64_t* applied, const int* nonfinite, const double* loss, void* stream);
+int ls2_sgd(uint16_t* p16, const uint16_t* g16, float* vel, int64_t n, const float* hyper,
+            const int* nonfinite, const double* loss, void* stream);
+/* applied += (nonfinite==0 && loss finite)  — one thread */
+int ls2_step_commit(int64_t* applied, const int* nonfinite, const double* loss,
+                    int* applied_flag, void* stream);
+/* g16 = RNE(acc32 * f32(loss_scale / max(count,1)) * post), count = out3[1] (device) or
+ * count_host (>=0); nonfinite += #non-finite g16 (NULL to skip) */
+int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_scale,
+                     const double* out3, int64_t count_host, float post, int* nonfinite,
+                     void* stream);
+int ls2_count_nonfinite_f16(const uint16_t* g16, int64_t n, int* nonfinite, void* stream);
+
+/* ---- GEMM on cuBLAS (F/kernels.py:413-447), row-major semantics ----
+ * C[b] = alpha * op(A[b]) @ op(B[b]) + beta * C[b], batch index b = (i, j) with
+ * i < n1, j < n2 and element offsets i*sX1 + j*sX2.  Compute fp32 (fp64 for F64),
+ * never TF32.  Types: (A,B) same; C may be wider (F16/BF16 in -> F32 out). */
+void* ls2_blas_create(void);
+void ls2_blas_destroy(void* h);
+int ls2_gemm(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+             double alpha, const void* A, int64_t lda, int64_t sA1, int64_t sA2,
+             const void* B, int64_t ldb, int64_t sB1, int64_t sB2, double beta, void* C,
+             int64_t ldc, int64_t sC1, int64_t sC2, int64_t n1, int64_t n2, int tab, int tc,
+             void* ptr_scratch, void* stream);
+/* bytes of device scratch ls2_gemm needs for pointer-array batches */
+int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LS2_H */

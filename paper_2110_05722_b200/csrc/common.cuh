@@ -1,0 +1,197 @@
+// Shared device/host helpers for the sm_100a hot-path kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <type_traits>
+
+#include "../../include/ls2.h"
+
+namespace ls2 {
+
+// ---------------------------------------------------------------------------
+// status / error text (host)
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+extern std::atomic<int64_t> g_launches;
+
+inline int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LS2_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return LS2_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kNumSMs = 148;  // B200; grid sizes below are fixed for determinism
+
+// ---------------------------------------------------------------------------
+// element types
+// ---------------------------------------------------------------------------
+template <typename T> struct CompOf { using type = float; };
+template <> struct CompOf<double> { using type = double; };
+
+template <typename C, typename T> __device__ __forceinline__ C to_c(T v);
+template <> __device__ __forceinline__ float to_c<float, __half>(__half v) { return __half2float(v); }
+template <> __device__ __forceinline__ float to_c<float, __nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <> __device__ __forceinline__ float to_c<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double to_c<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ double to_c<double, float>(float v) { return (double)v; }
+
+template <typename T, typename C> __device__ __forceinline__ T from_c(C v);
+template <> __device__ __forceinline__ __half from_c<__half, float>(float v) { return __float2half_rn(v); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_c<__nv_bfloat16, float>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ float from_c<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double from_c<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ float from_c<float, double>(double v) { return (float)v; }
+
+// general conversion (single rounding from double where possible)
+template <typename To, typename From>
+__device__ __forceinline__ To cvt(From v) {
+  if constexpr (std::is_same<To, From>::value) {
+    return v;
+  } else if constexpr (std::is_same<To, __half>::value) {
+    if constexpr (std::is_same<From, double>::value) return __double2half(v);
+    else return __float2half_rn((float)v);
+  } else if constexpr (std::is_same<To, __nv_bfloat16>::value) {
+    if constexpr (std::is_same<From, double>::value) return __double2bfloat16(v);
+    else return __float2bfloat16_rn((float)v);
+  } else if constexpr (std::is_same<From, __half>::value) {
+    return (To)__half2float(v);
+  } else if constexpr (std::is_same<From, __nv_bfloat16>::value) {
+    return (To)__bfloat162float(v);
+  } else {
+    return (To)v;
+  }
+}
+
+// IEEE-exact arithmetic in the compute type (no FMA contraction) so the fused
+// element-wise ops reproduce numpy's float32 op order bit for bit.
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// 8 consecutive elements; loaded/stored with 16-byte transactions.
+template <typename T>
+struct alignas(16) Pack8 {
+  T v[8];
+};
+
+template <typename T>
+__device__ __forceinline__ Pack8<T> ld8(const T* p) {
+  Pack8<T> r;
+  constexpr int kWords = sizeof(Pack8<T>) / 16;
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < kWords; ++i) d[i] = __ldg(s + i);
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ Pack8<T> ld8_stream(const T* p) {  // evict-first streaming read
+  Pack8<T> r;
+  constexpr int kWords = sizeof(Pack8<T>) / 16;
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < kWords; ++i) d[i] = __ldcs(s + i);
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const Pack8<T>& v) {
+  constexpr int kWords = sizeof(Pack8<T>) / 16;
+  uint4* d = reinterpret_cast<uint4*>(p);
+  const uint4* s = reinterpret_cast<const uint4*>(&v);
+#pragma unroll
+  for (int i = 0; i < kWords; ++i) d[i] = s[i];
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------
+// splitmix64 counter RNG (F/numerics.py:133-155)
+// ---------------------------------------------------------------------------
+constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMixA = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMixB = 0x94D049BB133111EBull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMixA;
+  z = (z ^ (z >> 27)) * kMixB;
+  return z ^ (z >> 31);
+}
+
+// keep bits for flat elements [8g, 8g+8): bit e set iff mix(seed + (8g+e)*phi)>>11 >= thresh.
+// The counter is advanced by +phi (strength-reduced from the multiply).
+__device__ __forceinline__ uint32_t keep_byte(uint64_t seed, uint64_t first, uint64_t thresh) {
+  uint64_t z = seed + first * kPhi;
+  uint32_t b = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    b |= (uint32_t)((mix64(z) >> 11) >= thresh) << e;
+    z += kPhi;
+  }
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v, int width = 32) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < width) v += __shfl_xor_sync(0xffffffffu, v, o, width);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v, int width = 32) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < width) v = max(v, __shfl_xor_sync(0xffffffffu, v, o, width));
+  return v;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int grid_for(int64_t work, int tpb = 256) {
+  int64_t g = ceil_div(work, tpb);
+  if (g > kNumSMs * 16) g = kNumSMs * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace ls2
+
+// dtype dispatch over the (input, output) pairs the kernels are built for.
+#define LS2_DISPATCH_IO(TIN, TOUT, NAME, ...)                                                  \
+  [&]() -> int {                                                                             \
+    if (TIN == LS2_F16 && TOUT == LS2_F16) { using Tin = __half; using Tout = __half; return __VA_ARGS__(); } \
+    if (TIN == LS2_F16 && TOUT == LS2_F32) { using Tin = __half; using Tout = float; return __VA_ARGS__(); } \
+    if (TIN == LS2_BF16 && TOUT == LS2_BF16) { using Tin = __nv_bfloat16; using Tout = __nv_bfloat16; return __VA_ARGS__(); } \
+    if (TIN == LS2_BF16 && TOUT == LS2_F32) { using Tin = __nv_bfloat16; using Tout = float; return __VA_ARGS__(); } \
+    if (TIN == LS2_F32 && TOUT == LS2_F32) { using Tin = float; using Tout = float; return __VA_ARGS__(); } \
+    if (TIN == LS2_F32 && TOUT == LS2_F16) { using Tin = float; using Tout = __half; return __VA_ARGS__(); } \
+    if (TIN == LS2_F32 && TOUT == LS2_BF16) { using Tin = float; using Tout = __nv_bfloat16; return __VA_ARGS__(); } \
+    if (TIN == LS2_F64 && TOUT == LS2_F64) { using Tin = double; using Tout = double; return __VA_ARGS__(); } \
+    return ::ls2::fail(LS2_ERR_DTYPE, std::string(NAME) + ": unsupported dtype pair");         \
+  }()
+
+#define LS2_DISPATCH_ONE(T, NAME, ...)                                                          \
+  [&]() -> int {                                                                             \
+    if (T == LS2_F16) { using Tx = __half; return __VA_ARGS__(); }                             \
+    if (T == LS2_BF16) { using Tx = __nv_bfloat16; return __VA_ARGS__(); }                     \
+    if (T == LS2_F32) { using Tx = float; return __VA_ARGS__(); }                              \
+    if (T == LS2_F64) { using Tx = double; return __VA_ARGS__(); }                             \
+    return ::ls2::fail(LS2_ERR_DTYPE, std::string(NAME) + ": unsupported dtype");              \
+  }()

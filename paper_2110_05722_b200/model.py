@@ -1,0 +1,1072 @@
+"""Pre-LayerNorm encoder/decoder built from the libls2 fused kernels.
+
+Drop-in for F/model.py (same names, signatures, stash/LIFO discipline, packed
+cross-attention and the "encoder gradient only after decoder layer 0"
+ordering contract).  B200-specific choices, all invisible at the API:
+
+* activations are stored in the parameters' dtype (fp16 on the training
+  path; f32/f64 reproduce the reference's compute dtypes for parity tests);
+* the attention contractions read Q/K/V straight out of the fused [B,L,3d]
+  projection and write the context straight into [B,L,d] (two-level
+  pointer-array cuBLAS batches), so there are no head split/merge copies;
+* 1/sqrt(hd) is folded into the QK^T GEMM alpha and the softmax backward;
+* dropout and relu masks are 1-bit device masks;
+* parameter gradients are written directly into the fp32 gradient workspace
+  (GEMM output / column-sum / LayerNorm partial reductions), never staged;
+* per-step dropout seeds live in a small device table filled by one H2D copy,
+  so a captured CUDA graph of the whole step replays with fresh masks.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import gradients as G
+from . import kernels as K
+from .errors import ConfigError, IncompleteGradientSet, SequenceTooLong, ShapeMismatch, TokenOutOfRange
+from .kernels import AttentionMask, DropoutMask, EmbeddingConfig, LNCache, ReluMask, SoftmaxCache
+from .memplan import NullArena
+from .numerics import derive_seed, rand_uniform_array
+
+
+# ---------------------------------------------------------------------------
+# configuration and parameters (F/model.py:30-127)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ModelConfig:
+    n_enc: int = 2
+    n_dec: int = 2
+    d_model: int = 32
+    n_heads: int = 4
+    d_ff: int = 128
+    vocab: int = 32
+    max_len: int = 16
+    pre_ln: bool = True
+    tie_embeddings: bool = True
+    learned_positional: bool = True
+    eps: float = 1e-5
+    embed_scale: float | None = None
+
+    def __post_init__(self):
+        if self.d_model % self.n_heads:
+            raise ConfigError(f"d_model {self.d_model} not divisible by n_heads {self.n_heads}")
+        if self.vocab < 2:
+            raise ConfigError("vocab must be >= 2")
+        if not self.pre_ln:
+            raise ConfigError("only the pre-LayerNorm layout is implemented")
+
+    @property
+    def d_head(self) -> int:
+        return self.d_model // self.n_heads
+
+    @property
+    def scale(self) -> float:
+        return self.embed_scale if self.embed_scale is not None else math.sqrt(self.d_model)
+
+
+def _layer_spec(pre: str, d: int, dff: int, decoder: bool):
+    s = [(pre + "ln1.w", (d,)), (pre + "ln1.b", (d,)), (pre + "attn.wqkv", (3 * d, d)),
+         (pre + "attn.bqkv", (3 * d,)), (pre + "attn.wo", (d, d)), (pre + "attn.bo", (d,)),
+         (pre + "ln2.w", (d,)), (pre + "ln2.b", (d,))]
+    if decoder:
+        s += [(pre + "cross.wq", (d, d)), (pre + "cross.bq", (d,)), (pre + "cross.wo", (d, d)),
+              (pre + "cross.bo", (d,)), (pre + "ln3.w", (d,)), (pre + "ln3.b", (d,))]
+    return s + [(pre + "ffn.w1", (dff, d)), (pre + "ffn.b1", (dff,)), (pre + "ffn.w2", (d, dff)),
+                (pre + "ffn.b2", (d,))]
+
+
+def param_spec(cfg: ModelConfig):
+    """(name, shape) list; the order defines the workspace layout (F/model.py:82-97)."""
+    d, dff = cfg.d_model, cfg.d_ff
+    spec = [("tok_emb", (cfg.vocab, d))]
+    if cfg.learned_positional:
+        spec.append(("pos_emb", (cfg.max_len, d)))
+    for i in range(cfg.n_enc):
+        spec += _layer_spec(f"enc{i}.", d, dff, False)
+    spec += [("enc_ln.w", (d,)), ("enc_ln.b", (d,)),
+             ("cross_kv.w", (2 * cfg.n_dec * d, d)), ("cross_kv.b", (2 * cfg.n_dec * d,))]
+    for i in range(cfg.n_dec):
+        spec += _layer_spec(f"dec{i}.", d, dff, True)
+    spec += [("dec_ln.w", (d,)), ("dec_ln.b", (d,))]
+    if not cfg.tie_embeddings:
+        spec.append(("out_proj.w", (cfg.vocab, d)))
+    return spec
+
+
+def init_params(cfg: ModelConfig, seed: int, device=None) -> dict:
+    """Counter-RNG init on the device, bit-identical to F/model.py:100-118."""
+    ctx = _lib.context(device)
+    params = {}
+    for idx, (name, shape) in enumerate(param_spec(cfg)):
+        n = int(np.prod(shape))
+        leaf = name.rsplit(".", 1)[-1]
+        if leaf == "w" and "ln" in name:
+            params[name] = torch.ones(shape, dtype=torch.float32, device=ctx.device)
+        elif leaf in ("b", "bqkv", "bo", "bq", "b1", "b2"):
+            params[name] = torch.zeros(shape, dtype=torch.float32, device=ctx.device)
+        else:
+            u = rand_uniform_array(derive_seed(seed, idx), 0, n, device=ctx.device)
+            if "emb" in name or name == "out_proj.w":
+                lim = 0.02 * math.sqrt(3.0)
+            else:
+                fo, fi = (shape[0], shape[1]) if len(shape) == 2 else (shape[0], shape[0])
+                lim = math.sqrt(6.0 / (fi + fo))
+            params[name] = ((2.0 * u - 1.0) * lim).to(torch.float32).reshape(shape)
+    return params
+
+
+def sinusoidal_table(max_len: int, d: int, dtype=torch.float32, device=None) -> torch.Tensor:
+    """Fixed positional table (F/model.py:121-127), built in float64 then cast."""
+    pos = np.arange(max_len, dtype=np.float64)[:, None]
+    j = np.arange(d, dtype=np.float64)[None, :]
+    ang = pos / np.power(10000.0, 2.0 * np.floor(j / 2.0) / d)
+    tab = np.where(j % 2 == 0, np.sin(ang), np.cos(ang))
+    return torch.from_numpy(tab).to(device or _lib.context().device).to(dtype)
+
+
+# ---------------------------------------------------------------------------
+# layer weight views (F/model.py:134-172)
+# ---------------------------------------------------------------------------
+
+_ENC_FIELDS = [("ln1_w", "ln1.w"), ("ln1_b", "ln1.b"), ("wqkv", "attn.wqkv"), ("bqkv", "attn.bqkv"),
+               ("wo", "attn.wo"), ("bo", "attn.bo"), ("ln2_w", "ln2.w"), ("ln2_b", "ln2.b"),
+               ("w1", "ffn.w1"), ("b1", "ffn.b1"), ("w2", "ffn.w2"), ("b2", "ffn.b2")]
+_DEC_EXTRA = [("cross_wq", "cross.wq"), ("cross_bq", "cross.bq"), ("cross_wo", "cross.wo"),
+              ("cross_bo", "cross.bo"), ("ln3_w", "ln3.w"), ("ln3_b", "ln3.b")]
+
+
+class EncoderLayerWeights:
+    _fields = _ENC_FIELDS
+
+    def __init__(self, **kw):
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+    @classmethod
+    def from_params(cls, params, prefix: str):
+        return cls(**{attr: params[prefix + key] for attr, key in cls._fields})
+
+
+class DecoderLayerWeights(EncoderLayerWeights):
+    _fields = _ENC_FIELDS + _DEC_EXTRA
+
+
+# ---------------------------------------------------------------------------
+# packed cross-attention K/V projection (F/model.py:179-260)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class PackedCrossWeights:
+    """[Wkey_0; ..; Wkey_{n-1}; Wval_0; ..; Wval_{n-1}]  ([2*n*d, d])."""
+
+    w: torch.Tensor
+    b: torch.Tensor
+    n_layers: int
+    d: int
+
+    def key_slice(self, i: int):
+        return self.w[i * self.d:(i + 1) * self.d]
+
+    def value_slice(self, i: int):
+        return self.w[(self.n_layers + i) * self.d:(self.n_layers + i + 1) * self.d]
+
+
+def pack_cross_weights(keys, values, key_biases, value_biases) -> PackedCrossWeights:
+    n = len(keys)
+    if n < 1 or len(values) != n or len(key_biases) != n or len(value_biases) != n:
+        raise ShapeMismatch("need matching, non-empty key/value weight lists")
+    ks = [K.dev(m) for m in keys]
+    vs = [K.dev(m) for m in values]
+    d = ks[0].shape[1]
+    for m in ks + vs:
+        if tuple(m.shape) != (d, d):
+            raise ShapeMismatch(f"cross projection must be [{d}x{d}], got {tuple(m.shape)}")
+    w = torch.cat(ks + vs, dim=0)
+    b = torch.cat([K.dev(v).reshape(-1) for v in list(key_biases) + list(value_biases)])
+    return PackedCrossWeights(w=w, b=b, n_layers=n, d=d)
+
+
+def unpack_cross_weights(pw: PackedCrossWeights):
+    n, d = pw.n_layers, pw.d
+    keys = [pw.key_slice(i).clone() for i in range(n)]
+    values = [pw.value_slice(i).clone() for i in range(n)]
+    kb = [pw.b[i * d:(i + 1) * d].clone() for i in range(n)]
+    vb = [pw.b[(n + i) * d:(n + i + 1) * d].clone() for i in range(n)]
+    return keys, values, kb, vb
+
+
+def _as_dt(t, dt):
+    t = t if isinstance(t, torch.Tensor) else K.dev(t)
+    return t if t.dtype == dt else t.to(dt)
+
+
+def _linear(x2d, w, b, out2d):
+    """out = x @ w^T (+ b) on cuBLAS; bias added in place by libls2."""
+    K.gemm(x2d, _as_dt(w, out2d.dtype), trans_b=True, out=out2d)
+    if b is not None:
+        bb = _as_dt(b, out2d.dtype).contiguous()
+        _lib.call("ls2_bias_add", out2d.data_ptr(), bb.data_ptr(), out2d.shape[0],
+                  out2d.shape[1], _lib.dtype_code(out2d), _lib.stream_handle())
+    return out2d
+
+
+def packed_kv_forward(enc_out, pw: PackedCrossWeights, arena=None):
+    """One GEMM of enc_out against the packed weights, then a 2n-way view split."""
+    arena = arena or NullArena()
+    enc_out = enc_out if isinstance(enc_out, torch.Tensor) else K.dev(enc_out)
+    if enc_out.shape[-1] != pw.d:
+        raise ShapeMismatch(f"enc_out feature dim {enc_out.shape[-1]} != {pw.d}")
+    b, ls, d = enc_out.shape
+    n = pw.n_layers
+    if enc_out.dtype in (torch.float16, torch.bfloat16):
+        dt = enc_out.dtype                       # storage dtype of the training path
+    else:
+        dt = K.compute_dtype(enc_out, pw.w)      # reference dtype rule
+    buf = arena.alloc((b, ls, 2 * n * d), dt)
+    _linear(_as_dt(enc_out, dt).reshape(b * ls, d), pw.w, pw.b, buf.view(b * ls, 2 * n * d))
+    pairs = [(buf[..., i * d:(i + 1) * d], buf[..., (n + i) * d:(n + i + 1) * d]) for i in range(n)]
+    return pairs, buf
+
+
+def packed_kv_backward(dks, dvs, enc_out, pw: PackedCrossWeights, arena=None, packed=None,
+                       sink=None):
+    """dx = sum_i Wkey_i^T dK_i + Wval_i^T dV_i via one packed GEMM; (dx, dw, db).
+
+    Raises IncompleteGradientSet unless every decoder layer contributed.  When
+    the dK_i/dV_i are already views of one packed buffer (`packed`), no copy is
+    made.  With a sink the weight/bias grads go straight into it (dw, db None)."""
+    arena = arena or NullArena()
+    n = pw.n_layers
+    if len(dks) != n or len(dvs) != n or any(g is None for g in dks) or any(g is None for g in dvs):
+        raise IncompleteGradientSet("missing dK/dV contribution for some decoder layer")
+    enc_out = enc_out if isinstance(enc_out, torch.Tensor) else K.dev(enc_out)
+    b, ls, d = enc_out.shape
+    dt = dks[0].dtype if isinstance(dks[0], torch.Tensor) else K.compute_dtype(enc_out, dks[0])
+    own = packed is None
+    if own:
+        dy = arena.alloc((b, ls, 2 * n * d), dt)
+        for i in range(n):
+            dy[..., i * d:(i + 1) * d].copy_(K.dev(dks[i]).view(b, ls, d))
+            dy[..., (n + i) * d:(n + i + 1) * d].copy_(K.dev(dvs[i]).view(b, ls, d))
+    else:
+        dy = packed
+    dy2 = dy.view(b * ls, 2 * n * d)
+    dx = arena.alloc((b, ls, d), dt)
+    K.gemm(dy2, _as_dt(pw.w, dt), out=dx.view(b * ls, d))
+    e2 = _as_dt(enc_out, dt).reshape(b * ls, d)
+    dw = db = None
+    if sink is not None:
+        _wgrad(sink, "cross_kv.w", dy2, e2)
+        _colsum_grad(sink, "cross_kv.b", dy2)
+    else:
+        dw = K.gemm(dy2, e2, trans_a=True)
+        db = G.column_sum(dy2)
+    if own:
+        arena.free(dy)
+    return dx, dw, db
+
+
+# ---------------------------------------------------------------------------
+# activation stash and gradient sinks (F/model.py:267-311)
+# ---------------------------------------------------------------------------
+
+class ActivationStash:
+    """LIFO store of saved activations; every entry is consumed exactly once."""
+
+    def __init__(self):
+        self._items: list = []
+
+    def push(self, tag: str, value):
+        self._items.append((tag, value))
+
+    def pop(self, tag: str):
+        if not self._items:
+            raise ShapeMismatch(f"stash empty, wanted {tag!r}")
+        got, value = self._items.pop()
+        if got != tag:
+            raise ShapeMismatch(f"stash order broken: wanted {tag!r}, top is {got!r}")
+        return value
+
+    def drain(self, arena):
+        while self._items:
+            _, value = self._items.pop()
+            if isinstance(value, torch.Tensor):
+                arena.free(value)
+
+    def __len__(self):
+        return len(self._items)
+
+
+class GradSink:
+    """Accumulates named parameter gradients (dict-backed by default)."""
+
+    def __init__(self, store: dict | None = None):
+        self.store = store if store is not None else {}
+
+    def add(self, name: str, value):
+        if name in self.store:
+            self.store[name] += value
+        else:
+            self.store[name] = value.clone()
+
+    def target(self, name: str):
+        """(view, beta) to write a gradient in place, or None to use add()."""
+        return None
+
+
+class _ViewSink(GradSink):
+    """Writes into preallocated views of the fp32 gradient workspace; the first
+    producer of a name overwrites (beta=0), later producers accumulate."""
+
+    def __init__(self, store: dict):
+        super().__init__(store)
+        self.written: set = set()
+
+    def add(self, name: str, value):
+        if name in self.written:
+            self.store[name] += value
+        else:
+            self.store[name].copy_(value)
+            self.written.add(name)
+
+    def target(self, name: str):
+        beta = 1 if name in self.written else 0
+        self.written.add(name)
+        return self.store[name], beta
+
+
+def _wgrad(sink, name, dy2d, x2d):
+    """dW = dy^T x straight into the sink (cuBLAS, fp32 output)."""
+    tgt = sink.target(name)
+    if tgt is None:
+        sink.add(name, K.gemm(dy2d, x2d, trans_a=True))
+    else:
+        v, beta = tgt
+        K.gemm(dy2d, x2d, trans_a=True, out=v.view(dy2d.shape[1], x2d.shape[1]), beta=float(beta))
+
+
+def _colsum_grad(sink, name, x2d):
+    tgt = sink.target(name)
+    if tgt is None:
+        sink.add(name, G.column_sum(x2d))
+    else:
+        v, beta = tgt
+        G.column_sum(x2d, out=v, beta=beta)
+
+
+def _bias_target(sink, name):
+    tgt = sink.target(name)
+    return (None, 0, False) if tgt is None else (tgt[0], tgt[1], True)
+
+
+def _ln_targets(sink, pp, ln):
+    tw, tb = sink.target(pp + ln + ".w"), sink.target(pp + ln + ".b")
+    if tw is None or tb is None or tw[1] != tb[1]:
+        return None, None, 0
+    return tw[0], tb[0], tw[1]
+
+
+def _ln_bwd(sink, pp, ln, du, x_in, w, mu, sg, out, dres):
+    dwv, dbv, beta = _ln_targets(sink, pp, ln)
+    _, dw, db = G.layernorm_backward(du, x_in, _as_dt(w, du.dtype), LNCache(mu, sg), out=out,
+                                     dres=dres, dw_out=dwv, db_out=dbv, beta=beta)
+    if dwv is None:
+        sink.add(pp + ln + ".w", dw)
+        sink.add(pp + ln + ".b", db)
+
+
+def _bdr_bwd(sink, name, dy, keep_bits, p_drop, out):
+    dv, beta, direct = _bias_target(sink, name)
+    _, db, _ = G.bias_dropout_residual_backward(
+        dy, DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dy.shape)), out=out,
+        dbias_out=dv, beta=beta)
+    if not direct:
+        sink.add(name, db)
+
+
+def _brd_bwd(sink, name, dz, keep_bits, relu_bits, p_drop, out):
+    dv, beta, direct = _bias_target(sink, name)
+    _, db = G.bias_relu_dropout_backward(
+        dz, DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dz.shape)),
+        ReluMask(bits=relu_bits, shape=tuple(dz.shape)), out=out, dbias_out=dv, beta=beta)
+    if not direct:
+        sink.add(name, db)
+
+
+# ---------------------------------------------------------------------------
+# attention helpers (F/model.py:318-328) — views, never copies
+# ---------------------------------------------------------------------------
+
+def _heads(x, n_heads: int):
+    """[B, L, d] -> [B, N, L, d/N] strided view."""
+    b, l, d = x.shape
+    return x.view(b, l, n_heads, d // n_heads).transpose(1, 2) if x.is_contiguous() else \
+        x.unflatten(-1, (n_heads, d // n_heads)).transpose(1, 2)
+
+
+def _merge_heads(xh, out):
+    """[B, N, L, hd] -> [B, L, d] copy into out (API helper; the model writes
+    attention contexts directly in merged layout)."""
+    b, n, l, hd = xh.shape
+    out.view(b, l, n, hd).copy_(xh.transpose(1, 2))
+    return out
+
+
+def _qkv_heads(qkv, n_heads: int):
+    d = qkv.shape[-1] // 3
+    return tuple(_heads(qkv[..., i * d:(i + 1) * d], n_heads) for i in range(3))
+
+
+class SeedTable:
+    """Per-step dropout seeds on the device (one H2D copy per step).
+
+    slot(group_base, site, k) -> 1-element uint64 CUDA view holding
+    derive_seed(group_base, site, k); kernels read it through seed_ptr."""
+
+    def __init__(self, device, capacity: int = 256):
+        self.host = torch.zeros(capacity, dtype=torch.int64).pin_memory()
+        self.dev = torch.zeros(capacity, dtype=torch.int64, device=device)
+        self.index: dict = {}
+        self.values: list = []
+        self._evt = None
+
+    def reset(self):
+        self.index.clear()
+        self.values.clear()
+
+    def slot(self, base: int, *tags: int):
+        key = (base,) + tags
+        i = self.index.get(key)
+        if i is None:
+            i = self.index[key] = len(self.values)
+            self.values.append(derive_seed(base, *tags) if tags else base)
+        return self.dev[i:i + 1]
+
+    def upload(self):
+        n = len(self.values)
+        if n > self.host.numel():
+            raise ShapeMismatch("seed table overflow")
+        self.write_host()
+        self.dev[:n].copy_(self.host[:n], non_blocking=True)
+        if not torch.cuda.is_current_stream_capturing():
+            self._evt = torch.cuda.Event()
+            self._evt.record()
+
+    def write_host(self):
+        """Fill the pinned staging buffer (waits until the previous copy ran)."""
+        if self._evt is not None:
+            self._evt.synchronize()
+        n = len(self.values)
+        vals = np.array([v - (1 << 64) if v >= (1 << 63) else v for v in self.values], dtype=np.int64)
+        self.host[:n].copy_(torch.from_numpy(vals))
+
+
+class _LayerSeed:
+    """Seed handle handed to a layer: int (reference API) or table-backed."""
+
+    def __init__(self, table: SeedTable, base: int):
+        self.table, self.base = table, base
+
+    def site(self, site: int, k: int):
+        return self.table.slot(self.base, site, k)
+
+
+def _site_seed(seed, site: int, k: int):
+    if isinstance(seed, _LayerSeed):
+        return seed.site(site, k)
+    return derive_seed(seed, site, k)
+
+
+def _stat_dtype(dt):
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+def _nbits(n: int) -> int:
+    return (n + 7) // 8
+
+
+# ---------------------------------------------------------------------------
+# encoder layer (F/model.py:335-510)
+# ---------------------------------------------------------------------------
+
+def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, p):
+    b, l, d = x.shape
+    r, dt, hd = b * l, x.dtype, d // n_heads
+    sdt = _stat_dtype(dt)
+    stash.push(p + "x_in", x)
+    mu1, sg1 = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
+    u1 = arena.alloc((b, l, d), dt)
+    K.layernorm_forward(x, _as_dt(w.ln1_w, dt), _as_dt(w.ln1_b, dt), eps, out=u1, mu_out=mu1,
+                        sigma_out=sg1, check_degenerate=False)
+    stash.push(p + "mu1", mu1); stash.push(p + "sg1", sg1); stash.push(p + "u1", u1)
+    qkv = arena.alloc((b, l, 3 * d), dt)
+    _linear(u1.view(r, d), w.wqkv, w.bqkv, qkv.view(r, 3 * d))
+    stash.push(p + "qkv", qkv)
+    qh, kh, vh = _qkv_heads(qkv, n_heads)
+    scores = arena.alloc((b, n_heads, l, l), dt)
+    K.gemm(qh, kh, trans_b=True, out=scores, alpha=1.0 / math.sqrt(hd))
+    K.softmax_forward(scores, mask=mask, out=scores)
+    stash.push(p + "probs", scores)
+    ctxm = arena.alloc((b, l, d), dt)
+    K.gemm(scores, vh, out=_heads(ctxm, n_heads))
+    stash.push(p + "ctxm", ctxm)
+    proj = arena.alloc((b, l, d), dt)
+    _linear(ctxm.view(r, d), w.wo, None, proj.view(r, d))
+    y1 = arena.alloc((b, l, d), dt)
+    keep1 = arena.alloc((_nbits(r * d),), torch.uint8)
+    K.bias_dropout_residual(proj, _as_dt(w.bo, dt), x, p_drop, _site_seed(seed, site, 0),
+                            out=y1, bits_out=keep1)
+    arena.free(proj)
+    stash.push(p + "keep1", keep1); stash.push(p + "y1", y1)
+    return y1
+
+
+def _ffn_fwd(y_in, w, ln_w, ln_b, p_drop, seed, site, k_relu, k_tail, eps, arena, stash, p, ln):
+    b, l, d = y_in.shape
+    r, dt = b * l, y_in.dtype
+    sdt = _stat_dtype(dt)
+    dff = w.w1.shape[0]
+    mu, sg = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
+    u = arena.alloc((b, l, d), dt)
+    K.layernorm_forward(y_in, _as_dt(ln_w, dt), _as_dt(ln_b, dt), eps, out=u, mu_out=mu,
+                        sigma_out=sg, check_degenerate=False)
+    stash.push(p + "mu" + ln, mu); stash.push(p + "sg" + ln, sg); stash.push(p + "u" + ln, u)
+    a1 = arena.alloc((b, l, dff), dt)
+    _linear(u.view(r, d), w.w1, None, a1.view(r, dff))
+    z = arena.alloc((b, l, dff), dt)
+    keep_r = arena.alloc((_nbits(r * dff),), torch.uint8)
+    relum = arena.alloc((_nbits(r * dff),), torch.uint8)
+    K.bias_relu_dropout(a1, _as_dt(w.b1, dt), p_drop, _site_seed(seed, site, k_relu), out=z,
+                        bits_out=keep_r, relu_bits_out=relum)
+    arena.free(a1)
+    stash.push(p + "keepr", keep_r); stash.push(p + "relum", relum); stash.push(p + "z", z)
+    f = arena.alloc((b, l, d), dt)
+    _linear(z.view(r, dff), w.w2, None, f.view(r, d))
+    y2 = arena.alloc((b, l, d), dt)
+    keep_t = arena.alloc((_nbits(r * d),), torch.uint8)
+    K.bias_dropout_residual(f, _as_dt(w.b2, dt), y_in, p_drop, _site_seed(seed, site, k_tail),
+                            out=y2, bits_out=keep_t)
+    arena.free(f)
+    stash.push(p + "keept", keep_t)
+    return y2
+
+
+def encoder_layer_forward(x, w: EncoderLayerWeights, mask, p_drop, seed, *, n_heads, eps=1e-5,
+                          arena=None, stash=None, prefix="", site=0, strategy=None):
+    """One pre-LN encoder layer; returns (y, stash).  x moves into the stash."""
+    arena = arena or NullArena()
+    stash = stash if stash is not None else ActivationStash()
+    x = x if isinstance(x, torch.Tensor) else K.dev(x)
+    y1 = _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, prefix)
+    y2 = _ffn_fwd(y1, w, w.ln2_w, w.ln2_b, p_drop, seed, site, 1, 2, eps, arena, stash, prefix, "2")
+    return y2, stash
+
+
+def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag):
+    b, l, d = dy.shape
+    r, dt = b * l, dy.dtype
+    dff = w.w1.shape[0]
+    keep_t = stash.pop(p + "keept")
+    z = stash.pop(p + "z")
+    relum = stash.pop(p + "relum")
+    keep_r = stash.pop(p + "keepr")
+    u = stash.pop(p + "u" + ln)
+    sg = stash.pop(p + "sg" + ln)
+    mu = stash.pop(p + "mu" + ln)
+    y_in = stash.pop(p + y_in_tag)
+    df = arena.alloc((b, l, d), dt)
+    _bdr_bwd(sink, pp + "ffn.b2", dy, keep_t, p_drop, df)
+    arena.free(keep_t)
+    dz = arena.alloc((b, l, dff), dt)
+    K.gemm(df.view(r, d), _as_dt(w.w2, dt), out=dz.view(r, dff))
+    _wgrad(sink, pp + "ffn.w2", df.view(r, d), z.view(r, dff))
+    arena.free(z); arena.free(df)
+    da1 = arena.alloc((b, l, dff), dt)
+    _brd_bwd(sink, pp + "ffn.b1", dz, keep_r, relum, p_drop, da1)
+    arena.free(dz); arena.free(relum); arena.free(keep_r)
+    du = arena.alloc((b, l, d), dt)
+    K.gemm(da1.view(r, dff), _as_dt(w.w1, dt), out=du.view(r, d))
+    _wgrad(sink, pp + "ffn.w1", da1.view(r, dff), u.view(r, d))
+    arena.free(da1); arena.free(u)
+    dyo = arena.alloc((b, l, d), dt)
+    _ln_bwd(sink, pp, "ln" + ln, du, y_in, getattr(w, f"ln{ln}_w"), mu, sg, dyo, dy)
+    arena.free(du); arena.free(mu); arena.free(sg); arena.free(y_in)
+    arena.free(dy)
+    return dyo
+
+
+def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp):
+    b, l, d = dy1.shape
+    r, dt, hd = b * l, dy1.dtype, d // n_heads
+    keep1 = stash.pop(p + "keep1")
+    ctxm = stash.pop(p + "ctxm")
+    probs = stash.pop(p + "probs")
+    qkv = stash.pop(p + "qkv")
+    u1 = stash.pop(p + "u1")
+    sg1 = stash.pop(p + "sg1")
+    mu1 = stash.pop(p + "mu1")
+    x_in = stash.pop(p + "x_in")
+    dproj = arena.alloc((b, l, d), dt)
+    _bdr_bwd(sink, pp + "attn.bo", dy1, keep1, p_drop, dproj)
+    arena.free(keep1)
+    dctxm = arena.alloc((b, l, d), dt)
+    K.gemm(dproj.view(r, d), _as_dt(w.wo, dt), out=dctxm.view(r, d))
+    _wgrad(sink, pp + "attn.wo", dproj.view(r, d), ctxm.view(r, d))
+    arena.free(dproj); arena.free(ctxm)
+    dctx = _heads(dctxm, n_heads)
+    qh, kh, vh = _qkv_heads(qkv, n_heads)
+    dscores = arena.alloc((b, n_heads, l, l), dt)
+    K.gemm(dctx, vh, trans_b=True, out=dscores)
+    G.softmax_backward(dscores, SoftmaxCache(probs), out=dscores, out_scale=1.0 / math.sqrt(hd))
+    dqkv = arena.alloc((b, l, 3 * d), dt)
+    dq, dk, dv = _qkv_heads(dqkv, n_heads)
+    K.gemm(dscores, kh, out=dq)
+    K.gemm(dscores, qh, trans_a=True, out=dk)
+    K.gemm(probs, dctx, trans_a=True, out=dv)
+    arena.free(dscores); arena.free(probs); arena.free(dctxm); arena.free(qkv)
+    du1 = arena.alloc((b, l, d), dt)
+    K.gemm(dqkv.view(r, 3 * d), _as_dt(w.wqkv, dt), out=du1.view(r, d))
+    _wgrad(sink, pp + "attn.wqkv", dqkv.view(r, 3 * d), u1.view(r, d))
+    _colsum_grad(sink, pp + "attn.bqkv", dqkv.view(r, 3 * d))
+    arena.free(dqkv); arena.free(u1)
+    dx = arena.alloc((b, l, d), dt)
+    _ln_bwd(sink, pp, "ln1", du1, x_in, w.ln1_w, mu1, sg1, dx, dy1)
+    arena.free(du1); arena.free(mu1); arena.free(sg1); arena.free(x_in)
+    arena.free(dy1)
+    return dx
+
+
+def encoder_layer_backward(dy, w: EncoderLayerWeights, stash: ActivationStash, sink: GradSink, *,
+                           n_heads, p_drop, arena=None, prefix="", param_prefix=""):
+    """Backward of one encoder layer. Takes ownership of dy, returns dx."""
+    arena = arena or NullArena()
+    dy = dy if isinstance(dy, torch.Tensor) else K.dev(dy)
+    dy1 = _ffn_bwd(dy, w, stash, sink, p_drop, arena, prefix, param_prefix, "2", "y1")
+    return _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, prefix, param_prefix)
+
+
+# ---------------------------------------------------------------------------
+# decoder layer (F/model.py:517-775)
+# ---------------------------------------------------------------------------
+
+def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, p_drop, seed, *,
+                          n_heads, eps=1e-5, arena=None, stash=None, prefix="", site=0,
+                          strategy=None):
+    """One pre-LN decoder layer consuming precomputed (K_i, V_i)."""
+    arena = arena or NullArena()
+    stash = stash if stash is not None else ActivationStash()
+    x = x if isinstance(x, torch.Tensor) else K.dev(x)
+    k_i, v_i = kv
+    b, l, d = x.shape
+    r, dt, hd = b * l, x.dtype, d // n_heads
+    ls = k_i.shape[1]
+    sdt = _stat_dtype(dt)
+    p = prefix
+    y1 = _self_attention_fwd(x, w, self_mask, p_drop, seed, site, n_heads, eps, arena, stash, p)
+    mu2, sg2 = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
+    u2 = arena.alloc((b, l, d), dt)
+    K.layernorm_forward(y1, _as_dt(w.ln2_w, dt), _as_dt(w.ln2_b, dt), eps, out=u2, mu_out=mu2,
+                        sigma_out=sg2, check_degenerate=False)
+    stash.push(p + "mu2", mu2); stash.push(p + "sg2", sg2); stash.push(p + "u2", u2)
+    qc = arena.alloc((b, l, d), dt)
+    _linear(u2.view(r, d), w.cross_wq, w.cross_bq, qc.view(r, d))
+    stash.push(p + "qc", qc)
+    scores_x = arena.alloc((b, n_heads, l, ls), dt)
+    K.gemm(_heads(qc, n_heads), _heads(_as_dt(k_i, dt), n_heads), trans_b=True, out=scores_x,
+           alpha=1.0 / math.sqrt(hd))
+    K.softmax_forward(scores_x, mask=cross_mask, out=scores_x)
+    stash.push(p + "probs_x", scores_x)
+    ctxm_x = arena.alloc((b, l, d), dt)
+    K.gemm(scores_x, _heads(_as_dt(v_i, dt), n_heads), out=_heads(ctxm_x, n_heads))
+    stash.push(p + "ctxm_x", ctxm_x)
+    proj_x = arena.alloc((b, l, d), dt)
+    _linear(ctxm_x.view(r, d), w.cross_wo, None, proj_x.view(r, d))
+    y2 = arena.alloc((b, l, d), dt)
+    keep2 = arena.alloc((_nbits(r * d),), torch.uint8)
+    K.bias_dropout_residual(proj_x, _as_dt(w.cross_bo, dt), y1, p_drop, _site_seed(seed, site, 1),
+                            out=y2, bits_out=keep2)
+    arena.free(proj_x)
+    stash.push(p + "keep2", keep2); stash.push(p + "y2", y2)
+    y3 = _ffn_fwd(y2, w, w.ln3_w, w.ln3_b, p_drop, seed, site, 2, 3, eps, arena, stash, p, "3")
+    return y3, stash
+
+
+def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStash, sink: GradSink,
+                           *, n_heads, p_drop, arena=None, prefix="", param_prefix="",
+                           dkv_out=None):
+    """Backward of one decoder layer; returns (dx, dK_i, dV_i).
+
+    dkv_out: optional (dK_i, dV_i) destination views (slices of the packed
+    cross-K/V gradient buffer) so packed_kv_backward needs no gather copy."""
+    arena = arena or NullArena()
+    dy = dy if isinstance(dy, torch.Tensor) else K.dev(dy)
+    k_i, v_i = kv
+    b, l, d = dy.shape
+    r, dt, hd = b * l, dy.dtype, d // n_heads
+    ls = k_i.shape[1]
+    p, pp = prefix, param_prefix
+    dy2 = _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, "3", "y2")
+    keep2 = stash.pop(p + "keep2")
+    ctxm_x = stash.pop(p + "ctxm_x")
+    probs_x = stash.pop(p + "probs_x")
+    qc = stash.pop(p + "qc")
+    u2 = stash.pop(p + "u2")
+    sg2 = stash.pop(p + "sg2")
+    mu2 = stash.pop(p + "mu2")
+    dproj_x = arena.alloc((b, l, d), dt)
+    _bdr_bwd(sink, pp + "cross.bo", dy2, keep2, p_drop, dproj_x)
+    arena.free(keep2)
+    dctxm_x = arena.alloc((b, l, d), dt)
+    K.gemm(dproj_x.view(r, d), _as_dt(w.cross_wo, dt), out=dctxm_x.view(r, d))
+    _wgrad(sink, pp + "cross.wo", dproj_x.view(r, d), ctxm_x.view(r, d))
+    arena.free(dproj_x); arena.free(ctxm_x)
+    dctx_x = _heads(dctxm_x, n_heads)
+    kh, vh = _heads(_as_dt(k_i, dt), n_heads), _heads(_as_dt(v_i, dt), n_heads)
+    dscores_x = arena.alloc((b, n_heads, l, ls), dt)
+    K.gemm(dctx_x, vh, trans_b=True, out=dscores_x)
+    G.softmax_backward(dscores_x, SoftmaxCache(probs_x), out=dscores_x,
+                       out_scale=1.0 / math.sqrt(hd))
+    dqc = arena.alloc((b, l, d), dt)
+    K.gemm(dscores_x, kh, out=_heads(dqc, n_heads))
+    if dkv_out is not None:
+        dk_i, dv_i = dkv_out
+    else:
+        dk_i, dv_i = arena.alloc((b, ls, d), dt), arena.alloc((b, ls, d), dt)
+    K.gemm(dscores_x, _heads(qc, n_heads), trans_a=True, out=_heads(dk_i, n_heads))
+    K.gemm(probs_x, dctx_x, trans_a=True, out=_heads(dv_i, n_heads))
+    arena.free(dscores_x); arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
+    du2 = arena.alloc((b, l, d), dt)
+    K.gemm(dqc.view(r, d), _as_dt(w.cross_wq, dt), out=du2.view(r, d))
+    _wgrad(sink, pp + "cross.wq", dqc.view(r, d), u2.view(r, d))
+    _colsum_grad(sink, pp + "cross.bq", dqc.view(r, d))
+    arena.free(dqc); arena.free(u2)
+    y1 = stash.pop(p + "y1")
+    dy1 = arena.alloc((b, l, d), dt)
+    _ln_bwd(sink, pp, "ln2", du2, y1, w.ln2_w, mu2, sg2, dy1, dy2)
+    arena.free(du2); arena.free(mu2); arena.free(sg2); arena.free(y1)
+    arena.free(dy2)
+    dx = _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp)
+    return dx, dk_i, dv_i
+
+
+# ---------------------------------------------------------------------------
+# full model (F/model.py:782-1003)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Batch:
+    src: object
+    tgt_in: object
+    tgt_out: object
+    src_len: object
+    pad_id: int = 0
+
+
+class ModelOutput:
+    """(loss_sum, token_count, correct); device-resident until first read."""
+
+    def __init__(self, out3: torch.Tensor):
+        self.out3 = out3
+        self._host = None
+
+    def _h(self):
+        if self._host is None:
+            self._host = self.out3.detach().cpu().numpy()
+        return self._host
+
+    @property
+    def loss_sum(self) -> float:
+        return float(self._h()[0])
+
+    @property
+    def token_count(self) -> int:
+        return int(self._h()[1])
+
+    @property
+    def correct(self) -> int:
+        return int(self._h()[2])
+
+    @property
+    def loss_per_token(self) -> float:
+        return self.loss_sum / max(self.token_count, 1)
+
+    @property
+    def accuracy(self) -> float:
+        return self.correct / max(self.token_count, 1)
+
+
+def validate_batch(batch: Batch, cfg: ModelConfig):
+    """Host-side checks the reference raises before compute."""
+    src = np.asarray(batch.src)
+    tin = np.asarray(batch.tgt_in)
+    tout = np.asarray(batch.tgt_out)
+    lens = np.asarray(batch.src_len)
+    for name, t in (("src", src), ("tgt_in", tin)):
+        if t.ndim != 2:
+            raise ShapeMismatch(f"{name} must be [B, L]")
+        if t.shape[1] > cfg.max_len:
+            raise SequenceTooLong(f"sequence length {t.shape[1]} > max_len {cfg.max_len}")
+        if t.size and (t.min() < 0 or t.max() >= cfg.vocab):
+            raise TokenOutOfRange(f"token ids outside [0, {cfg.vocab})")
+    valid = tout[tout != batch.pad_id]
+    if valid.size and (valid.min() < 0 or valid.max() >= cfg.vocab):
+        raise TokenOutOfRange(f"target outside [0, {cfg.vocab})")
+    if lens.min() < 1 or lens.max() > src.shape[1]:
+        raise ShapeMismatch("padding valid length outside [1, Lk]")
+
+
+class Transformer:
+    """Fused-graph encoder-decoder with a hand-wired forward/backward."""
+
+    def __init__(self, cfg: ModelConfig, compute_dtype: torch.dtype | None = None):
+        self.cfg = cfg
+        self.param_names = [name for name, _ in param_spec(cfg)]
+        self.compute_dtype = compute_dtype
+        self._sin = None
+        self._seeds: SeedTable | None = None
+
+    def param_spec(self):
+        return param_spec(self.cfg)
+
+    def init_params(self, seed: int):
+        return init_params(self.cfg, seed)
+
+    def _positional(self, params, dtype):
+        if self.cfg.learned_positional:
+            return params["pos_emb"]
+        if self._sin is None or self._sin.dtype != dtype:
+            self._sin = sinusoidal_table(self.cfg.max_len, self.cfg.d_model, dtype)
+        return self._sin
+
+    def packed_weights(self, params) -> PackedCrossWeights:
+        return PackedCrossWeights(w=params["cross_kv.w"], b=params["cross_kv.b"],
+                                  n_layers=self.cfg.n_dec, d=self.cfg.d_model)
+
+    def act_dtype(self, params) -> torch.dtype:
+        if self.compute_dtype is not None:
+            return self.compute_dtype
+        dt = params["tok_emb"].dtype if isinstance(params["tok_emb"], torch.Tensor) else \
+            K.compute_dtype(params["tok_emb"])
+        return dt if dt in (torch.float16, torch.bfloat16, torch.float32, torch.float64) else torch.float32
+
+    def seed_table(self, device) -> SeedTable:
+        if self._seeds is None:
+            self._seeds = SeedTable(device)
+        return self._seeds
+
+    def forward_backward(self, params, batch: Batch, *, p_drop=0.0, alpha=0.0, seed=0, step=0,
+                         arena=None, sink: GradSink | None = None, compute_grads=True,
+                         grad_scale=1.0, trace=None, strategy=None, capture: dict | None = None,
+                         validate: bool = True, upload_seeds: bool = True) -> ModelOutput:
+        """Run one batch end to end; gradients go into `sink`.
+
+        grad_scale multiplies the criterion gradient.  compute_grads=False is a
+        pure forward (evaluation).  capture receives "logq" (debug hook)."""
+        cfg = self.cfg
+        ctx = _lib.context()
+        arena = arena or NullArena(ctx.device)
+        stash = ActivationStash()
+        sink = GradSink() if sink is None else sink
+        emit = trace.append if trace is not None else (lambda ev: None)
+        if validate:
+            validate_batch(batch, cfg)
+        src = K.dev(batch.src, torch.int64)
+        tgt_in = K.dev(batch.tgt_in, torch.int64)
+        tgt_out = K.dev(batch.tgt_out, torch.int64).reshape(-1)
+        src_len = K.dev(batch.src_len, torch.int64)
+        b, ls = src.shape
+        lt = tgt_in.shape[1]
+        d, n, v = cfg.d_model, cfg.n_heads, cfg.vocab
+        params = {k: (t if isinstance(t, torch.Tensor) else K.dev(t)) for k, t in params.items()}
+        dt = self.act_dtype(params)
+        sdt = _stat_dtype(dt)
+        emb_cfg = EmbeddingConfig(scale=cfg.scale, vocab=v, max_len=cfg.max_len,
+                                  learned_positional=cfg.learned_positional)
+        tok_emb = _as_dt(params["tok_emb"], dt)
+        pos = _as_dt(self._positional(params, dt), dt)
+        enc_mask = AttentionMask("padding", src_len)
+        dec_mask = AttentionMask("causal")
+        cross_mask = AttentionMask("padding", src_len)
+
+        seeds = self.seed_table(ctx.device)
+        seeds.reset()
+        s_src = seeds.slot(derive_seed(seed, step, 0))
+        enc_seed = _LayerSeed(seeds, derive_seed(seed, step, 1))
+        s_tgt = seeds.slot(derive_seed(seed, step, 2))
+        dec_seed = _LayerSeed(seeds, derive_seed(seed, step, 3))
+        if p_drop > 0.0:
+            for i in range(cfg.n_enc):
+                for k in range(3):
+                    enc_seed.site(i, k)
+            for i in range(cfg.n_dec):
+                for k in range(4):
+                    dec_seed.site(i, k)
+            if upload_seeds:
+                seeds.upload()
+
+        # --- forward: encoder ---
+        h = arena.alloc((b, ls, d), dt)
+        keep_src = arena.alloc((_nbits(b * ls * d),), torch.uint8)
+        K.embedding_forward(tok_emb, pos, src, emb_cfg, p_drop, s_src, out=h, bits_out=keep_src,
+                            validate=False)
+        stash.push("src_keep", keep_src)
+        enc_w = [EncoderLayerWeights.from_params(params, f"enc{i}.") for i in range(cfg.n_enc)]
+        for i in range(cfg.n_enc):
+            h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
+                                         eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
+                                         site=i)
+        stash.push("enc_ln_in", h)
+        mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
+        enc_out = arena.alloc((b, ls, d), dt)
+        K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
+                            cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
+                            check_degenerate=False)
+        stash.push("enc_ln_mu", mu_e); stash.push("enc_ln_sg", sg_e)
+        stash.push("enc_out", enc_out)
+        pw = self.packed_weights(params)
+        kv_pairs, kv_buf = packed_kv_forward(enc_out, pw, arena=arena)
+
+        # --- forward: decoder ---
+        g = arena.alloc((b, lt, d), dt)
+        keep_tgt = arena.alloc((_nbits(b * lt * d),), torch.uint8)
+        K.embedding_forward(tok_emb, pos, tgt_in, emb_cfg, p_drop, s_tgt, out=g,
+                            bits_out=keep_tgt, validate=False)
+        stash.push("tgt_keep", keep_tgt)
+        dec_w = [DecoderLayerWeights.from_params(params, f"dec{i}.") for i in range(cfg.n_dec)]
+        for i in range(cfg.n_dec):
+            g, _ = decoder_layer_forward(g, dec_w[i], kv_pairs[i], dec_mask, cross_mask, p_drop,
+                                         dec_seed, n_heads=n, eps=cfg.eps, arena=arena,
+                                         stash=stash, prefix=f"dec{i}.", site=i)
+        stash.push("dec_ln_in", g)
+        mu_d, sg_d = arena.alloc((b * lt,), sdt), arena.alloc((b * lt,), sdt)
+        dec_out = arena.alloc((b, lt, d), dt)
+        K.layernorm_forward(g, _as_dt(params["dec_ln.w"], dt), _as_dt(params["dec_ln.b"], dt),
+                            cfg.eps, out=dec_out, mu_out=mu_d, sigma_out=sg_d,
+                            check_degenerate=False)
+        stash.push("dec_ln_mu", mu_d); stash.push("dec_ln_sg", sg_d)
+        stash.push("dec_out", dec_out)
+
+        # --- criterion: one fused pass -> loss/count/correct (+ dlogits in place) ---
+        proj_w = tok_emb if cfg.tie_embeddings else _as_dt(params["out_proj.w"], dt)
+        rt = b * lt
+        logits = arena.alloc((rt, v), dt)
+        K.gemm(dec_out.view(rt, d), proj_w, trans_b=True, out=logits)
+        row_stats = arena.alloc((2 * rt,), torch.float64)
+        out3 = torch.empty(3, dtype=torch.float64, device=ctx.device)
+        logq = None
+        if capture is not None:
+            logq = torch.empty((rt, v), dtype=dt if dt != torch.float64 else torch.float32,
+                               device=ctx.device)
+        if dt == torch.float64:
+            self._criterion_f64(logits, tgt_out, out3, alpha, batch.pad_id, grad_scale,
+                                compute_grads, logq)
+        else:
+            _lib.call("ls2_criterion_fused", logits.data_ptr(), tgt_out.data_ptr(),
+                      logits.data_ptr() if compute_grads else None, _lib.ptr(logq),
+                      row_stats.data_ptr(), out3.data_ptr(), None, rt, v, float(alpha),
+                      int(batch.pad_id), 1, float(grad_scale), _lib.dtype_code(logits),
+                      _lib.stream_handle())
+        arena.free(row_stats)
+        out = ModelOutput(out3)
+        if capture is not None:
+            capture["logq"] = logq.view(b, lt, v)
+        if not compute_grads:
+            stash.drain(arena)
+            arena.free(kv_buf)
+            arena.free(logits)
+            return out
+
+        # --- backward: output projection ---
+        dlogits = logits
+        dec_out = stash.pop("dec_out")
+        ddec = arena.alloc((b, lt, d), dt)
+        K.gemm(dlogits, proj_w, out=ddec.view(rt, d))
+        _wgrad(sink, "tok_emb" if cfg.tie_embeddings else "out_proj.w", dlogits,
+               dec_out.view(rt, d))
+        arena.free(dlogits); arena.free(dec_out)
+        sg_d = stash.pop("dec_ln_sg"); mu_d = stash.pop("dec_ln_mu")
+        g_in = stash.pop("dec_ln_in")
+        dg = arena.alloc((b, lt, d), dt)
+        _ln_bwd(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg, None)
+        arena.free(ddec); arena.free(mu_d); arena.free(sg_d); arena.free(g_in)
+
+        # --- backward: decoder stack; dK_i/dV_i land in one packed buffer ---
+        dkv = arena.alloc((b, ls, 2 * cfg.n_dec * d), dt)
+        nd = cfg.n_dec
+        dks: list = [None] * nd
+        dvs: list = [None] * nd
+        for i in reversed(range(nd)):
+            dest = (dkv[..., i * d:(i + 1) * d], dkv[..., (nd + i) * d:(nd + i + 1) * d])
+            dg, dks[i], dvs[i] = decoder_layer_backward(
+                dg, dec_w[i], kv_pairs[i], stash, sink, n_heads=n, p_drop=p_drop, arena=arena,
+                prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest)
+            emit(("dec_layer_backward_done", i))
+        keep_tgt = stash.pop("tgt_keep")
+        self._embedding_grads(sink, dg, tgt_in, keep_tgt, p_drop, emb_cfg)
+        arena.free(dg); arena.free(keep_tgt)
+        arena.free(kv_buf)
+
+        # --- backward: packed cross K/V (only now is the enc grad legal) ---
+        enc_out = stash.pop("enc_out")
+        denc, _, _ = packed_kv_backward(dks, dvs, enc_out, pw, arena=arena, packed=dkv, sink=sink)
+        emit(("enc_out_grad_emitted",))
+        arena.free(dkv)
+        arena.free(enc_out)
+        sg_e = stash.pop("enc_ln_sg"); mu_e = stash.pop("enc_ln_mu")
+        h_in = stash.pop("enc_ln_in")
+        dh = arena.alloc((b, ls, d), dt)
+        _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
+        arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
+        for i in reversed(range(cfg.n_enc)):
+            dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
+                                        arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
+        keep_src = stash.pop("src_keep")
+        self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
+        arena.free(dh); arena.free(keep_src)
+        if len(stash):
+            raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")
+        return out
+
+    def _embedding_grads(self, sink, dy, tokens, keep_bits, p_drop, emb_cfg):
+        mask = DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dy.shape))
+        te = sink.target("tok_emb")
+        tp = sink.target("pos_emb") if emb_cfg.learned_positional else None
+        if te is not None and (tp is not None or not emb_cfg.learned_positional):
+            ev, ebeta = te
+            if not ebeta:
+                ev.zero_()
+            G.embedding_backward(dy, tokens, mask, emb_cfg, dE_out=ev,
+                                 dP_out=None if tp is None else tp[0],
+                                 beta_pos=0 if tp is None else tp[1], validate=False)
+            return
+        de, dp = G.embedding_backward(dy, tokens, mask, emb_cfg, validate=False)
+        sink.add("tok_emb", de)
+        if dp is not None:
+            sink.add("pos_emb", dp)
+
+    def _criterion_f64(self, logits, tgt_out, out3, alpha, pad_id, grad_scale, compute_grads,
+                       logq_out):
+        """float64 path (finite-difference checks): reference-API kernels."""
+        lq = K.log_softmax_forward(logits)
+        loss, count = K.ls_cross_entropy_forward(lq, tgt_out, alpha, pad_id)
+        ok = tgt_out != pad_id
+        correct = int((lq.argmax(dim=-1)[ok] == tgt_out[ok]).sum())
+        out3.copy_(torch.tensor([loss, count, correct], dtype=torch.float64))
+        if logq_out is not None:
+            logq_out.copy_(lq)
+        if compute_grads:
+            G.ls_cross_entropy_backward(torch.exp(lq), tgt_out, alpha, pad_id,
+                                        grad_scale=grad_scale, out=logits, check=False)
+
+
+def transformer_forward_backward(cfg: ModelConfig, params, batch: Batch, **kwargs):
+    """Functional wrapper: run one batch and return (output, grads dict)."""
+    sink = kwargs.pop("sink", None) or GradSink()
+    out = Transformer(cfg).forward_backward(params, batch, sink=sink, **kwargs)
+    return out, sink.store

@@ -1,0 +1,410 @@
+"""GPU parity of every hot-path operator against the reference's golden vectors
+and the CPU oracle (oracle/lsport.py).  Calls go through the package API, i.e.
+through the C ABI of libls2.so.
+
+Tolerances (BASELINE.json north star): bit-exact for masks/indices/trainer;
+1e-5 relative for fp32; 2e-2 relative for fp16/bf16 storage.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import lsport as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2110_05722_b200 import gradients as G
+    from paper_2110_05722_b200 import kernels as K
+    from paper_2110_05722_b200 import numerics as N
+    from paper_2110_05722_b200 import trainer as T
+    from paper_2110_05722_b200.errors import (AllMaskedRow, DegenerateRow, ShapeMismatch,
+                                              SequenceTooLong, TokenOutOfRange)
+
+
+def C(x):
+    return torch.as_tensor(np.ascontiguousarray(x)).cuda()
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+# --- RNG ------------------------------------------------------------------------------
+
+def test_rand_uniform_bit_identical(golden_ops):
+    g = golden_ops
+    for i in range(5):
+        u = N.rand_uniform_array(int(g[f"rng_seed_{i}"][0]), int(g[f"rng_start_{i}"][0]), 4099)
+        assert np.array_equal(H(u).view(np.uint64), g[f"rng_u_{i}"].view(np.uint64))
+
+
+def test_dropout_masks_bit_identical(golden_ops):
+    g = golden_ops
+    for j in range(4):
+        keep = g[f"mask_{j}_keep"]
+        m = K.make_dropout_mask(keep.shape, float(g[f"mask_{j}_p"][0]),
+                                int(g[f"mask_{j}_seed"][0]), np.float32)
+        assert np.array_equal(H(m.keep), keep)
+
+
+def test_large_mask_matches_oracle_bits():
+    n = 3 * 4096 * 512 + 5
+    m = K.make_dropout_mask((n,), 0.1, 0xDEADBEEF12345, torch.float32)
+    bits = H(m.bits)
+    ref = np.packbits(O.dropout_keep((n,), 0.1, 0xDEADBEEF12345).astype(np.uint8),
+                      bitorder="little")
+    assert np.array_equal(bits, ref)
+
+
+# --- LayerNorm ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag,tol", [("f64", 1e-10), ("f32", 1e-5), ("f16", 1e-5)])
+def test_layernorm_golden(golden_ops, tag, tol):
+    g = golden_ops
+    y, c = K.layernorm_forward(C(g[f"ln_{tag}_x"]), C(g[f"ln_{tag}_w"]), C(g[f"ln_{tag}_b"]), 1e-5)
+    assert y.dtype == (torch.float64 if tag == "f64" else torch.float32)
+    assert rel_err(H(y), g[f"ln_{tag}_y"], 1.0) < tol
+    assert rel_err(H(c.mu), g[f"ln_{tag}_mu"], 1.0) < tol
+    assert rel_err(H(c.sigma), g[f"ln_{tag}_sigma"]) < tol
+    dx, dw, db = G.layernorm_backward(C(g[f"ln_{tag}_dy"]), C(g[f"ln_{tag}_x"]),
+                                      C(g[f"ln_{tag}_w"]), c)
+    assert rel_err(H(dx), g[f"ln_{tag}_dx"], 1.0) < tol * 10
+    assert rel_err(H(dw), g[f"ln_{tag}_dw"], 1.0) < tol * 10
+    assert rel_err(H(db), g[f"ln_{tag}_db"], 1.0) < tol * 10
+
+
+def test_layernorm_known_answers_and_errors(golden_ops):
+    y, c = K.layernorm_forward(C(np.array([[1.0, -1.0]])), C(np.ones(2)), C(np.zeros(2)), eps=0.0)
+    assert np.allclose(H(y), [[1.0, -1.0]]) and H(c.sigma)[0] == 1.0
+    y, c = K.layernorm_forward(C(np.array([[1.0, 2.0, 3.0, 4.0]])), C(np.ones(4)), C(np.zeros(4)),
+                               eps=0.0)
+    assert np.allclose(H(y), [[-1.34164079, -0.4472136, 0.4472136, 1.34164079]], atol=1e-8)
+    with pytest.raises(DegenerateRow):
+        K.layernorm_forward(C(np.full((1, 4), 3.0)), C(np.ones(4)), C(np.zeros(4)), eps=0.0)
+    g = golden_ops
+    _, cs = K.layernorm_forward(C(g["ln_shift_x"]), C(np.ones(16)), C(np.zeros(16)), eps=0.0)
+    assert rel_err(H(cs.sigma), g["ln_shift_sigma"]) < 1e-9
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 512), (1000, 1024), (333, 48), (64, 2048), (7, 13)])
+def test_layernorm_fp16_storage_vs_oracle(rows, cols):
+    rng = np.random.default_rng(rows + cols)
+    x = (rng.normal(size=(rows, cols)) * 2 + 0.5).astype(np.float16)
+    w = (1 + 0.1 * rng.normal(size=cols)).astype(np.float16)
+    b = (0.1 * rng.normal(size=cols)).astype(np.float16)
+    dy = rng.normal(size=(rows, cols)).astype(np.float16)
+    res = rng.normal(size=(rows, cols)).astype(np.float16)
+    yo, mu, sg = O.layernorm_fwd(x, w, b, 1e-5)
+    y = torch.empty((rows, cols), dtype=torch.float16, device="cuda")
+    mu_d = torch.empty(rows, device="cuda")
+    sg_d = torch.empty(rows, device="cuda")
+    K.layernorm_forward(C(x), C(w), C(b), 1e-5, out=y, mu_out=mu_d, sigma_out=sg_d)
+    assert np.abs(H(y).astype(np.float32) - yo).max() <= 2e-2 * max(1, np.abs(yo).max())
+    assert rel_err(H(sg_d), sg) < 1e-5
+    dxo, dwo, dbo = O.layernorm_bwd(dy, x, w, mu, sg)
+    dx = torch.empty((rows, cols), dtype=torch.float16, device="cuda")
+    dw = torch.zeros(cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    G.layernorm_backward(C(dy), C(x), C(w), K.LNCache(mu_d, sg_d), out=dx, dres=C(res),
+                         dw_out=dw, db_out=db)
+    want = dxo + res.astype(np.float32)
+    assert np.abs(H(dx).astype(np.float32) - want).max() <= 2e-2 * max(1, np.abs(want).max())
+    assert np.abs(H(dw) - dwo).max() <= 1e-3 * max(1, np.abs(dwo).max())
+    assert np.abs(H(db) - dbo).max() <= 1e-3 * max(1, np.abs(dbo).max())
+
+
+# --- softmax --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag,tol", [("f64", 1e-10), ("f32", 2e-6)])
+def test_softmax_golden(golden_ops, tag, tol):
+    g = golden_ops
+    x, dy, lens = g[f"sm_{tag}_x"], g[f"sm_{tag}_dy"], g[f"sm_{tag}_lens"]
+    masks = {"none": None, "pad": K.AttentionMask("padding", lens), "causal": K.AttentionMask("causal")}
+    for mk, mask in masks.items():
+        y, cache = K.softmax_forward(C(x), mask=mask)
+        assert cache.probs is y
+        assert rel_err(H(y), g[f"sm_{tag}_{mk}_y"], 1.0) < tol, mk
+        dx = G.softmax_backward(C(dy), cache)
+        assert rel_err(H(dx), g[f"sm_{tag}_{mk}_dx"], 1.0) < tol * 5, mk
+    lq = K.log_softmax_forward(C(g[f"lsm_{tag}_h"]))
+    assert rel_err(H(lq), g[f"lsm_{tag}_y"], 1.0) < tol * 5
+
+
+def test_softmax_known_answers_and_inplace():
+    y, _ = K.softmax_forward(C(np.array([[1.0, 2.0, 3.0]])))
+    assert np.allclose(H(y), [[0.0900306, 0.2447285, 0.6652410]], atol=1e-6)
+    y, _ = K.softmax_forward(C(np.array([[1.0, 1.0]])), mask=np.array([[True, False]]))
+    assert np.array_equal(H(y), [[1.0, 0.0]])
+    with pytest.raises(AllMaskedRow):
+        K.softmax_forward(C(np.ones((1, 3))), mask=np.zeros((1, 3), dtype=bool))
+    x = C(np.random.default_rng(0).normal(size=(8, 64)).astype(np.float32))
+    ref = O.softmax_fwd(H(x))
+    y, _ = K.softmax_forward(x, out=x)
+    assert y is x and rel_err(H(x), ref, 1.0) < 2e-6
+    y = K.log_softmax_forward(C(np.array([[1000.0, 0.0]])))
+    assert np.allclose(H(y), [[0.0, -1000.0]], atol=1e-9)
+
+
+@pytest.mark.parametrize("shape,kind", [((64, 8, 64, 64), "pad"), ((64, 8, 64, 64), "causal"),
+                                        ((3, 2, 5, 37), "pad"), ((2, 4, 17, 300), "none"),
+                                        ((2, 2, 4, 5000), "none")])
+def test_softmax_fp16_vs_oracle(shape, kind):
+    rng = np.random.default_rng(1)
+    x = (rng.normal(size=shape) * 3).astype(np.float16)
+    dy = rng.normal(size=shape).astype(np.float16)
+    lens = rng.integers(1, shape[-1] + 1, shape[0])
+    keep = {"pad": O.pad_keep(lens, shape[2], shape[3]), "causal": O.causal_keep(shape[2], shape[3]),
+            "none": None}[kind]
+    mask = {"pad": K.AttentionMask("padding", lens), "causal": K.AttentionMask("causal"),
+            "none": None}[kind]
+    scale = 0.125
+    want = O.softmax_fwd(x.astype(np.float32) * np.float32(scale), keep)
+    y = torch.empty(shape, dtype=torch.float16, device="cuda")
+    K.softmax_forward(C(x), mask=mask, out=y, in_scale=scale)
+    assert np.abs(H(y).astype(np.float32) - want).max() <= 2e-3
+    if keep is not None:
+        assert np.all(H(y)[~np.broadcast_to(keep, shape)] == 0)
+    dwant = O.softmax_bwd(dy, H(y)) * np.float32(scale)
+    dx = torch.empty(shape, dtype=torch.float16, device="cuda")
+    G.softmax_backward(C(dy), K.SoftmaxCache(y), out=dx, out_scale=scale)
+    assert np.abs(H(dx).astype(np.float32) - dwant).max() <= 2e-2 * max(1, np.abs(dwant).max())
+
+
+# --- criterion ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag,tol", [("f64", 1e-10), ("f32", 2e-6)])
+def test_criterion_golden(golden_ops, tag, tol):
+    g = golden_ops
+    h, tg = g[f"ce_{tag}_h"], g[f"ce_{tag}_t"]
+    for a in (0.0, 0.1, 1.0):
+        loss, cnt = K.ls_cross_entropy_forward(K.log_softmax_forward(C(h)), C(tg), a, pad_id=0)
+        want = g[f"ce_{tag}_{a}_loss"]
+        assert cnt == int(want[1]) and abs(loss - want[0]) <= tol * max(1.0, abs(want[0]))
+        pr, _ = K.softmax_forward(C(h))
+        dh = G.ls_cross_entropy_backward(pr, C(tg), a, pad_id=0, grad_scale=0.25)
+        assert rel_err(H(dh), g[f"ce_{tag}_{a}_dh"], 1.0) < tol * 5
+
+
+def test_criterion_known_answers():
+    assert K.ls_cross_entropy_forward(C(np.log(np.full((1, 2), 0.5))), C(np.array([0])), 0.0)[0] == \
+        pytest.approx(np.log(2.0), rel=1e-12)
+    dh = G.ls_cross_entropy_backward(C(np.full((1, 4), 0.25)), C(np.array([0])), alpha=0.1)
+    assert np.allclose(H(dh), [[-0.675, 0.225, 0.225, 0.225]], atol=1e-12)
+    with pytest.raises(TokenOutOfRange):
+        K.ls_cross_entropy_forward(K.log_softmax_forward(C(np.zeros((3, 4)))),
+                                   C(np.array([0, 9, 0])), alpha=0.0)
+
+
+@pytest.mark.parametrize("rows,v", [(4096, 32000), (512, 250000), (37, 29), (64, 1000)])
+def test_fused_criterion_vs_oracle(rows, v):
+    from paper_2110_05722_b200 import _lib
+    rng = np.random.default_rng(v)
+    h = (rng.normal(size=(rows, v)) * 2).astype(np.float16)
+    tg = rng.integers(0, v, rows)
+    tg[::7] = 0
+    logq = O.log_softmax_fwd(h)
+    loss, cnt = O.ls_ce_fwd(logq, tg, 0.1, 0)
+    ok = tg != 0
+    correct = int((np.argmax(h.astype(np.float32), axis=-1)[ok] == tg[ok]).sum())
+    d_ref = O.ls_ce_bwd(np.exp(logq), tg, 0.1, 0, grad_scale=4.0)
+    hd = C(h)
+    td = C(tg.astype(np.int64))
+    stats = torch.empty(2 * rows, dtype=torch.float64, device="cuda")
+    out3 = torch.empty(3, dtype=torch.float64, device="cuda")
+    _lib.call("ls2_criterion_fused", hd.data_ptr(), td.data_ptr(), hd.data_ptr(), None,
+              stats.data_ptr(), out3.data_ptr(), None, rows, v, 0.1, 0, 1, 4.0, _lib.F16,
+              _lib.stream_handle())
+    o = H(out3)
+    assert o[1] == cnt and abs(o[2] - correct) <= max(1, rows // 500)
+    assert abs(o[0] - loss) <= 1e-4 * abs(loss)
+    assert np.abs(H(hd).astype(np.float32) - d_ref).max() <= 2e-2 * 4.0
+
+
+# --- elementwise tails ----------------------------------------------------------------
+
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+def test_elementwise_golden_bit_exact(golden_ops, tag):
+    g = golden_ops
+    x, res, bias, dy = (C(g[f"bdr_{tag}_{k}"]) for k in ("x", "res", "bias", "dy"))
+    y, m = K.bias_dropout_residual(x, bias, res, 0.3, seed=1234)
+    assert np.array_equal(H(m.keep), g[f"bdr_{tag}_keep"])
+    assert np.array_equal(H(y), g[f"bdr_{tag}_y"])
+    dx, db, dres = G.bias_dropout_residual_backward(dy, m)
+    assert dres is dy and np.array_equal(H(dx), g[f"bdr_{tag}_dx"])
+    assert rel_err(H(db), g[f"bdr_{tag}_db"], 1.0) < 1e-12
+    y2, m2, relu = K.bias_relu_dropout(x, bias, 0.25, seed=99)
+    assert np.array_equal(H(y2), g[f"brd_{tag}_y"]) and np.array_equal(H(relu), g[f"brd_{tag}_relu"])
+    assert np.array_equal(H(m2.keep), g[f"brd_{tag}_keep"])
+    dx2, db2 = G.bias_relu_dropout_backward(dy, m2, relu)
+    assert np.array_equal(H(dx2), g[f"brd_{tag}_dx"])
+    assert rel_err(H(db2), g[f"brd_{tag}_db"], 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 512), (4096, 2048), (100, 24), (9, 7)])
+def test_elementwise_fp16_storage_vs_oracle(rows, cols):
+    rng = np.random.default_rng(cols)
+    x, res, dy = (rng.normal(size=(rows, cols)).astype(np.float16) for _ in range(3))
+    bias = rng.normal(size=cols).astype(np.float16)
+    keep = O.dropout_keep((rows, cols), 0.1, 77)
+    y = torch.empty((rows, cols), dtype=torch.float16, device="cuda")
+    bits = torch.empty((rows * cols + 7) // 8, dtype=torch.uint8, device="cuda")
+    _, m = K.bias_dropout_residual(C(x), C(bias), C(res), 0.1, 77, out=y, bits_out=bits)
+    want = O.bias_dropout_residual_fwd(x, bias, res, keep, 0.1)
+    assert np.array_equal(H(y), want.astype(np.float16))
+    assert np.array_equal(H(bits), np.packbits(keep.astype(np.uint8).reshape(-1), bitorder="little"))
+    dx = torch.empty_like(y)
+    db = torch.zeros(cols, device="cuda")
+    G.bias_dropout_residual_backward(C(dy), m, out=dx, dbias_out=db)
+    dxo, dbo, _ = O.bias_dropout_residual_bwd(dy, keep, 0.1)
+    assert np.array_equal(H(dx), dxo.astype(np.float16))
+    assert np.abs(H(db) - dbo).max() <= 1e-5 * max(1, np.abs(dbo).max())
+    z = torch.empty_like(y)
+    rb = torch.empty_like(bits)
+    _, m2, rl = K.bias_relu_dropout(C(x), C(bias), 0.1, 78, out=z, bits_out=bits.clone(),
+                                    relu_bits_out=rb)
+    keep2 = O.dropout_keep((rows, cols), 0.1, 78)
+    zo, relu = O.bias_relu_dropout_fwd(x, bias, keep2, 0.1)
+    assert np.array_equal(H(z), zo.astype(np.float16))
+    da = torch.empty_like(y)
+    G.bias_relu_dropout_backward(C(dy), m2, rl, out=da, dbias_out=db)
+    dao, dbo2 = O.bias_relu_dropout_bwd(dy, keep2, relu, 0.1)
+    assert np.array_equal(H(da), dao.astype(np.float16))
+    assert np.abs(H(db) - dbo2).max() <= 1e-5 * max(1, np.abs(dbo2).max())
+
+
+# --- embedding ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_embedding_golden(golden_ops, tag):
+    g = golden_ops
+    cfg = K.EmbeddingConfig(scale=4.0, vocab=23, max_len=9)
+    E, P = C(g[f"emb_{tag}_E"]), C(g[f"emb_{tag}_P"])
+    y, m = K.embedding_forward(E, P, g[f"emb_{tag}_tok"], cfg, 0.2, seed=31)
+    assert np.array_equal(H(m.keep), g[f"emb_{tag}_keep"])
+    assert np.array_equal(H(y), g[f"emb_{tag}_y"])
+    de, dp = G.embedding_backward(C(g[f"emb_{tag}_dy"]), g[f"emb_{tag}_tok"], m, cfg)
+    tol = 1e-12 if tag == "f64" else 1e-6
+    assert rel_err(H(de), g[f"emb_{tag}_dE"], 1.0) < tol
+    assert rel_err(H(dp), g[f"emb_{tag}_dP"], 1.0) < tol
+
+
+def test_embedding_errors_and_known_answer():
+    e = C(np.array([[1.0, 2.0], [3.0, 4.0]]))
+    p = C(np.array([[0.1, 0.2], [0.3, 0.4]]))
+    cfg = K.EmbeddingConfig(scale=2.0, vocab=2, max_len=2)
+    y, _ = K.embedding_forward(e, p, [[1, 0]], cfg, 0.0, seed=0)
+    assert np.allclose(H(y)[0], [[6.1, 8.2], [2.3, 4.4]])
+    with pytest.raises(TokenOutOfRange):
+        K.embedding_forward(e, p, [[2, 0]], cfg, 0.0, seed=0)
+    with pytest.raises(SequenceTooLong):
+        K.embedding_forward(e, p, [[0, 1, 0]], cfg, 0.0, seed=0)
+
+
+def test_embedding_fp16_tbase_shape():
+    rng = np.random.default_rng(5)
+    V, d, B, L = 32000, 512, 64, 64
+    E = (rng.normal(size=(V, d)) * 0.02).astype(np.float16)
+    P = (rng.normal(size=(256, d)) * 0.02).astype(np.float16)
+    tok = rng.integers(2, V, (B, L))
+    tok[:, :5] = 7       # heavy repeats exercise the atomics
+    cfg = K.EmbeddingConfig(scale=np.sqrt(d), vocab=V, max_len=256)
+    y = torch.empty((B, L, d), dtype=torch.float16, device="cuda")
+    bits = torch.empty(B * L * d // 8, dtype=torch.uint8, device="cuda")
+    _, m = K.embedding_forward(C(E), C(P), tok, cfg, 0.1, 5, out=y, bits_out=bits)
+    keep = O.dropout_keep((B, L, d), 0.1, 5)
+    want = O.embedding_fwd(E, P, tok, np.sqrt(d), keep, 0.1)
+    assert np.abs(H(y).astype(np.float32) - want).max() <= 1e-3
+    dy = rng.normal(size=(B, L, d)).astype(np.float16)
+    de, dp = G.embedding_backward(C(dy), tok, m, cfg)
+    deo, dpo = O.embedding_bwd(dy, tok, keep, 0.1, V, 256, np.sqrt(d))
+    assert np.abs(H(de) - deo).max() <= 1e-4 * max(1, np.abs(deo).max())
+    assert np.abs(H(dp) - dpo).max() <= 1e-5 * max(1, np.abs(dpo).max())
+
+
+# --- trainer --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("algo", ["adam", "sgd"])
+def test_trainer_bit_exact_golden(golden_ops, algo):
+    g = golden_ops
+    ws = T.workspace_pack([("p", np.zeros(777, np.float32))], algo)
+    ws.params16.copy_(C(g[f"tr_{algo}_p0"]))
+    ws.m32.copy_(C(g[f"tr_{algo}_m0"]))
+    if algo == "adam":
+        ws.v32.copy_(C(g[f"tr_{algo}_v0"]))
+    cfg = T.OptimConfig(algorithm=algo, lr=3e-3, weight_decay=0.01, momentum=0.9, loss_scale=8.0)
+    for t in range(1, 6):
+        ws.grads16.copy_(C(g[f"tr_{algo}_g"][t - 1]))
+        rep = T.optimizer_step(ws, cfg, t)
+        applied, nonfinite = g[f"tr_{algo}_applied{t}"]
+        assert rep.applied == bool(applied) and rep.nonfinite == nonfinite
+        assert np.array_equal(H(ws.params16).view(np.uint16), g[f"tr_{algo}_p{t}"].view(np.uint16))
+    assert np.array_equal(H(ws.m32), g[f"tr_{algo}_mfinal"])
+    if algo == "adam":
+        assert np.array_equal(H(ws.v32), g[f"tr_{algo}_vfinal"])
+
+
+def test_adam_bit_exact_random_states():
+    rng = np.random.default_rng(2)
+    for trial in range(40):
+        n = int(rng.integers(1, 5000))
+        p0 = (rng.normal(size=n) * rng.choice([0.01, 1.0, 30.0])).astype(np.float32)
+        g0 = (rng.normal(size=n) * rng.choice([1e-4, 0.1, 5.0])).astype(np.float32)
+        m0 = (rng.normal(size=n) * 0.1).astype(np.float32)
+        v0 = rng.uniform(0.0, 0.2, size=n).astype(np.float32)
+        lr = float(rng.choice([1e-4, 1e-3, 0.01]))
+        wd = float(rng.choice([0.0, 0.01]))
+        t = int(rng.integers(1, 50))
+        ls = float(rng.choice([1.0, 8.0]))
+        ws = T.workspace_pack([("p", p0)], "adam")
+        g16 = O.to_half(g0)
+        ws.grads16.copy_(C(g16))
+        ws.m32.copy_(C(m0))
+        ws.v32.copy_(C(v0))
+        T.adam_step(ws, T.OptimConfig(lr=lr, weight_decay=wd, loss_scale=ls), t)
+        p16 = O.to_half(p0)
+        m, v = m0.copy(), v0.copy()
+        O.adam_flat(p16, g16, m, v, lr=lr, beta1=0.9, beta2=0.999, eps=1e-8, wd=wd,
+                    loss_scale=ls, t=t)
+        assert np.array_equal(H(ws.params16).view(np.uint16), p16.view(np.uint16)), trial
+        assert np.array_equal(H(ws.m32), m) and np.array_equal(H(ws.v32), v), trial
+
+
+# --- gemm -----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt,tol", [(np.float64, 1e-12), (np.float32, 1e-5), (np.float16, 2e-2)])
+def test_gemm_layouts(dt, tol):
+    rng = np.random.default_rng(8)
+    a, b = rng.normal(size=(33, 17)).astype(dt), rng.normal(size=(17, 29)).astype(dt)
+    want = a.astype(np.float64) @ b.astype(np.float64)
+    got = K.gemm(C(a), C(b))
+    assert rel_err(H(got), want, 1.0) < tol
+    assert rel_err(H(K.gemm(C(a.T.copy()), C(b), trans_a=True)), want, 1.0) < tol
+    assert rel_err(H(K.gemm(C(a), C(b.T.copy()), trans_b=True)), want, 1.0) < tol
+    acc = C(np.ones((33, 29), dtype=np.float64 if dt == np.float64 else np.float32))
+    K.gemm(C(a), C(b), accumulate_into=acc)
+    assert rel_err(H(acc), want + 1.0, 1.0) < tol
+    # two-level head views (pointer-array batch)
+    B_, L_, h, hd = 3, 5, 2, 4
+    qkv = rng.normal(size=(B_, L_, 3 * h * hd)).astype(dt)
+    qt = C(qkv)
+    q = qt[..., :h * hd].view(B_, L_, h, hd).permute(0, 2, 1, 3)
+    k = qt[..., h * hd:2 * h * hd].view(B_, L_, h, hd).permute(0, 2, 1, 3)
+    s = K.gemm(q, k, trans_b=True)
+    qn = qkv[..., :h * hd].reshape(B_, L_, h, hd).transpose(0, 2, 1, 3).astype(np.float64)
+    kn = qkv[..., h * hd:2 * h * hd].reshape(B_, L_, h, hd).transpose(0, 2, 1, 3).astype(np.float64)
+    assert rel_err(H(s), qn @ kn.swapaxes(-1, -2), 1.0) < tol
+    ctx = torch.zeros((B_, L_, h * hd), dtype=qt.dtype, device="cuda")
+    cv = ctx.view(B_, L_, h, hd).permute(0, 2, 1, 3)
+    K.gemm(s.to(qt.dtype), k, out=cv)
+    want_ctx = (H(s).astype(np.float64) @ kn).transpose(0, 2, 1, 3).reshape(B_, L_, h * hd)
+    assert rel_err(H(ctx), want_ctx, 1.0) < tol * 2
+
+
+def test_gemm_known_and_errors():
+    c = K.gemm(C(np.array([[1.0, 2.0], [3.0, 4.0]])), C(np.array([[5.0, 6.0], [7.0, 8.0]])))
+    assert np.array_equal(H(c), [[19.0, 22.0], [43.0, 50.0]])
+    with pytest.raises(ShapeMismatch):
+        K.gemm(C(np.zeros((2, 3))), C(np.zeros((4, 2))))
