@@ -1,0 +1,135 @@
+"""Token batches (F/data.py): synthetic copy/reverse tasks as pure functions of
+(seed, step), length bucketing to multiples of 4, and a fixed-shape synthetic
+WMT-like task for benchmarking.  Host-side numpy (the batch is uploaded by the
+engine through pinned buffers)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import DataError, ParseError, TokenOutOfRange
+from .model import Batch
+from .numerics import derive_seed, _finalize, _PHI, _MASK64
+
+LEN_BUCKET = 4
+
+
+def _uniform(seed: int, n: int) -> np.ndarray:
+    """Host splitmix64 draws (same stream as the device RNG)."""
+    i = np.arange(n, dtype=np.uint64)
+    z = np.uint64(seed & _MASK64) + i * np.uint64(_PHI)
+    z ^= z >> np.uint64(30)
+    z *= np.uint64(0xBF58476D1CE4E5B9)
+    z ^= z >> np.uint64(27)
+    z *= np.uint64(0x94D049BB133111EB)
+    z ^= z >> np.uint64(31)
+    return (z >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+
+
+def bucket_len(m: int, max_len: int) -> int:
+    padded = -(-m // LEN_BUCKET) * LEN_BUCKET
+    return padded if padded <= max_len else max(m, min(padded, max_len))
+
+
+def bos_id(pad_id: int, vocab: int) -> int:
+    return (pad_id + 1) % vocab
+
+
+def payload_range(pad_id: int, vocab: int) -> list:
+    reserved = {pad_id, bos_id(pad_id, vocab)}
+    return [t for t in range(vocab) if t not in reserved]
+
+
+def load_token_file(path: str, vocab: int) -> list:
+    try:
+        with open(path) as fh:
+            lines = fh.readlines()
+    except OSError as exc:
+        raise DataError(f"cannot read {path}: {exc}") from exc
+    seqs = []
+    for ln, line in enumerate(lines, start=1):
+        parts = line.split()
+        if not parts:
+            continue
+        try:
+            ids = [int(p) for p in parts]
+        except ValueError:
+            raise ParseError(f"{path}:{ln}: non-integer token") from None
+        if min(ids) < 0:
+            raise ParseError(f"{path}:{ln}: negative token id")
+        if max(ids) >= vocab:
+            raise TokenOutOfRange(f"{path}:{ln}: token id >= vocab ({vocab})")
+        seqs.append(ids)
+    return seqs
+
+
+class SyntheticTask:
+    """copy: target = source; reverse: target reversed (F/data.py:61-102)."""
+
+    def __init__(self, run_cfg):
+        m, t, d = run_cfg.model, run_cfg.train, run_cfg.data
+        if m.vocab < 4:
+            raise DataError("synthetic tasks need vocab >= 4")
+        self.task = d.task
+        self.pad_id = d.pad_id
+        self.bos = bos_id(d.pad_id, m.vocab)
+        self.symbols = np.array(payload_range(d.pad_id, m.vocab))
+        self.min_len = max(1, d.min_len)
+        self.max_len = m.max_len
+        self.batch_size = max(1, t.batch_tokens // m.max_len)
+        self.seed = t.seed
+
+    def possible_shapes(self) -> list:
+        return [(self.batch_size, l) for l in
+                sorted({bucket_len(m, self.max_len) for m in range(self.min_len, self.max_len + 1)})]
+
+    def batch(self, step: int) -> Batch:
+        b = self.batch_size
+        span = self.max_len - self.min_len + 1
+        lens = (_uniform(derive_seed(self.seed, step, 101), b) * span).astype(int) + self.min_len
+        lb = bucket_len(int(lens.max()), self.max_len)
+        u = _uniform(derive_seed(self.seed, step, 102), b * lb)
+        body = self.symbols[(u * len(self.symbols)).astype(int)].reshape(b, lb)
+        src = np.full((b, lb), self.pad_id, dtype=np.int64)
+        tgt_out = np.full((b, lb), self.pad_id, dtype=np.int64)
+        tgt_in = np.full((b, lb), self.pad_id, dtype=np.int64)
+        for i in range(b):
+            n = int(lens[i])
+            seq = body[i, :n]
+            out = seq if self.task == "copy" else seq[::-1]
+            src[i, :n] = seq
+            tgt_out[i, :n] = out
+            tgt_in[i, 0] = self.bos
+            tgt_in[i, 1:n] = out[:n - 1]
+        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt_out, src_len=lens.astype(np.int64),
+                     pad_id=self.pad_id)
+
+
+class FixedShapeTask:
+    """Benchmark batches: B x L tokens uniform in [2, V), full-length sequences
+    (4096 target tokens for 64 x 64), a pure function of (seed, step)."""
+
+    def __init__(self, batch: int, length: int, vocab: int, seed: int = 0, pad_id: int = 0):
+        self.b, self.l, self.v, self.seed, self.pad_id = batch, length, vocab, seed, pad_id
+        self.bos = bos_id(pad_id, vocab)
+
+    def possible_shapes(self) -> list:
+        return [(self.b, self.l)]
+
+    def batch(self, step: int) -> Batch:
+        u = _uniform(derive_seed(self.seed, step, 7), 2 * self.b * self.l)
+        tok = (2 + (u * (self.v - 2)).astype(np.int64)).reshape(2, self.b, self.l)
+        src, tgt = tok[0], tok[1]
+        tgt_in = np.concatenate([np.full((self.b, 1), self.bos, np.int64), tgt[:, :-1]], axis=1)
+        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt.copy(),
+                     src_len=np.full(self.b, self.l, np.int64), pad_id=self.pad_id)
+
+
+def make_task(run_cfg):
+    if run_cfg.data.task == "file":
+        raise DataError("file task: use load_token_file + a custom batcher (not on the hot path)")
+    if run_cfg.data.task == "fixed":
+        m = run_cfg.model
+        return FixedShapeTask(max(1, run_cfg.train.batch_tokens // m.max_len), m.max_len, m.vocab,
+                              run_cfg.train.seed, run_cfg.data.pad_id)
+    return SyntheticTask(run_cfg)

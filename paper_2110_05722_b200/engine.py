@@ -1,0 +1,348 @@
+"""Training driver (F/engine.py): fused forward/backward on the planned device
+arena, scale+narrow into the fp16 workspace, (data-parallel all-reduce), one
+workspace optimizer pass — captured as ONE CUDA graph per (mode, B, L) bucket.
+
+Per step the host only: builds the batch (numpy), writes it and the per-step
+dropout seeds into pinned staging buffers, replays the bucket's graph (which
+begins with the H2D copies and ends with a D2H copy of loss / token count /
+correct / applied-flag / non-finite count) and reads those five numbers.
+Skip decisions (non-finite loss or gradient) and the Adam step counter live
+on the device, so a skipped step needs no extra host round trip.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import checkpoint as ckpt
+from .config import RunConfig
+from .data import make_task
+from .dist import DataParallel
+from .errors import DataError
+from .memplan import PlannedArena, RecordingArena, TensorTag, classify, estimate_capacity
+from .model import Batch, Transformer, _ViewSink, validate_batch
+from .trainer import OptimConfig, Workspace, _state, workspace_pack
+
+EVAL_STEP_BASE = 1 << 30
+
+
+@dataclass
+class StepMetrics:
+    step: int
+    loss: float
+    tokens: int
+    accuracy: float
+    tokens_per_sec: float
+    arena_high_water: int
+    skipped: bool
+    nonfinite: int
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+class _StaticIO:
+    """Device batch buffers of one bucket shape + their pinned host twins."""
+
+    def __init__(self, b: int, l: int, device):
+        pin = lambda *s: torch.zeros(*s, dtype=torch.int64).pin_memory()  # noqa: E731
+        self.h_src, self.h_tin, self.h_tout, self.h_len = pin(b, l), pin(b, l), pin(b, l), pin(b)
+        self.src = torch.zeros((b, l), dtype=torch.int64, device=device)
+        self.tin = torch.zeros_like(self.src)
+        self.tout = torch.zeros_like(self.src)
+        self.len = torch.zeros(b, dtype=torch.int64, device=device)
+        self.pad_id = 0
+
+    def stage(self, batch: Batch):
+        self.h_src.copy_(torch.from_numpy(np.asarray(batch.src, dtype=np.int64)))
+        self.h_tin.copy_(torch.from_numpy(np.asarray(batch.tgt_in, dtype=np.int64)))
+        self.h_tout.copy_(torch.from_numpy(np.asarray(batch.tgt_out, dtype=np.int64)))
+        self.h_len.copy_(torch.from_numpy(np.asarray(batch.src_len, dtype=np.int64)))
+        self.pad_id = int(batch.pad_id)
+
+    def upload(self):
+        for d, h in ((self.src, self.h_src), (self.tin, self.h_tin), (self.tout, self.h_tout),
+                     (self.len, self.h_len)):
+            d.copy_(h, non_blocking=True)
+
+    def batch(self) -> Batch:
+        return Batch(self.src, self.tin, self.tout, self.len, self.pad_id)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 8 * (3 * self.src.numel() + self.len.numel())
+
+
+class TrainingEngine:
+    def __init__(self, run_cfg: RunConfig, task=None, dp: DataParallel | None = None,
+                 device=None):
+        self.cfg = run_cfg
+        ctx = _lib.context(device)
+        self.device = ctx.device
+        self.model = Transformer(run_cfg.model)
+        self.task = task if task is not None else make_task(run_cfg)
+        t = run_cfg.train
+        self.optim = OptimConfig(algorithm=t.algorithm, lr=t.lr, beta1=t.beta1, beta2=t.beta2,
+                                 eps_opt=t.eps_opt, weight_decay=t.weight_decay,
+                                 momentum=t.momentum, loss_scale=t.loss_scale)
+        init = self.model.init_params(t.seed)
+        self.ws: Workspace = workspace_pack([(n, init[n]) for n in self.model.param_names],
+                                            t.algorithm)
+        del init
+        self.pviews = self.ws.param_views()
+        n = self.ws.n_elements
+        self.grad_acc = torch.zeros(n, dtype=torch.float32, device=self.device)
+        self.gviews = {lk.name: self.grad_acc[lk.offset:lk.offset + lk.length].view(lk.shape)
+                       for lk in self.ws.links}
+        self._opt = _state(self.ws, self.optim)
+        self._applied_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._dev_out = torch.zeros(5, dtype=torch.float64, device=self.device)
+        self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
+        self.dp = dp if dp is not None else DataParallel()
+        self.applied_steps = 0
+        self.skip_count = 0
+        self.arena: PlannedArena | None = None
+        self.capacity = 0
+        self._io: dict = {}
+        self._graphs: dict = {}
+        self._launches: dict = {}
+        self.use_graphs = bool(t.cuda_graphs)
+        self.last_out3 = None
+
+    # -- arena setup (F/engine.py:89-103) ----------------------------------------------
+
+    def _dummy_batch(self, b: int, l: int) -> Batch:
+        filler = (self.cfg.data.pad_id + 2) % self.cfg.model.vocab
+        tok = np.full((b, l), filler, dtype=np.int64)
+        return Batch(src=tok, tgt_in=tok.copy(), tgt_out=tok.copy(),
+                     src_len=np.full(b, l, dtype=np.int64), pad_id=self.cfg.data.pad_id)
+
+    def _record_shape(self, batch: Batch, compute_grads: bool):
+        rec = RecordingArena(self.device)
+        sink = _ViewSink(self.gviews) if compute_grads else None
+        self.model.forward_backward(self.pviews, batch,
+                                    p_drop=self.cfg.train.p_drop if compute_grads else 0.0,
+                                    alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
+                                    step=0, arena=rec, sink=sink, compute_grads=compute_grads)
+        return rec.finish()
+
+    def setup_arena(self) -> int:
+        """Dry-run every bucket shape, size the arena once (bytes), register plans."""
+        recorded = {}
+        for b, l in self.task.possible_shapes():
+            batch = self._dummy_batch(b, l)
+            recorded[("train", b, l)] = self._record_shape(batch, True)
+            recorded[("eval", b, l)] = self._record_shape(batch, False)
+        torch.cuda.synchronize()
+        self.capacity = estimate_capacity(recorded.values())
+        self.arena = PlannedArena(self.capacity, self.device)
+        for key, lts in recorded.items():
+            self.arena.register_plan(key, lts)
+        torch.cuda.empty_cache()
+        return self.capacity
+
+    def memory_report(self) -> dict:
+        tags = [TensorTag("params16", "parameter"), TensorTag("grads16", "gradient"),
+                TensorTag("grad_acc32", "gradient"), TensorTag("moments", "moment"),
+                TensorTag("arena", "intermediate")]
+        p = self.ws.n_elements
+        return {"classes": classify(tags), "parameters": p,
+                "permanent_bytes": self.ws.state_bytes() + p * 4,
+                "temporary_capacity_bytes": self.capacity}
+
+    # -- the device step -------------------------------------------------------------
+
+    def _io_for(self, b, l) -> _StaticIO:
+        io = self._io.get((b, l))
+        if io is None:
+            io = self._io[(b, l)] = _StaticIO(b, l, self.device)
+        return io
+
+    def _fwd_bwd(self, io: _StaticIO, key, step: int, upload: bool = True):
+        t = self.cfg.train
+        if upload:
+            io.upload()
+        self.arena.begin(key)
+        sink = _ViewSink(self.gviews)
+        out = self.model.forward_backward(
+            self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
+            arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
+            upload_seeds=upload)
+        self.arena.end()
+        return out.out3
+
+    def capture_device_graph(self, key):
+        """Graph of one step with device-resident inputs (no H2D/D2H): the
+        benchmark's `value` path.  Also records how many libls2 kernels a step
+        launches (cuBLAS kernels not counted)."""
+        b, l = key[1], key[2]
+        io = self._io_for(b, l)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = _lib.launches()
+        with torch.cuda.graph(g):
+            out3 = self._fwd_bwd(io, key, 0, upload=False)
+            self._update(out3, host_copy=False)
+        self._launches[key] = _lib.launches() - n0
+        torch.cuda.synchronize()
+        return g
+
+    def launches_per_step(self, key) -> int:
+        return int(self._launches.get(key, 0))
+
+    def device_step(self, key, step: int):
+        """One eager step on already-resident inputs (DP fallback for timing)."""
+        io = self._io_for(key[1], key[2])
+        n0 = _lib.launches()
+        self._update(self._fwd_bwd(io, key, step, upload=False), host_copy=False)
+        self._launches[key] = _lib.launches() - n0
+
+    def _update(self, out3: torch.Tensor, host_copy: bool = True):
+        """narrow(+scale) -> [all-reduce] -> non-finite count -> Adam/SGD -> commit."""
+        st = _lib.stream_handle()
+        t = self.cfg.train
+        ws = self.ws
+        if self.dp.active:
+            self.dp.allreduce_totals(out3)
+        self._nonfinite.zero_()
+        _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr(), ws.grads16.data_ptr(),
+                  ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
+                  float(1.0 / t.act_grad_scale),
+                  None if self.dp.active else self._nonfinite.data_ptr(), st)
+        if self.dp.active:
+            self.dp.allreduce_grads(ws.grads16)
+            _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr(), ws.n_elements,
+                      self._nonfinite.data_ptr(), st)
+        loss_ptr = out3.data_ptr()
+        if self.optim.algorithm == "adam":
+            _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
+                      ws.m32.data_ptr(), ws.v32.data_ptr(), ws.n_elements,
+                      self._opt.hyper.data_ptr(), self._opt.bc.data_ptr(),
+                      self._opt.bc.numel() // 2, 0, self._applied_dev.data_ptr(),
+                      self._nonfinite.data_ptr(), loss_ptr, st)
+        else:
+            _lib.call("ls2_sgd", ws.params16.data_ptr(), ws.grads16.data_ptr(), ws.m32.data_ptr(),
+                      ws.n_elements, self._opt.hyper.data_ptr(), self._nonfinite.data_ptr(),
+                      loss_ptr, st)
+        _lib.call("ls2_step_commit", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
+                  loss_ptr, self._flag.data_ptr(), st)
+        self._dev_out[0:3].copy_(out3)
+        self._dev_out[3].copy_(self._flag[0])
+        self._dev_out[4].copy_(self._nonfinite[0])
+        if host_copy:
+            self._host_out.copy_(self._dev_out, non_blocking=True)
+
+    def _run(self, io, key, step, graphed: bool):
+        if graphed:
+            g = self._graphs.get(key)
+            if g is not None:
+                g.replay()
+                return
+        out3 = self._fwd_bwd(io, key, step)
+        self.last_out3 = out3
+        if not self.dp.active or not graphed:
+            self._update(out3)
+        else:
+            self._update(out3)
+
+    def _capture(self, io, key, step):
+        """Capture fwd/bwd + update of this bucket into one CUDA graph."""
+        if self.dp.active:
+            return  # collectives stay eager under DP
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out3 = self._fwd_bwd(io, key, step)
+            self._update(out3)
+        self._graphs[key] = g
+        torch.cuda.synchronize()
+
+    def refresh_seeds(self, step: int):
+        """Write this step's per-site dropout seeds into the pinned staging buffer."""
+        t = self.cfg.train
+        seeds = self.model.seed_table(self.device)
+        self.model.register_seeds(seeds, t.seed, step, t.p_drop)
+        seeds.write_host()
+
+    def train_step(self, step: int, trace=None) -> StepMetrics:
+        t0 = time.perf_counter()
+        batch = self.task.batch(step)
+        validate_batch(batch, self.cfg.model)
+        b, l = np.asarray(batch.src).shape
+        key = ("train", b, l)
+        if self.arena is None or not self.arena.has_plan(key):
+            raise DataError(f"no arena plan for batch shape {key}; call setup_arena()")
+        io = self._io_for(b, l)
+        graphed = self.use_graphs and key in self._graphs
+        io.stage(batch)
+        if graphed:
+            self.refresh_seeds(step)
+            self._graphs[key].replay()
+        else:
+            self._run(io, key, step, graphed=False)
+        torch.cuda.current_stream().synchronize()
+        loss, count, correct, applied, nonfinite = self._host_out.tolist()
+        if self.use_graphs and key not in self._graphs:
+            self._capture(io, key, step + 1)
+        applied = bool(applied)
+        skipped = not applied
+        if applied:
+            self.applied_steps += 1
+        else:
+            self.skip_count += 1
+        dt = time.perf_counter() - t0
+        count = int(count)
+        return StepMetrics(step=step, loss=loss / max(count, 1), tokens=count,
+                           accuracy=correct / max(count, 1),
+                           tokens_per_sec=count / dt if dt > 0 else 0.0,
+                           arena_high_water=self.arena.high_water, skipped=skipped,
+                           nonfinite=int(nonfinite) if np.isfinite(loss) else 0)
+
+    def evaluate(self, n_batches: int = 8) -> float:
+        """Teacher-forced next-token accuracy on fresh batches, dropout off."""
+        correct = total = 0
+        for i in range(n_batches):
+            batch = self.task.batch(EVAL_STEP_BASE + i)
+            key = ("eval",) + tuple(np.asarray(batch.src).shape)
+            self.arena.begin(key)
+            out = self.model.forward_backward(self.pviews, batch, p_drop=0.0,
+                                              alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
+                                              step=EVAL_STEP_BASE + i, arena=self.arena,
+                                              compute_grads=False)
+            self.arena.end()
+            correct += out.correct
+            total += out.token_count
+        return correct / max(total, 1)
+
+    # -- checkpointing (F/engine.py:189-208, F/checkpoint.py) ----------------------------
+
+    def checkpoint_tensors(self):
+        torch.cuda.synchronize()
+        tensors = [("params16", self.ws.params16.cpu().numpy()),
+                   ("moments_m", self.ws.m32.cpu().numpy())]
+        if self.ws.v32 is not None:
+            tensors.append(("moments_v", self.ws.v32.cpu().numpy()))
+        tensors.append(("applied_steps", np.array([self.applied_steps], dtype=np.float32)))
+        return tensors
+
+    def save(self, path: str, step: int) -> None:
+        ckpt.save_checkpoint(path, step, self.checkpoint_tensors())
+
+    def restore(self, path: str) -> int:
+        step, tensors = ckpt.load_checkpoint(path)
+        if tensors["params16"].size != self.ws.n_elements:
+            raise DataError("checkpoint parameter count does not match the model")
+        self.ws.params16.copy_(torch.from_numpy(tensors["params16"]).to(self.device))
+        self.ws.m32.copy_(torch.from_numpy(tensors["moments_m"]).to(self.device))
+        if self.ws.v32 is not None:
+            self.ws.v32.copy_(torch.from_numpy(tensors["moments_v"]).to(self.device))
+        self.applied_steps = int(tensors["applied_steps"][0])
+        self._applied_dev.fill_(self.applied_steps)
+        return step

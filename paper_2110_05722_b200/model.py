@@ -452,15 +452,16 @@ class SeedTable:
         n = len(self.values)
         if n > self.host.numel():
             raise ShapeMismatch("seed table overflow")
-        self.write_host()
+        capturing = torch.cuda.is_current_stream_capturing()
+        self.write_host(sync=not capturing)
         self.dev[:n].copy_(self.host[:n], non_blocking=True)
-        if not torch.cuda.is_current_stream_capturing():
+        if not capturing:
             self._evt = torch.cuda.Event()
             self._evt.record()
 
-    def write_host(self):
+    def write_host(self, sync: bool = True):
         """Fill the pinned staging buffer (waits until the previous copy ran)."""
-        if self._evt is not None:
+        if sync and self._evt is not None:
             self._evt.synchronize()
         n = len(self.values)
         vals = np.array([v - (1 << 64) if v >= (1 << 63) else v for v in self.values], dtype=np.int64)
@@ -860,6 +861,24 @@ class Transformer:
             self._seeds = SeedTable(device)
         return self._seeds
 
+    def register_seeds(self, seeds: SeedTable, seed: int, step: int, p_drop: float):
+        """Per-site dropout seeds of one step in a fixed slot order
+        (F/model.py:868-898 seed derivations: (seed,step,0..3), then site, k)."""
+        cfg = self.cfg
+        seeds.reset()
+        s_src = seeds.slot(derive_seed(seed, step, 0))
+        enc_seed = _LayerSeed(seeds, derive_seed(seed, step, 1))
+        s_tgt = seeds.slot(derive_seed(seed, step, 2))
+        dec_seed = _LayerSeed(seeds, derive_seed(seed, step, 3))
+        if p_drop > 0.0:
+            for i in range(cfg.n_enc):
+                for k in range(3):
+                    enc_seed.site(i, k)
+            for i in range(cfg.n_dec):
+                for k in range(4):
+                    dec_seed.site(i, k)
+        return s_src, enc_seed, s_tgt, dec_seed
+
     def forward_backward(self, params, batch: Batch, *, p_drop=0.0, alpha=0.0, seed=0, step=0,
                          arena=None, sink: GradSink | None = None, compute_grads=True,
                          grad_scale=1.0, trace=None, strategy=None, capture: dict | None = None,
@@ -895,20 +914,9 @@ class Transformer:
         cross_mask = AttentionMask("padding", src_len)
 
         seeds = self.seed_table(ctx.device)
-        seeds.reset()
-        s_src = seeds.slot(derive_seed(seed, step, 0))
-        enc_seed = _LayerSeed(seeds, derive_seed(seed, step, 1))
-        s_tgt = seeds.slot(derive_seed(seed, step, 2))
-        dec_seed = _LayerSeed(seeds, derive_seed(seed, step, 3))
-        if p_drop > 0.0:
-            for i in range(cfg.n_enc):
-                for k in range(3):
-                    enc_seed.site(i, k)
-            for i in range(cfg.n_dec):
-                for k in range(4):
-                    dec_seed.site(i, k)
-            if upload_seeds:
-                seeds.upload()
+        s_src, enc_seed, s_tgt, dec_seed = self.register_seeds(seeds, seed, step, p_drop)
+        if p_drop > 0.0 and upload_seeds:
+            seeds.upload()
 
         # --- forward: encoder ---
         h = arena.alloc((b, ls, d), dt)

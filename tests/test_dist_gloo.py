@@ -1,0 +1,112 @@
+"""Data-parallel semantics on CPU with gloo (world_size 2, 127.0.0.1).
+
+Each rank runs the oracle step on its half of the batch and then the exact DP
+recipe of paper_2110_05722_b200.dist / engine._update:
+  totals all-reduce -> scale by loss_scale / GLOBAL token count -> fp16 narrow
+  -> bucketed fp16 all-reduce (reverse order) -> global non-finite check -> Adam.
+The 2-rank result must equal the 1-rank step on the concatenated batch within
+fp16 tolerance, and both ranks must hold bit-identical parameters.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lsport as O
+
+CFG = dict(n_enc=1, n_dec=1, d=16, heads=4, dff=24, vocab=19, max_len=8)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _setup():
+    shapes = O.model_param_shapes(CFG["n_enc"], CFG["n_dec"], CFG["d"], CFG["dff"], CFG["vocab"],
+                                  CFG["max_len"])
+    init = O.model_init(shapes, 3)
+    p16 = np.concatenate([O.to_half(init[n].reshape(-1)) for n, _ in shapes])
+    rng = np.random.default_rng(9)
+    b, l = 4, 6
+    batch = (rng.integers(2, 19, (b, l)), rng.integers(2, 19, (b, l)), rng.integers(2, 19, (b, l)),
+             np.array([6, 5, 3, 6]))
+    batch[2][1, 4:] = 0      # some pad targets: per-rank token counts differ
+    model = O.OracleTransformer(CFG["n_enc"], CFG["n_dec"], CFG["d"], CFG["heads"], CFG["dff"],
+                                CFG["vocab"], CFG["max_len"])
+    return shapes, p16, batch, model
+
+
+def _grads(model, shapes, p16, batch):
+    P, off = {}, 0
+    for name, shp in shapes:
+        n = int(np.prod(shp))
+        P[name] = p16[off:off + n].reshape(shp)
+        off += n
+    src, tin, tout, lens = batch
+    loss, cnt, _, G = model.forward_backward(P, src, tin, tout, lens, pad_id=0, p=0.0, alpha=0.1)
+    return loss, cnt, np.concatenate([np.asarray(G[n], np.float32).reshape(-1) for n, _ in shapes])
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_05722_b200.dist import DataParallel
+    dp = DataParallel(bucket_bytes=512)        # many buckets
+    shapes, p16, batch, model = _setup()
+    half = [x[rank * 2:(rank + 1) * 2] for x in batch]
+    loss, cnt, acc = _grads(model, shapes, p16, half)
+    totals = torch.tensor([loss, float(cnt), 0.0], dtype=torch.float64)
+    dp.allreduce_totals(totals)
+    scale = np.float32(4.0 / totals[1].item())          # loss_scale 4 / global count
+    g16 = torch.from_numpy(O.to_half(acc * scale))
+    dp.allreduce_grads(g16)
+    m = np.zeros(p16.size, np.float32)
+    v = np.zeros(p16.size, np.float32)
+    bad = O.adam_flat(p16, g16.numpy(), m, v, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0,
+                      loss_scale=4.0, t=1)
+    out_q.put((rank, totals.numpy().tolist(), p16.copy(), bad, dp.buckets(p16.size)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_step_equals_one_rank_step():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, tot0, p0, bad0, buckets), (_, tot1, p1, bad1, _) = res
+    assert bad0 == bad1 == 0
+    assert np.array_equal(p0.view(np.uint16), p1.view(np.uint16))   # identical replicas
+    assert tot0 == tot1
+    # buckets: contiguous cover in reverse layout order
+    spans = sorted(buckets)
+    assert spans[0][0] == 0 and spans[-1][1] == p0.size and buckets[0][1] == p0.size
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    # single-rank reference on the concatenated batch
+    shapes, p16, batch, model = _setup()
+    loss, cnt, acc = _grads(model, shapes, p16, batch)
+    assert cnt == int(tot0[1]) and abs(loss - tot0[0]) <= 1e-5 * abs(loss)
+    g16 = O.to_half(acc * np.float32(4.0 / cnt))
+    m = np.zeros(p16.size, np.float32)
+    v = np.zeros(p16.size, np.float32)
+    O.adam_flat(p16, g16, m, v, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0,
+                loss_scale=4.0, t=1)
+    diff = np.abs(p0.astype(np.float32) - p16.astype(np.float32))
+    assert diff.max() <= 2e-2 * max(1.0, np.abs(p16.astype(np.float32)).max())
+    assert np.mean(p0 != p16) < 0.2

@@ -1,0 +1,247 @@
+"""GPU parity of the model composition, workspace step and engine against the
+reference's golden vectors (tests/golden/model.npz) and the CPU oracle.
+
+f64: grads within 1e-9 of the reference (the reference's own model-vs-oracle
+bar, pkg/tests/test_model.py:228-242); f32: 1e-5 relative; fp16 activations:
+2e-2 relative (BASELINE.json north star).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import lsport as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2110_05722_b200 import model as M
+    from paper_2110_05722_b200 import trainer as T
+    from paper_2110_05722_b200 import _lib
+    from paper_2110_05722_b200.config import RunConfig, TrainConfig
+    from paper_2110_05722_b200.engine import TrainingEngine
+    from paper_2110_05722_b200.errors import IncompleteGradientSet
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def tiny_golden_cfg():
+    return M.ModelConfig(n_enc=2, n_dec=2, d_model=16, n_heads=4, d_ff=24, vocab=19, max_len=8)
+
+
+def _golden_batch(gm):
+    return M.Batch(gm["src"], gm["tgt_in"], gm["tgt_out"], gm["src_len"], 0)
+
+
+def test_init_params_bit_identical(golden_model):
+    cfg = tiny_golden_cfg()
+    init = M.init_params(cfg, seed=3)
+    for name, _ in M.param_spec(cfg):
+        assert np.array_equal(H(init[name]), golden_model[f"init_{name}"]), name
+
+
+@pytest.mark.parametrize("tag,dt,tol", [("f64", torch.float64, 1e-9), ("f32", torch.float32, 2e-5)])
+def test_model_forward_backward_golden(golden_model, tag, dt, tol):
+    gm = golden_model
+    cfg = tiny_golden_cfg()
+    tf = M.Transformer(cfg)
+    params = {k: v.to(dt) for k, v in M.init_params(cfg, seed=3).items()}
+    sink = M.GradSink()
+    cap = {}
+    out = tf.forward_backward(params, _golden_batch(gm), p_drop=0.2, alpha=0.1, seed=11, step=4,
+                              sink=sink, capture=cap)
+    want = gm[f"{tag}_out"]
+    assert out.token_count == want[1] and out.correct == want[2]
+    assert abs(out.loss_sum - want[0]) <= tol * abs(want[0])
+    assert rel_err(H(cap["logq"]), gm[f"{tag}_logq"], 1.0) < tol
+    for name, _ in M.param_spec(cfg):
+        ref = gm[f"{tag}_g_{name}"]
+        got = H(sink.store[name])
+        assert np.abs(got - ref).max() <= tol * max(1.0, np.abs(ref).max()), name
+
+
+def test_view_sink_writes_match_dict_sink(golden_model):
+    """Direct workspace writes (_ViewSink) == staged adds (GradSink)."""
+    gm = golden_model
+    cfg = tiny_golden_cfg()
+    tf = M.Transformer(cfg)
+    params = {k: v.to(torch.float64) for k, v in M.init_params(cfg, seed=3).items()}
+    views = {k: torch.full_like(v, 123.0) for k, v in params.items()}
+    tf.forward_backward(params, _golden_batch(gm), p_drop=0.2, alpha=0.1, seed=11, step=4,
+                        sink=M._ViewSink(views))
+    for name, _ in M.param_spec(cfg):
+        ref = gm[f"f64_g_{name}"]
+        assert np.abs(H(views[name]) - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), name
+
+
+def test_workspace_engine_steps_vs_reference(golden_model):
+    """Engine arithmetic (grad_acc * f32(ls/count) -> narrow -> Adam) on an fp16
+    workspace with f32 activations, vs the reference engine's params16."""
+    gm = golden_model
+    cfg = tiny_golden_cfg()
+    tf = M.Transformer(cfg, compute_dtype=torch.float32)
+    init = M.init_params(cfg, seed=3)
+    ws = T.workspace_pack([(n, init[n]) for n in tf.param_names], "adam")
+    pv = ws.param_views()
+    acc = torch.zeros(ws.n_elements, device="cuda")
+    gv = {lk.name: acc[lk.offset:lk.offset + lk.length].view(lk.shape) for lk in ws.links}
+    ocfg = T.OptimConfig(lr=2e-3, loss_scale=4.0)
+    for step in range(3):
+        out = tf.forward_backward(pv, _golden_batch(gm), p_drop=0.1, alpha=0.1, seed=7, step=step,
+                                  sink=M._ViewSink(gv))
+        want = gm[f"eng_loss_{step}"]
+        assert abs(out.loss_sum - want[0]) <= 1e-5 * abs(want[0])
+        _lib.call("ls2_scale_narrow", acc.data_ptr(), ws.grads16.data_ptr(), ws.n_elements, 4.0,
+                  out.out3.data_ptr(), -1, 1.0, None, _lib.stream_handle())
+        g16 = H(ws.grads16).astype(np.float32)
+        ref_g = gm[f"eng_g16_{step}"].astype(np.float32)
+        assert np.abs(g16 - ref_g).max() <= 2e-3 * max(1.0, np.abs(ref_g).max())
+        T.adam_step(ws, ocfg, step + 1)
+        ref = gm[f"eng_p16_{step}"].astype(np.float32)
+        mine = H(ws.params16).astype(np.float32)
+        assert np.mean(mine != ref) < 2e-2
+        assert np.abs(mine - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max())
+
+
+def _tbase_layer_inputs(b=8, l=64, d=512, seed=0):
+    rng = np.random.default_rng(seed)
+    return rng.normal(size=(b, l, d)).astype(np.float32), rng.normal(size=(b, l, d)).astype(np.float32)
+
+
+def test_encoder_layer_fp16_vs_oracle_tbase_dims():
+    """Config 1 of BASELINE.json (one encoder layer, B8 x L64, d512, h8, f2048),
+    fp16 storage vs the f32 oracle with identical dropout masks (p=0.1)."""
+    cfg = M.ModelConfig(n_enc=1, n_dec=1, d_model=512, n_heads=8, d_ff=2048, vocab=64, max_len=64)
+    init = M.init_params(cfg, seed=0)
+    x, dy = _tbase_layer_inputs()
+    params16 = {k: v.half() for k, v in init.items()}
+    w = M.EncoderLayerWeights.from_params(params16, "enc0.")
+    lens = np.array([64, 60, 33, 64, 1, 64, 48, 64])
+    mask = M.AttentionMask("padding", torch.tensor(lens, device="cuda"))
+    y, stash = M.encoder_layer_forward(torch.tensor(x, device="cuda").half(), w, mask, 0.1, 99,
+                                       n_heads=8)
+    sink = M.GradSink()
+    dx = M.encoder_layer_backward(torch.tensor(dy, device="cuda").half(), w, stash, sink,
+                                  n_heads=8, p_drop=0.1, param_prefix="enc0.")
+    P = {k: v.float().cpu().numpy() for k, v in params16.items()}
+    ora = O.OracleTransformer(1, 1, 512, 8, 2048, 64, 64)
+    yo, c = ora.enc_fwd(x.astype(np.float16).astype(np.float32), P, "enc0.",
+                        O.pad_keep(lens, 64, 64), 0.1, 99, 0, np.float32)
+    G = {}
+    dxo = ora.enc_bwd(dy.astype(np.float16).astype(np.float32), c, P, "enc0.", 0.1, G, np.float32)
+    assert np.abs(H(y).astype(np.float32) - yo).max() <= 2e-2 * np.abs(yo).max()
+    assert np.abs(H(dx).astype(np.float32) - dxo).max() <= 2e-2 * np.abs(dxo).max()
+    for name, ref in G.items():
+        got = H(sink.store[name])
+        assert np.abs(got - ref).max() <= 2e-2 * max(1e-3, np.abs(ref).max()), name
+
+
+def test_packed_kv_and_ordering():
+    cfg = M.ModelConfig(n_enc=1, n_dec=2, d_model=8, n_heads=2, d_ff=16, vocab=11, max_len=6)
+    tf = M.Transformer(cfg)
+    params = tf.init_params(seed=1)
+    rng = np.random.default_rng(5)
+    batch = M.Batch(rng.integers(2, 11, (2, 5)), rng.integers(2, 11, (2, 5)),
+                    rng.integers(2, 11, (2, 5)), np.array([5, 4]), 0)
+    trace = []
+    tf.forward_backward(params, batch, sink=M.GradSink(), trace=trace)
+    assert trace.index(("enc_out_grad_emitted",)) > trace.index(("dec_layer_backward_done", 0))
+    pw = M.pack_cross_weights([np.array([[2.0]])], [np.array([[4.0]])], [np.zeros(1)], [np.zeros(1)])
+    x = np.full((1, 3, 1), 1.0)
+    dx, dw, db = M.packed_kv_backward([np.ones((1, 3, 1))], [np.ones((1, 3, 1))], x, pw)
+    assert np.allclose(H(dx), 6.0) and np.allclose(H(dw).ravel(), [3.0, 3.0])
+    assert np.allclose(H(db).ravel(), [3.0, 3.0])
+    with pytest.raises(IncompleteGradientSet):
+        M.packed_kv_backward([np.zeros((1, 1, 1)), None], [np.zeros((1, 1, 1))] * 2,
+                             np.zeros((1, 1, 1)), M.pack_cross_weights([np.eye(1)] * 2, [np.eye(1)] * 2,
+                                                                       [np.zeros(1)] * 2, [np.zeros(1)] * 2))
+
+
+def test_padding_positions_do_not_affect_loss_or_grads():
+    cfg = M.ModelConfig(n_enc=1, n_dec=1, d_model=8, n_heads=2, d_ff=16, vocab=11, max_len=6)
+    tf = M.Transformer(cfg)
+    params = {k: v.double() for k, v in tf.init_params(seed=4).items()}
+    rng = np.random.default_rng(11)
+    src = rng.integers(2, 11, (2, 5))
+    batch = M.Batch(src, rng.integers(2, 11, (2, 5)), rng.integers(2, 11, (2, 5)),
+                    np.array([3, 2]), 0)
+    s1 = M.GradSink()
+    o1 = tf.forward_backward(params, batch, alpha=0.1, sink=s1)
+    src2 = src.copy()
+    src2[0, 3:] = 7
+    src2[1, 2:] = 7
+    s2 = M.GradSink()
+    o2 = tf.forward_backward(params, M.Batch(src2, batch.tgt_in, batch.tgt_out, batch.src_len, 0),
+                             alpha=0.1, sink=s2)
+    assert o1.loss_sum == o2.loss_sum
+    for name in s1.store:
+        if name != "tok_emb":
+            assert torch.equal(s1.store[name], s2.store[name]), name
+
+
+def _tiny_run(graphs: bool, steps: int, p_drop=0.1):
+    run = RunConfig()
+    run.train.p_drop = p_drop
+    run.train.cuda_graphs = graphs
+    run.train.steps = steps
+    eng = TrainingEngine(run)
+    eng.setup_arena()
+    ms = [eng.train_step(s) for s in range(steps)]
+    return eng, ms
+
+
+def test_engine_graph_replay_matches_eager():
+    e1, m1 = _tiny_run(False, 12)
+    e2, m2 = _tiny_run(True, 12)
+    assert e2._graphs, "graphs were captured"
+    for a, b in zip(m1, m2):
+        assert abs(a.loss - b.loss) <= 1e-3 * max(1.0, abs(a.loss)), (a.step, a.loss, b.loss)
+    p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
+    assert np.abs(p1 - p2).max() <= 2e-2
+    assert e2.arena.realloc_count == 0 and e2.arena.high_water <= e2.capacity
+
+
+def test_engine_learns_copy_task():
+    run = RunConfig()
+    run.train.steps = 400
+    eng = TrainingEngine(run)
+    eng.setup_arena()
+    losses = [eng.train_step(s).loss for s in range(400)]
+    assert np.mean(losses[-20:]) < 0.5 * np.mean(losses[:20])
+    assert eng.evaluate() > 0.5
+
+
+def test_checkpoint_resume_bit_exact(tmp_path):
+    run = RunConfig()
+    run.train.p_drop = 0.1
+    a = TrainingEngine(run)
+    a.setup_arena()
+    for s in range(6):
+        a.train_step(s)
+    a.save(str(tmp_path / "c.bin"), 6)
+    for s in range(6, 10):
+        a.train_step(s)
+    b = TrainingEngine(run)
+    b.setup_arena()
+    assert b.restore(str(tmp_path / "c.bin")) == 6
+    for s in range(6, 10):
+        b.train_step(s)
+    pa, pb = H(a.ws.params16).astype(np.float32), H(b.ws.params16).astype(np.float32)
+    assert np.abs(pa - pb).max() <= 2e-3     # atomics only
+
+
+def test_tbase_step_runs_and_is_finite():
+    from paper_2110_05722_b200.config import transformer_base
+    from paper_2110_05722_b200.data import FixedShapeTask
+    run = RunConfig(model=transformer_base(), train=TrainConfig(p_drop=0.1, batch_tokens=4096))
+    eng = TrainingEngine(run, task=FixedShapeTask(64, 64, 32000))
+    eng.setup_arena()
+    ms = [eng.train_step(s) for s in range(4)]
+    assert all(np.isfinite(m.loss) for m in ms) and ms[0].tokens == 4096
+    assert abs(ms[0].loss - math.log(32000)) < 1.0
+    assert not ms[-1].skipped
