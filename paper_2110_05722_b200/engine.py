@@ -12,6 +12,7 @@ on the device, so a skipped step needs no extra host round trip.
 
 from __future__ import annotations
 
+import gc
 import time
 from dataclasses import dataclass
 
@@ -29,6 +30,22 @@ from .model import Batch, Transformer, _ViewSink, validate_batch
 from .trainer import OptimConfig, Workspace, _state, workspace_pack
 
 EVAL_STEP_BASE = 1 << 30
+
+
+class _no_gc:
+    """Collect garbage first, then keep the collector off while a CUDA graph is
+    being captured: destroying another (dead) graph mid-capture invalidates it."""
+
+    def __enter__(self):
+        torch.cuda.synchronize()
+        gc.collect()
+        self._was = gc.isenabled()
+        gc.disable()
+
+    def __exit__(self, *a):
+        if self._was:
+            gc.enable()
+        torch.cuda.synchronize()
 
 
 @dataclass
@@ -184,12 +201,12 @@ class TrainingEngine:
         launches (cuBLAS kernels not counted)."""
         b, l = key[1], key[2]
         io = self._io_for(b, l)
-        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
-        with torch.cuda.graph(g):
-            out3 = self._fwd_bwd(io, key, 0, upload=False)
-            self._update(out3, host_copy=False)
+        with _no_gc():
+            with torch.cuda.graph(g):
+                out3 = self._fwd_bwd(io, key, 0, upload=False)
+                self._update(out3, host_copy=False)
         self._launches[key] = _lib.launches() - n0
         torch.cuda.synchronize()
         return g
@@ -256,11 +273,11 @@ class TrainingEngine:
         """Capture fwd/bwd + update of this bucket into one CUDA graph."""
         if self.dp.active:
             return  # collectives stay eager under DP (see DESIGN.md)
-        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            out3 = self._fwd_bwd(io, key, step)
-            self._update(out3)
+        with _no_gc():
+            with torch.cuda.graph(g):
+                out3 = self._fwd_bwd(io, key, step)
+                self._update(out3)
         self._graphs[key] = g
         torch.cuda.synchronize()
 

@@ -969,8 +969,7 @@ class Transformer:
         out3 = torch.empty(3, dtype=torch.float64, device=ctx.device)
         logq = None
         if capture is not None:
-            logq = torch.empty((rt, v), dtype=dt if dt != torch.float64 else torch.float32,
-                               device=ctx.device)
+            logq = torch.empty((rt, v), dtype=dt, device=ctx.device)
         if dt == torch.float64:
             self._criterion_f64(logits, tgt_out, out3, alpha, batch.pad_id, grad_scale,
                                 compute_grads, logq)

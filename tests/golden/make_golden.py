@@ -217,7 +217,19 @@ def main():
         mout[f"eng_p16_{step}"] = ws.params16.copy()
         mout[f"eng_loss_{step}"] = np.array([o.loss_sum, o.token_count, o.correct])
     np.savez_compressed(os.path.join(OUT, "model.npz"), **mout)
-    print("wrote", os.path.join(OUT, "ops.npz"), os.path.join(OUT, "model.npz"))
+
+    # --- default-config training trajectory (F/engine.py, copy task, 400 steps) --
+    from ftrain.config import RunConfig
+    from ftrain.engine import TrainingEngine
+    run = RunConfig()
+    run.train.p_drop = 0.1
+    eng = TrainingEngine(run)
+    eng.setup_arena()
+    losses = [eng.train_step(s).loss for s in range(400)]
+    np.savez_compressed(os.path.join(OUT, "traj.npz"), losses=np.array(losses),
+                        eval_acc=np.array([eng.evaluate()]))
+    print("wrote", os.path.join(OUT, "ops.npz"), os.path.join(OUT, "model.npz"),
+          os.path.join(OUT, "traj.npz"))
 
 
 if __name__ == "__main__":

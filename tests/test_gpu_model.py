@@ -136,9 +136,15 @@ def test_encoder_layer_fp16_vs_oracle_tbase_dims():
     dxo = ora.enc_bwd(dy.astype(np.float16).astype(np.float32), c, P, "enc0.", 0.1, G, np.float32)
     assert np.abs(H(y).astype(np.float32) - yo).max() <= 2e-2 * np.abs(yo).max()
     assert np.abs(H(dx).astype(np.float32) - dxo).max() <= 2e-2 * np.abs(dxo).max()
+    errs = {}
     for name, ref in G.items():
-        got = H(sink.store[name])
-        assert np.abs(got - ref).max() <= 2e-2 * max(1e-3, np.abs(ref).max()), name
+        got = H(sink.store[name]).astype(np.float64)
+        errs[name] = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-12)
+    # Normwise 2e-2 everywhere except the relu bias: its column sums inherit sign
+    # flips of (x + b1) for pre-activations within fp16 rounding of 0 (the oracle
+    # keeps u2 in f32), a few O(|dz|) terms per column -> a few percent.
+    for name, e in errs.items():
+        assert e <= (6e-2 if name.endswith("ffn.b1") else 2e-2), (name, e, errs)
 
 
 def test_packed_kv_and_ordering():
@@ -206,14 +212,24 @@ def test_engine_graph_replay_matches_eager():
     assert e2.arena.realloc_count == 0 and e2.arena.high_water <= e2.capacity
 
 
-def test_engine_learns_copy_task():
+def test_engine_trajectory_tracks_reference():
+    """400 steps of the default copy-task job (p_drop 0.1) vs the reference
+    engine's own trajectory (tests/golden/traj.npz): same batches, same dropout
+    masks; fp16 workspace both sides, fp16 activations here."""
+    import os
+    from conftest import GOLDEN
+    ref = np.load(os.path.join(GOLDEN, "traj.npz"))
     run = RunConfig()
-    run.train.steps = 400
+    run.train.p_drop = 0.1
     eng = TrainingEngine(run)
     eng.setup_arena()
-    losses = [eng.train_step(s).loss for s in range(400)]
-    assert np.mean(losses[-20:]) < 0.5 * np.mean(losses[:20])
-    assert eng.evaluate() > 0.5
+    losses = np.array([eng.train_step(s).loss for s in range(400)])
+    want = ref["losses"]
+    assert abs(losses[0] - want[0]) <= 2e-3 * want[0]
+    for a in range(0, 400, 50):
+        got_w, want_w = losses[a:a + 50].mean(), want[a:a + 50].mean()
+        assert abs(got_w - want_w) <= 3e-2 * want_w, (a, got_w, want_w)
+    assert abs(eng.evaluate() - float(ref["eval_acc"][0])) <= 0.06
 
 
 def test_checkpoint_resume_bit_exact(tmp_path):
