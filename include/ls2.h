@@ -185,9 +185,16 @@ int ls2_gemm(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
              double alpha, const void* A, int64_t lda, int64_t sA1, int64_t sA2,
              const void* B, int64_t ldb, int64_t sB1, int64_t sB2, double beta, void* C,
              int64_t ldc, int64_t sC1, int64_t sC2, int64_t n1, int64_t n2, int tab, int tc,
-             void* ptr_scratch, void* stream);
-/* bytes of device scratch ls2_gemm needs for pointer-array batches */
+             void* ptr_scratch, int ptrs_ready, void* stream);
+/* bytes of device scratch ls2_gemm needs for pointer-array batches
+ * (ptrs_ready=1: the caller guarantees ptr_scratch already holds this call's
+ *  A/B/C pointer arrays, e.g. cached per static arena address) */
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2);
+/* plain GEMM on cuBLASLt with an optional fused bias epilogue (C += bias[n] per row);
+ * LS2_ERR_CUBLAS if no Lt algorithm supports the combination (caller falls back) */
+int ls2_gemm_lt(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+                const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                int64_t ldc, const void* bias, int tab, int tc, void* stream);
 
 #ifdef __cplusplus
 }

@@ -63,7 +63,8 @@ _SIGS = {
     "ls2_count_nonfinite_f16": [P, L, P, P],
     "ls2_blas_create": [],
     "ls2_blas_destroy": [P],
-    "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, P],
+    "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, I, P],
+    "ls2_gemm_lt": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, P],
     "ls2_gemm_scratch_bytes": [L, L],
 }
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,
@@ -151,6 +152,8 @@ class DeviceContext:
             raise DeviceError("cuBLAS init failed: " + _lib.ls2_last_error().decode())
         self._scratch: dict[str, torch.Tensor] = {}
         self._keep: list[torch.Tensor] = []
+        self.ptr_cache: dict = {}        # pointer arrays of pointer-array GEMM batches
+        self.lt_unsupported: set = set()  # cuBLASLt keys that fell back
 
     def scratch(self, name: str, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)

@@ -59,6 +59,7 @@ def _link_flags():
         if cublas:
             break
     lib = ["-Xlinker", "-l:" + os.path.basename(cublas)] if cublas else ["-lcublas"]
+    lib += ["-Xlinker", "-l:libcublasLt.so.12"]
     return rp + ldirs + lib + ["-cudart", "shared"]
 
 

@@ -63,7 +63,7 @@ __device__ T block_sum(T v) {
 // ITERS > 0: register-cached single pass (8*ITERS elements per thread);
 // ITERS == 0: two passes over the row.
 template <typename T, int ITERS>
-__global__ void __launch_bounds__(kCeThreads) criterion_kernel(
+__global__ void __launch_bounds__(kCeThreads, 2) criterion_kernel(
     const T* __restrict__ logits, const int64_t* __restrict__ targets, T* dlogits, T* logq_out,
     double* __restrict__ row_stats, int* __restrict__ bad_target, int64_t rows, int64_t V,
     double alpha, int64_t pad_id, int has_pad, double grad_scale) {
@@ -75,19 +75,23 @@ __global__ void __launch_bounds__(kCeThreads) criterion_kernel(
   const bool tgt_ok = tgt >= 0 && tgt < V;
   if (valid && !tgt_ok && threadIdx.x == 0 && bad_target) *bad_target = 1;
 
-  float cache[ITERS > 0 ? ITERS : 1][8];
+  // the row stays in registers in its storage type (16-bit: 4 regs per 8 values)
+  Pack8<T> cache[ITERS > 0 ? ITERS : 1];
   MaxIdx mi{-INFINITY, INT64_MAX};
   float sh = 0.f;
   if (ITERS > 0) {
 #pragma unroll
     for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
       const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
+      if (c0 < V) cache[it] = ld8_stream(h + c0);
+    }
+#pragma unroll
+    for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
+      const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
       if (c0 < V) {
-        Pack8<T> q = ld8_stream(h + c0);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float v = cvt<float>(q.v[e]);
-          cache[it][e] = v;
+          const float v = cvt<float>(cache[it].v[e]);
           sh += v;
           mi_merge(mi, MaxIdx{v, c0 + e});
         }
@@ -109,10 +113,7 @@ __global__ void __launch_bounds__(kCeThreads) criterion_kernel(
       const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
       if (c0 < V) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          cache[it][e] = __expf(cache[it][e] - mx);  // now exp(h - max)
-          z += cache[it][e];
-        }
+        for (int e = 0; e < 8; ++e) z += __expf(cvt<float>(cache[it].v[e]) - mx);
       }
     }
   } else {
@@ -144,14 +145,14 @@ __global__ void __launch_bounds__(kCeThreads) criterion_kernel(
         if (logq_out) {
           Pack8<T> q;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) q.v[e] = cvt<T>(__logf(cache[it][e]) - lz);
+          for (int e = 0; e < 8; ++e) q.v[e] = cvt<T>((cvt<float>(cache[it].v[e]) - mx) - lz);
           st8(logq_out + r * V + c0, q);
         }
         if (dlogits) {
           Pack8<T> q;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            float g = cache[it][e] * rz - a_v;
+            float g = __expf(cvt<float>(cache[it].v[e]) - mx) * rz - a_v;
             if (c0 + e == tgt) g -= one_m_a;
             q.v[e] = cvt<T>(valid ? g * gs : 0.f);
           }

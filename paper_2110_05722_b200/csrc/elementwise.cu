@@ -75,13 +75,33 @@ __device__ __forceinline__ void store_row_group(T* p, const C (&v)[8]) {
 // ---------------------------------------------------------------------------
 // column-sum stage 2: out[c] (+)= sum_g partial[g, c] in fixed order
 // ---------------------------------------------------------------------------
+// CTA = 8 warps x 32 columns; warp w sums partial rows w, w+8, ... (coalesced
+// 256-byte row segments, 4 loads in flight), then the 8 warp sums are added in
+// fixed order -> deterministic and ~nblk/32 dependent L2 round trips.
 template <typename Tout>
-__global__ void colsum_finish_kernel(const double* __restrict__ partial, int nblk, int64_t cols,
-                                     Tout* __restrict__ out, int beta) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int g = 0; g < nblk; ++g) s += partial[(int64_t)g * cols + c];
+__global__ void __launch_bounds__(256) colsum_finish_kernel(const double* __restrict__ partial,
+                                                            int nblk, int64_t cols,
+                                                            Tout* __restrict__ out, int beta) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  if (c < cols) {
+    int g = w;
+    for (; g + 24 < nblk; g += 32) {
+      s0 += partial[(int64_t)g * cols + c];
+      s1 += partial[(int64_t)(g + 8) * cols + c];
+      s2 += partial[(int64_t)(g + 16) * cols + c];
+      s3 += partial[(int64_t)(g + 24) * cols + c];
+    }
+    for (; g < nblk; g += 8) s0 += partial[(int64_t)g * cols + c];
+  }
+  red[w][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][lane];
     if (beta) s += cvt<double>(out[c]);
     out[c] = cvt<Tout>(s);
   }
@@ -90,7 +110,8 @@ __global__ void colsum_finish_kernel(const double* __restrict__ partial, int nbl
 int colsum_finish(const double* partial, int nblk, int64_t cols, void* out, int tout, int beta,
                   cudaStream_t st) {
   return LS2_DISPATCH_ONE(tout, "colsum_finish", [&] {
-    colsum_finish_kernel<Tx><<<grid_for(cols), kTPB, 0, st>>>(partial, nblk, cols, (Tx*)out, beta);
+    colsum_finish_kernel<Tx><<<(unsigned)ceil_div(cols, 32), 256, 0, st>>>(partial, nblk, cols,
+                                                                         (Tx*)out, beta);
     return check_launch("colsum_finish");
   });
 }
@@ -405,8 +426,43 @@ __global__ void bias_add_kernel(T* __restrict__ x, const T* __restrict__ bias, i
     x[i] = cvt<T>(add_rn(cvt<C>(x[i]), cvt<C>(bias[i % cols])));
 }
 
+// vectorized stage 1: same (row lanes x column groups) tiling as the fused tails
+template <typename Tin>
+__global__ void __launch_bounds__(1024) colsum_vec(const Tin* __restrict__ x,
+                                                   double* __restrict__ partial, int64_t rows,
+                                                   int64_t cols, int64_t cgs, int rpp) {
+  using C = typename CompOf<Tin>::type;
+  extern __shared__ double smem[];
+  const int lane_row = (int)(threadIdx.x / cgs);
+  const int64_t cg = threadIdx.x % cgs;
+  C acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0;
+  if (lane_row < rpp) {
+    for (int64_t r = (int64_t)blockIdx.x * rpp + lane_row; r < rows; r += (int64_t)gridDim.x * rpp) {
+      C v[8];
+      load_row_group(x + (r * cgs + cg) * 8, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += v[e];
+    }
+  }
+  cta_colsum_store(acc, cgs, rpp, cols, partial, smem);
+}
+
 inline int colsum_generic(const void* x, int tin, int64_t rows, int64_t cols, void* out, int tout,
                           int beta, void* ws, cudaStream_t st) {
+  if (vec_ok(cols, {x})) {
+    Tiling t = tiling(rows, cols);
+    const int grid = colsum_blocks(t.passes);
+    const size_t sm = (size_t)t.rpp * cols * sizeof(double);
+    int rc = LS2_DISPATCH_ONE(tin, "colsum", [&] {
+      colsum_vec<Tx><<<grid, t.threads, sm, st>>>((const Tx*)x, (double*)ws, rows, cols, t.cgs,
+                                                  t.rpp);
+      return check_launch("colsum_vec");
+    });
+    if (rc) return rc;
+    return colsum_finish((const double*)ws, grid, cols, out, tout, beta, st);
+  }
   const int nblk = colsum_blocks(ceil_div(rows, 16));
   int rc = LS2_DISPATCH_ONE(tin, "colsum", [&] {
     colsum_stage1<Tx><<<nblk, kTPB, 0, st>>>((const Tx*)x, rows, cols, (double*)ws);

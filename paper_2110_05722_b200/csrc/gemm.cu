@@ -8,17 +8,43 @@
 // The pointer-array form lets the attention contractions read Q/K/V directly
 // out of the fused [B, L, 3d] projection and write the context straight into
 // the merged [B, L, d] layout, so no head split/merge copies exist.
+#include <cublasLt.h>
 #include <cublas_v2.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 
 namespace ls2 {
 
+// cuBLASLt plan for one (shape, layout, dtype, epilogue, alignment) key
+struct LtPlan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  cublasLtMatmulAlgo_t algo;
+  bool ok = false;
+};
+
+using LtKey = std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
+                         int, int, int>;
+
 struct Blas {
   cublasHandle_t h = nullptr;
+  cublasLtHandle_t lt = nullptr;
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  std::map<LtKey, LtPlan> plans;
+  std::mutex mu;
 };
+
+inline int align_of(const void* p) {
+  uintptr_t v = reinterpret_cast<uintptr_t>(p);
+  int a = 256;
+  while (a > 1 && (v % a)) a >>= 1;
+  return a;
+}
 
 inline size_t esize(int t) { return t == LS2_F64 ? 8 : t == LS2_F32 ? 4 : 2; }
 inline cudaDataType_t cuda_type(int t) {
@@ -67,6 +93,7 @@ void* ls2_blas_create(void) {
     return nullptr;
   }
   cublasSetWorkspace(b->h, b->ws, b->ws_bytes);
+  if (cublasLtCreate(&b->lt) != CUBLAS_STATUS_SUCCESS) b->lt = nullptr;
   // fp32 compute, no TF32, no reduced-precision split-K reductions
   cublasSetMathMode(b->h, (cublasMath_t)(CUBLAS_DEFAULT_MATH |
                                          CUBLAS_MATH_DISALLOW_REDUCED_PRECISION_REDUCTION));
@@ -76,9 +103,77 @@ void* ls2_blas_create(void) {
 void ls2_blas_destroy(void* p) {
   Blas* b = reinterpret_cast<Blas*>(p);
   if (!b) return;
+  for (auto& kv : b->plans) {
+    LtPlan& p = kv.second;
+    if (p.op) cublasLtMatmulDescDestroy(p.op);
+    if (p.a) cublasLtMatrixLayoutDestroy(p.a);
+    if (p.b) cublasLtMatrixLayoutDestroy(p.b);
+    if (p.c) cublasLtMatrixLayoutDestroy(p.c);
+  }
+  if (b->lt) cublasLtDestroy(b->lt);
   if (b->h) cublasDestroy(b->h);
   if (b->ws) cudaFree(b->ws);
   delete b;
+}
+
+/* C = alpha*op(A)@op(B) + beta*C (+ bias[n] broadcast over rows) on cuBLASLt, row-major.
+ * Returns LS2_ERR_CUBLAS when no Lt algorithm supports the combination (caller falls back). */
+int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+                const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                int64_t ldc, const void* bias, int tab, int tc, void* stream) {
+  Blas* bl = reinterpret_cast<Blas*>(hp);
+  if (!bl || !bl->lt) return fail(LS2_ERR_CUBLAS, "gemm_lt: no cublasLt handle");
+  if (m <= 0 || n <= 0) return LS2_OK;
+  if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_CUBLAS, "gemm_lt: f64 not routed to Lt");
+  const int al = std::min(std::min(align_of(A), align_of(B)), std::min(align_of(C),
+                          bias ? align_of(bias) : 256));
+  LtKey key{trans_a, trans_b, m, n, k, lda, ldb, ldc, tab, tc, bias != nullptr, beta != 0.0, al};
+  LtPlan* plan;
+  {
+    std::lock_guard<std::mutex> g(bl->mu);
+    plan = &bl->plans[key];
+    if (!plan->op) {
+      const cublasOperation_t opA = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;  // Lt A := row-major B
+      const cublasOperation_t opB = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;  // Lt B := row-major A
+      cublasLtMatmulDescCreate(&plan->op, CUBLAS_COMPUTE_32F, CUDA_R_32F);
+      cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_TRANSA, &opA, sizeof(opA));
+      cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_TRANSB, &opB, sizeof(opB));
+      if (bias) {
+        cublasLtEpilogue_t ep = CUBLASLT_EPILOGUE_BIAS;
+        cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof(ep));
+        cudaDataType_t bt = cuda_type(tc);
+        cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt));
+      }
+      const cudaDataType_t tAB = cuda_type(tab), tC = cuda_type(tc);
+      cublasLtMatrixLayoutCreate(&plan->a, tAB, trans_b ? k : n, trans_b ? n : k, ldb);
+      cublasLtMatrixLayoutCreate(&plan->b, tAB, trans_a ? m : k, trans_a ? k : m, lda);
+      cublasLtMatrixLayoutCreate(&plan->c, tC, n, m, ldc);
+      cublasLtMatmulPreference_t pref;
+      cublasLtMatmulPreferenceCreate(&pref);
+      size_t wsb = bl->ws_bytes;
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb));
+      uint32_t a32 = (uint32_t)al;
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &a32, sizeof(a32));
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &a32, sizeof(a32));
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &a32, sizeof(a32));
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &a32, sizeof(a32));
+      cublasLtMatmulHeuristicResult_t res;
+      int found = 0;
+      cublasStatus_t s = cublasLtMatmulAlgoGetHeuristic(bl->lt, plan->op, plan->a, plan->b, plan->c,
+                                                        plan->c, pref, 1, &res, &found);
+      cublasLtMatmulPreferenceDestroy(pref);
+      plan->ok = (s == CUBLAS_STATUS_SUCCESS && found > 0);
+      if (plan->ok) plan->algo = res.algo;
+    }
+  }
+  if (!plan->ok) return fail(LS2_ERR_CUBLAS, "gemm_lt: no algorithm for this combination");
+  if (bias)
+    cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
+  const float af = (float)alpha, bf = (float)beta;
+  cublasStatus_t s = cublasLtMatmul(bl->lt, plan->op, &af, B, plan->a, A, plan->b, &bf, C, plan->c,
+                                    C, plan->c, &plan->algo, bl->ws, bl->ws_bytes,
+                                    as_stream(stream));
+  return s == CUBLAS_STATUS_SUCCESS ? LS2_OK : blas_fail(s, "cublasLtMatmul");
 }
 
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2) { return 3 * n1 * n2 * (int64_t)sizeof(void*); }
@@ -87,7 +182,7 @@ int ls2_gemm(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k
              const void* A, int64_t lda, int64_t sA1, int64_t sA2, const void* B, int64_t ldb,
              int64_t sB1, int64_t sB2, double beta, void* C, int64_t ldc, int64_t sC1,
              int64_t sC2, int64_t n1, int64_t n2, int tab, int tc, void* ptr_scratch,
-             void* stream) {
+             int ptrs_ready, void* stream) {
   Blas* b = reinterpret_cast<Blas*>(hp);
   if (!b) return fail(LS2_ERR_CUBLAS, "gemm: null blas handle");
   if (m <= 0 || n <= 0 || n1 <= 0 || n2 <= 0) return LS2_OK;
@@ -128,11 +223,13 @@ int ls2_gemm(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k
   if (!ptr_scratch) return fail(LS2_ERR_SHAPE, "gemm: pointer-array batch needs scratch");
   const size_t ea = esize(tab), ec = esize(tc);
   const void** ptrs = reinterpret_cast<const void**>(ptr_scratch);
-  fill_ptrs_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
-      (const char*)A, (const char*)B, (char*)C, n2, total, sA1 * ea, sA2 * ea, sB1 * ea, sB2 * ea,
-      sC1 * ec, sC2 * ec, ptrs);
-  int rc = check_launch("gemm_fill_ptrs");
-  if (rc) return rc;
+  if (!ptrs_ready) {  // callers cache the arrays per (addresses, strides): filled once
+    fill_ptrs_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+        (const char*)A, (const char*)B, (char*)C, n2, total, sA1 * ea, sA2 * ea, sB1 * ea,
+        sB2 * ea, sC1 * ec, sC2 * ec, ptrs);
+    int rc = check_launch("gemm_fill_ptrs");
+    if (rc) return rc;
+  }
   s = cublasGemmBatchedEx(b->h, opB, opA, (int)n, (int)m, (int)k, pa, (const void* const*)(ptrs + total),
                           tAB, (int)ldb, (const void* const*)ptrs, tAB, (int)lda, pb,
                           (void* const*)(ptrs + 2 * total), tC, (int)ldc, (int)total, ct,

@@ -16,6 +16,7 @@
 namespace ls2 {
 
 constexpr int kLnWarps = 4;
+constexpr int kLnBwdWarps = 8;
 constexpr int kLnMaxBlocks = 2 * kNumSMs;
 
 template <typename T, typename C>
@@ -144,12 +145,12 @@ __global__ void ln_fwd_block(const Tin* __restrict__ x, const Tin* __restrict__ 
 // backward
 // ---------------------------------------------------------------------------
 template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES>
-__global__ void __launch_bounds__(kLnWarps * 32) ln_bwd_warp(
+__global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
     const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
     const Tstat* __restrict__ mu, const Tstat* __restrict__ sigma, const Tin* __restrict__ dres,
     Tout* __restrict__ dx, double* __restrict__ partial, int64_t rows, int64_t cols) {
   using C = typename CompOf<Tin>::type;
-  __shared__ double red[kLnWarps][2][256];  // per-warp column partials, one chunk at a time
+  __shared__ double red[kLnBwdWarps][2][256];  // per-warp column partials, one chunk at a time
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t cgs = cols / 8;
   C wv[ITERS][8], adw[ITERS][8], adb[ITERS][8];
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_bwd_warp(
     if (g < cgs) ld_group(w + g * 8, wv[it]);
   }
   const C inv_m = (C)(1.0 / (double)cols);
-  for (int64_t r = (int64_t)blockIdx.x * kLnWarps + wid; r < rows;
-       r += (int64_t)gridDim.x * kLnWarps) {
+  for (int64_t r = (int64_t)blockIdx.x * kLnBwdWarps + wid; r < rows;
+       r += (int64_t)gridDim.x * kLnBwdWarps) {
     const C m_r = (C)mu[r];
     const C rs = (C)(1.0 / (double)sigma[r]);
     C xh[ITERS][8], gg[ITERS][8];
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_bwd_warp(
     for (int c = threadIdx.x; c < 256 && base + c < cols; c += blockDim.x) {
       double sw = 0, sb = 0;
 #pragma unroll
-      for (int k = 0; k < kLnWarps; ++k) { sw += red[k][0][c]; sb += red[k][1][c]; }
+      for (int k = 0; k < kLnBwdWarps; ++k) { sw += red[k][0][c]; sb += red[k][1][c]; }
       partial[((int64_t)blockIdx.x * 2 + 0) * cols + base + c] = sw;
       partial[((int64_t)blockIdx.x * 2 + 1) * cols + base + c] = sb;
     }
@@ -284,16 +285,37 @@ __global__ void ln_param_partial(const Tin* __restrict__ dy, const Tin* __restri
   }
 }
 
+// CTA = 8 warps x 32 columns, warp w reduces partial blocks w, w+8, ...;
+// fixed-order combination of the warp sums (deterministic).
 template <typename Tp>
-__global__ void ln_param_finish(const double* __restrict__ partial, int nblk, int64_t cols,
-                                Tp* __restrict__ dw, Tp* __restrict__ db, int beta) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double sw = 0, sb = 0;
-    for (int g = 0; g < nblk; ++g) {
-      sw += partial[((int64_t)g * 2 + 0) * cols + c];
-      sb += partial[((int64_t)g * 2 + 1) * cols + c];
+__global__ void __launch_bounds__(256) ln_param_finish(const double* __restrict__ partial,
+                                                       int nblk, int64_t cols,
+                                                       Tp* __restrict__ dw, Tp* __restrict__ db,
+                                                       int beta) {
+  __shared__ double red[2][8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double sw0 = 0, sw1 = 0, sb0 = 0, sb1 = 0;
+  if (c < cols) {
+    int g = w;
+    for (; g + 8 < nblk; g += 16) {
+      sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
+      sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
+      sw1 += partial[((int64_t)(g + 8) * 2 + 0) * cols + c];
+      sb1 += partial[((int64_t)(g + 8) * 2 + 1) * cols + c];
     }
+    for (; g < nblk; g += 8) {
+      sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
+      sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
+    }
+  }
+  red[0][w][lane] = sw0 + sw1;
+  red[1][w][lane] = sb0 + sb1;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    double sw = 0, sb = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { sw += red[0][k][lane]; sb += red[1][k][lane]; }
     if (beta) { sw += cvt<double>(dw[c]); sb += cvt<double>(db[c]); }
     dw[c] = cvt<Tp>(sw);
     db[c] = cvt<Tp>(sb);
@@ -310,7 +332,7 @@ inline bool ln_vec_ok(int64_t cols, std::initializer_list<const void*> ptrs) {
 inline int ln_iters(int64_t cols) { return cols <= 256 ? 1 : cols <= 512 ? 2 : 4; }
 
 inline int ln_bwd_blocks(int64_t rows) {
-  int64_t g = ceil_div(rows, kLnWarps * 4);
+  int64_t g = ceil_div(rows, kLnBwdWarps * 2);
   return (int)(g < 1 ? 1 : (g > kLnMaxBlocks ? kLnMaxBlocks : g));
 }
 
@@ -372,7 +394,7 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
         auto go = [&](auto iters, auto res) {
           constexpr int I = decltype(iters)::value;
           constexpr bool R = decltype(res)::value;
-          ln_bwd_warp<Tin, Tout, Tstat, I, R><<<nblk, kLnWarps * 32, 0, st>>>(
+          ln_bwd_warp<Tin, Tout, Tstat, I, R><<<nblk, kLnBwdWarps * 32, 0, st>>>(
               (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
               (const Tin*)dres, (Tout*)dx, (double*)ws, rows, cols);
           return check_launch("layernorm_bwd");
@@ -401,7 +423,7 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
   if (rc) return rc;
   if (!dw || !db) return LS2_OK;
   return LS2_DISPATCH_ONE(tparam, "layernorm_param_finish", [&] {
-    ln_param_finish<Tx><<<grid_for(cols), 256, 0, st>>>((const double*)ws, nblk, cols, (Tx*)dw,
+    ln_param_finish<Tx><<<(unsigned)ceil_div(cols, 32), 256, 0, st>>>((const double*)ws, nblk, cols, (Tx*)dw,
                                                          (Tx*)db, beta_param);
     return check_launch("layernorm_param_finish");
   });

@@ -674,11 +674,24 @@ def gemm(a, b, trans_a: bool = False, trans_b: bool = False, accumulate_into=Non
         lv = _joint_levels([av, bv, Cw])
     lc = _mat_layout(Cw)
     (n1, s1), (n2, s2) = lv
-    scratch = ctx.scratch("gemm_ptrs", 3 * n1 * n2 * 8) if n1 * n2 > 1 else None
+    scratch, ready = None, 0
+    collapsible = n1 == 1 or n2 == 1 or all(a == n2 * b for a, b in zip(s1, s2))
+    if not collapsible:
+        # pointer-array batch: arrays cached per (addresses, strides) -> filled once;
+        # the planned arena makes the addresses static, so graph replays reuse them
+        key = (av.data_ptr(), bv.data_ptr(), Cw.data_ptr(), tuple(s1), tuple(s2), n1, n2,
+               av.element_size(), Cw.element_size())
+        scratch = ctx.ptr_cache.get(key)
+        if scratch is None:
+            scratch = torch.empty(3 * n1 * n2, dtype=torch.int64, device=ctx.device)
+            ctx.ptr_cache[key] = scratch
+        else:
+            ready = 1
     _lib.call("ls2_gemm", ctx.blas, int(la[0]), int(lb[0]), m, n, k, float(alpha),
               av.data_ptr(), la[1], s1[0], s2[0], bv.data_ptr(), lb[1], s1[1], s2[1],
               float(beta_v), Cw.data_ptr(), lc[1], s1[2], s2[2], n1, n2,
-              _lib.dtype_code(av), _lib.dtype_code(tc), _lib.ptr(scratch), _lib.stream_handle())
+              _lib.dtype_code(av), _lib.dtype_code(tc), _lib.ptr(scratch), ready,
+              _lib.stream_handle())
     if tmp_c is not None:
         Cv.copy_(tmp_c)
     return C

@@ -207,10 +207,27 @@ def _as_dt(t, dt):
 
 
 def _linear(x2d, w, b, out2d):
-    """out = x @ w^T (+ b) on cuBLAS; bias added in place by libls2."""
-    K.gemm(x2d, _as_dt(w, out2d.dtype), trans_b=True, out=out2d)
-    if b is not None:
-        bb = _as_dt(b, out2d.dtype).contiguous()
+    """out = x @ w^T (+ b): one cuBLASLt GEMM with the bias fused as its epilogue
+    (fallback: cuBLAS GEMM + libls2 bias-add where Lt has no algorithm)."""
+    dt = out2d.dtype
+    wt = _as_dt(w, dt)
+    bb = None if b is None else _as_dt(b, dt).contiguous()
+    ctx = _lib.context()
+    if dt != torch.float64 and x2d.is_contiguous() and wt.is_contiguous() and out2d.is_contiguous() \
+            and x2d.dtype == dt:
+        m, k = x2d.shape
+        n = wt.shape[0]
+        key = (m, n, k, dt, bb is not None)
+        if key not in ctx.lt_unsupported:
+            try:
+                _lib.call("ls2_gemm_lt", ctx.blas, 0, 1, m, n, k, 1.0, x2d.data_ptr(), k,
+                          wt.data_ptr(), k, 0.0, out2d.data_ptr(), n, _lib.ptr(bb),
+                          _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.stream_handle())
+                return out2d
+            except Exception:
+                ctx.lt_unsupported.add(key)
+    K.gemm(x2d, wt, trans_b=True, out=out2d)
+    if bb is not None:
         _lib.call("ls2_bias_add", out2d.data_ptr(), bb.data_ptr(), out2d.shape[0],
                   out2d.shape[1], _lib.dtype_code(out2d), _lib.stream_handle())
     return out2d
