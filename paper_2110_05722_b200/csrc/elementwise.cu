@@ -14,7 +14,7 @@
 namespace ls2 {
 
 constexpr int kTPB = 256;
-constexpr int kMaxColsumBlocks = 2 * kNumSMs;
+constexpr int kMaxColsumBlocks = kNumSMs;  // one partial row per SM: short finish
 
 struct Tiling {
   int64_t cgs;      // column groups per row (cols / 8)
@@ -37,9 +37,26 @@ inline Tiling tiling(int64_t rows, int64_t cols) {
   return t;
 }
 
+// tiling for kernels that also reduce columns: 1024-thread CTAs (256 for f64, whose
+// smem partials are twice as wide) so <= 148 CTAs still keep every SM busy
+inline Tiling tiling_cs(int64_t rows, int64_t cols, bool f64) {
+  const int tpb = f64 ? 256 : 1024;
+  Tiling t;
+  t.cgs = cols / 8;
+  if (t.cgs <= tpb) {
+    t.rpp = (int)(tpb / t.cgs);
+    t.threads = (int)(ceil_div((int64_t)t.rpp * t.cgs, 32) * 32);
+  } else {
+    t.threads = (int)(ceil_div(t.cgs, 32) * 32);
+    t.rpp = 1;
+  }
+  t.passes = ceil_div(rows, t.rpp);
+  return t;
+}
+
 // fixed (shape-only) grid for the column-sum kernels => deterministic results
 inline int colsum_blocks(int64_t passes) {
-  int64_t g = ceil_div(passes, 4);
+  int64_t g = ceil_div(passes, 2);
   return (int)(g < 1 ? 1 : (g > kMaxColsumBlocks ? kMaxColsumBlocks : g));
 }
 
@@ -75,33 +92,31 @@ __device__ __forceinline__ void store_row_group(T* p, const C (&v)[8]) {
 // ---------------------------------------------------------------------------
 // column-sum stage 2: out[c] (+)= sum_g partial[g, c] in fixed order
 // ---------------------------------------------------------------------------
-// CTA = 8 warps x 32 columns; warp w sums partial rows w, w+8, ... (coalesced
-// 256-byte row segments, 4 loads in flight), then the 8 warp sums are added in
-// fixed order -> deterministic and ~nblk/32 dependent L2 round trips.
+// CTA = 32 warps x 32 columns; warp w sums partial rows w, w+32, ... (coalesced
+// 256-byte row segments), then the 32 warp sums are added in fixed order ->
+// deterministic, and with <= 148 partial rows only ~5 dependent L2 round trips.
 template <typename Tout>
-__global__ void __launch_bounds__(256) colsum_finish_kernel(const double* __restrict__ partial,
-                                                            int nblk, int64_t cols,
-                                                            Tout* __restrict__ out, int beta) {
-  __shared__ double red[8][33];
+__global__ void __launch_bounds__(1024) colsum_finish_kernel(const double* __restrict__ partial,
+                                                             int nblk, int64_t cols,
+                                                             Tout* __restrict__ out, int beta) {
+  __shared__ double red[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
-  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  double s0 = 0, s1 = 0;
   if (c < cols) {
     int g = w;
-    for (; g + 24 < nblk; g += 32) {
+    for (; g + 32 < nblk; g += 64) {
       s0 += partial[(int64_t)g * cols + c];
-      s1 += partial[(int64_t)(g + 8) * cols + c];
-      s2 += partial[(int64_t)(g + 16) * cols + c];
-      s3 += partial[(int64_t)(g + 24) * cols + c];
+      s1 += partial[(int64_t)(g + 32) * cols + c];
     }
-    for (; g < nblk; g += 8) s0 += partial[(int64_t)g * cols + c];
+    for (; g < nblk; g += 32) s0 += partial[(int64_t)g * cols + c];
   }
-  red[w][lane] = (s0 + s1) + (s2 + s3);
+  red[w][lane] = s0 + s1;
   __syncthreads();
   if (w == 0 && c < cols) {
     double s = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][lane];
+    for (int k = 0; k < 32; ++k) s += red[k][lane];
     if (beta) s += cvt<double>(out[c]);
     out[c] = cvt<Tout>(s);
   }
@@ -110,31 +125,38 @@ __global__ void __launch_bounds__(256) colsum_finish_kernel(const double* __rest
 int colsum_finish(const double* partial, int nblk, int64_t cols, void* out, int tout, int beta,
                   cudaStream_t st) {
   return LS2_DISPATCH_ONE(tout, "colsum_finish", [&] {
-    colsum_finish_kernel<Tx><<<(unsigned)ceil_div(cols, 32), 256, 0, st>>>(partial, nblk, cols,
-                                                                         (Tx*)out, beta);
+    colsum_finish_kernel<Tx><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>(partial, nblk, cols,
+                                                                          (Tx*)out, beta);
     return check_launch("colsum_finish");
   });
 }
 
 // CTA-level reduction of the per-thread 8-column partials (rpp row lanes per
-// column group) into partial[blockIdx, cols], fixed order.
+// column group) into partial[blockIdx, cols], fixed order.  smem holds the
+// partials in the compute type (f32, or f64 for the f64 path).
 template <typename C>
 __device__ __forceinline__ void cta_colsum_store(const C (&acc)[8], int64_t cgs, int rpp,
                                                  int64_t cols, double* __restrict__ partial,
-                                                 double* smem) {
+                                                 C* smem) {
   const int tid = threadIdx.x;
   const int lane_row = (int)(tid / cgs);
   const int64_t cg = tid % cgs;
   if (lane_row < rpp) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) smem[(int64_t)lane_row * cols + cg * 8 + e] = (double)acc[e];
+    for (int e = 0; e < 8; ++e) smem[(int64_t)lane_row * cols + cg * 8 + e] = acc[e];
   }
   __syncthreads();
   for (int64_t c = tid; c < cols; c += blockDim.x) {
     double s = 0.0;
-    for (int r = 0; r < rpp; ++r) s += smem[(int64_t)r * cols + c];
+    for (int r = 0; r < rpp; ++r) s += (double)smem[(int64_t)r * cols + c];
     partial[(int64_t)blockIdx.x * cols + c] = s;
   }
+}
+
+template <typename C>
+__device__ __forceinline__ C* colsum_smem() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return reinterpret_cast<C*>(smem_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -214,7 +236,6 @@ __global__ void __launch_bounds__(1024) bdr_bwd_vec(const Tin* __restrict__ dy, 
                                   int64_t rows, int64_t cols, int64_t cgs, int rpp,
                                   typename CompOf<Tin>::type scale) {
   using C = typename CompOf<Tin>::type;
-  extern __shared__ double smem[];
   const int lane_row = (int)(threadIdx.x / cgs);
   const int64_t cg = threadIdx.x % cgs;
   C acc[8];
@@ -234,7 +255,7 @@ __global__ void __launch_bounds__(1024) bdr_bwd_vec(const Tin* __restrict__ dy, 
       store_row_group(dx + g * 8, d);
     }
   }
-  cta_colsum_store(acc, cgs, rpp, cols, partial, smem);
+  cta_colsum_store(acc, cgs, rpp, cols, partial, colsum_smem<C>());
 }
 
 template <typename Tin, typename Tout, bool DROP>
@@ -334,7 +355,6 @@ __global__ void __launch_bounds__(1024) brd_bwd_vec(const Tin* __restrict__ dy, 
                                   double* __restrict__ partial, int64_t rows, int64_t cols,
                                   int64_t cgs, int rpp, typename CompOf<Tin>::type scale) {
   using C = typename CompOf<Tin>::type;
-  extern __shared__ double smem[];
   const int lane_row = (int)(threadIdx.x / cgs);
   const int64_t cg = threadIdx.x % cgs;
   C acc[8];
@@ -356,7 +376,7 @@ __global__ void __launch_bounds__(1024) brd_bwd_vec(const Tin* __restrict__ dy, 
       store_row_group(dx + g * 8, d);
     }
   }
-  cta_colsum_store(acc, cgs, rpp, cols, partial, smem);
+  cta_colsum_store(acc, cgs, rpp, cols, partial, colsum_smem<C>());
 }
 
 template <typename Tin, typename Tout, bool DROP>
@@ -432,7 +452,6 @@ __global__ void __launch_bounds__(1024) colsum_vec(const Tin* __restrict__ x,
                                                    double* __restrict__ partial, int64_t rows,
                                                    int64_t cols, int64_t cgs, int rpp) {
   using C = typename CompOf<Tin>::type;
-  extern __shared__ double smem[];
   const int lane_row = (int)(threadIdx.x / cgs);
   const int64_t cg = threadIdx.x % cgs;
   C acc[8];
@@ -446,15 +465,15 @@ __global__ void __launch_bounds__(1024) colsum_vec(const Tin* __restrict__ x,
       for (int e = 0; e < 8; ++e) acc[e] += v[e];
     }
   }
-  cta_colsum_store(acc, cgs, rpp, cols, partial, smem);
+  cta_colsum_store(acc, cgs, rpp, cols, partial, colsum_smem<C>());
 }
 
 inline int colsum_generic(const void* x, int tin, int64_t rows, int64_t cols, void* out, int tout,
                           int beta, void* ws, cudaStream_t st) {
   if (vec_ok(cols, {x})) {
-    Tiling t = tiling(rows, cols);
+    Tiling t = tiling_cs(rows, cols, tin == LS2_F64);
     const int grid = colsum_blocks(t.passes);
-    const size_t sm = (size_t)t.rpp * cols * sizeof(double);
+    const size_t sm = (size_t)t.rpp * cols * (tin == LS2_F64 ? 8 : 4);
     int rc = LS2_DISPATCH_ONE(tin, "colsum", [&] {
       colsum_vec<Tx><<<grid, t.threads, sm, st>>>((const Tx*)x, (double*)ws, rows, cols, t.cgs,
                                                   t.rpp);
@@ -562,9 +581,9 @@ int ls2_bias_dropout_residual_bwd(const void* dy, const uint8_t* keep_bits, void
   int rc = LS2_DISPATCH_IO(tin, tout, "bias_dropout_residual_bwd", [&] {
     auto sc = cscale<Tin>(scale);
     if (vec) {
-      Tiling t = tiling(rows, cols);
+      Tiling t = tiling_cs(rows, cols, tin == LS2_F64);
       int grid = colsum_blocks(t.passes);
-      size_t sm = (size_t)t.rpp * cols * sizeof(double);
+      size_t sm = (size_t)t.rpp * cols * sizeof(typename CompOf<Tin>::type);
       if (use_drop)
         bdr_bwd_vec<Tin, Tout, true><<<grid, t.threads, sm, st>>>(
             (const Tin*)dy, keep_bits, (Tout*)dx, (double*)ws, rows, cols, t.cgs, t.rpp, sc);
@@ -632,9 +651,9 @@ int ls2_bias_relu_dropout_bwd(const void* dy, const uint8_t* keep_bits, const ui
   return LS2_DISPATCH_IO(tin, tout, "bias_relu_dropout_bwd", [&] {
     auto sc = cscale<Tin>(scale);
     if (vec) {
-      Tiling t = tiling(rows, cols);
+      Tiling t = tiling_cs(rows, cols, tin == LS2_F64);
       int grid = colsum_blocks(t.passes);
-      size_t sm = (size_t)t.rpp * cols * sizeof(double);
+      size_t sm = (size_t)t.rpp * cols * sizeof(typename CompOf<Tin>::type);
       if (use_drop)
         brd_bwd_vec<Tin, Tout, true><<<grid, t.threads, sm, st>>>(
             (const Tin*)dy, keep_bits, relu_bits, (Tout*)dx, (double*)ws, rows, cols, t.cgs,

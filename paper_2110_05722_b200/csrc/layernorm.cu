@@ -17,7 +17,7 @@ namespace ls2 {
 
 constexpr int kLnWarps = 4;
 constexpr int kLnBwdWarps = 8;
-constexpr int kLnMaxBlocks = 2 * kNumSMs;
+constexpr int kLnMaxBlocks = kNumSMs;
 
 template <typename T, typename C>
 __device__ __forceinline__ void ld_group(const T* p, C (&v)[8]) {
@@ -285,26 +285,26 @@ __global__ void ln_param_partial(const Tin* __restrict__ dy, const Tin* __restri
   }
 }
 
-// CTA = 8 warps x 32 columns, warp w reduces partial blocks w, w+8, ...;
+// CTA = 32 warps x 32 columns, warp w reduces partial blocks w, w+32, ...;
 // fixed-order combination of the warp sums (deterministic).
 template <typename Tp>
-__global__ void __launch_bounds__(256) ln_param_finish(const double* __restrict__ partial,
-                                                       int nblk, int64_t cols,
-                                                       Tp* __restrict__ dw, Tp* __restrict__ db,
-                                                       int beta) {
-  __shared__ double red[2][8][33];
+__global__ void __launch_bounds__(1024) ln_param_finish(const double* __restrict__ partial,
+                                                        int nblk, int64_t cols,
+                                                        Tp* __restrict__ dw, Tp* __restrict__ db,
+                                                        int beta) {
+  __shared__ double red[2][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   double sw0 = 0, sw1 = 0, sb0 = 0, sb1 = 0;
   if (c < cols) {
     int g = w;
-    for (; g + 8 < nblk; g += 16) {
+    for (; g + 32 < nblk; g += 64) {
       sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
       sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
-      sw1 += partial[((int64_t)(g + 8) * 2 + 0) * cols + c];
-      sb1 += partial[((int64_t)(g + 8) * 2 + 1) * cols + c];
+      sw1 += partial[((int64_t)(g + 32) * 2 + 0) * cols + c];
+      sb1 += partial[((int64_t)(g + 32) * 2 + 1) * cols + c];
     }
-    for (; g < nblk; g += 8) {
+    for (; g < nblk; g += 32) {
       sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
       sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
     }
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256) ln_param_finish(const double* __restrict_
   if (w == 0 && c < cols) {
     double sw = 0, sb = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { sw += red[0][k][lane]; sb += red[1][k][lane]; }
+    for (int k = 0; k < 32; ++k) { sw += red[0][k][lane]; sb += red[1][k][lane]; }
     if (beta) { sw += cvt<double>(dw[c]); sb += cvt<double>(db[c]); }
     dw[c] = cvt<Tp>(sw);
     db[c] = cvt<Tp>(sb);
@@ -423,7 +423,7 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
   if (rc) return rc;
   if (!dw || !db) return LS2_OK;
   return LS2_DISPATCH_ONE(tparam, "layernorm_param_finish", [&] {
-    ln_param_finish<Tx><<<(unsigned)ceil_div(cols, 32), 256, 0, st>>>((const double*)ws, nblk, cols, (Tx*)dw,
+    ln_param_finish<Tx><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>((const double*)ws, nblk, cols, (Tx*)dw,
                                                          (Tx*)db, beta_param);
     return check_launch("layernorm_param_finish");
   });
