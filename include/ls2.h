@@ -124,6 +124,23 @@ int ls2_softmax_bwd(const void* dy, const void* q, void* dx, int64_t rows, int64
 int ls2_log_softmax_fwd(const void* h, void* y, int64_t rows, int64_t cols, int tin,
                         int tout, void* stream);
 
+/* ---- fused short-sequence attention (fp16, head dim 64, Lq/Lk <= 128) ----
+ * Replaces scores = QK^T/sqrt(hd) -> softmax_forward(mask) -> P V -> merge heads
+ * (F/model.py:362-376) and its backward (F/model.py:482-495, F/gradients.py:77-100).
+ * Operands are addressed per (b, h) as base + b*L*ld + h*64 (row stride ld), so Q/K/V
+ * are read straight from the fused projection and outputs land in merged layouts.
+ * probs: [B, H, Lq, Lk] (written by fwd, read by bwd). mask: NONE/CAUSAL/PADDING. */
+int ls2_attention_supported(int64_t lq, int64_t lk, int64_t hd, int dtype);
+int ls2_attention_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                      int64_t ldv, void* probs, void* o, int64_t ldo, int64_t batch,
+                      int64_t heads, int64_t lq, int64_t lk, int64_t hd, int mask_kind,
+                      const int64_t* lens, double scale, void* stream);
+int ls2_attention_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                      int64_t ldv, const void* probs, const void* dout, int64_t lddo, void* dq,
+                      int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                      int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
+                      double scale, void* stream);
+
 /* ---- label-smoothed CE: F/kernels.py:338-360, F/gradients.py:47-74 ----
  * row_stats (double[rows*2]) receives per-row (loss, correct) partials;
  * out3 (double[3]) = (loss_sum, token_count, correct) after the fixed-order reduce. */

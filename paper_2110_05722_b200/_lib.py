@@ -54,6 +54,9 @@ _SIGS = {
     "ls2_ls_ce_fwd": [P, P, P, P, P, L, L, D, L, I, I, P],
     "ls2_ls_ce_bwd": [P, P, P, P, L, L, D, L, I, D, I, I, P],
     "ls2_criterion_fused": [P, P, P, P, P, P, P, L, L, D, L, I, D, I, P],
+    "ls2_attention_supported": [L, L, L, I],
+    "ls2_attention_fwd": [P, L, P, L, P, L, P, P, L, L, L, L, L, L, I, P, D, P],
+    "ls2_attention_bwd": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, D, P],
     "ls2_embedding_fwd": [P, P, P, P, P, P, L, L, L, L, D, I, I, U, P, U, D, I, I, P],
     "ls2_embedding_bwd": [P, P, P, P, P, I, I, L, L, L, L, D, I, D, I, P],
     "ls2_adam": [P, P, P, P, L, P, P, L, L, P, P, P, P],
@@ -69,6 +72,7 @@ _SIGS = {
 }
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,
              "ls2_colsum_ws_bytes": L, "ls2_layernorm_bwd_ws_bytes": L,
+             "ls2_attention_supported": ctypes.c_int,
              "ls2_gemm_scratch_bytes": L}
 
 _lib = None

@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import attention as ATT
 from . import gradients as G
 from . import kernels as K
 from .errors import ConfigError, IncompleteGradientSet, SequenceTooLong, ShapeMismatch, TokenOutOfRange
@@ -526,13 +527,19 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     qkv = arena.alloc((b, l, 3 * d), dt)
     _linear(u1.view(r, d), w.wqkv, w.bqkv, qkv.view(r, 3 * d))
     stash.push(p + "qkv", qkv)
-    qh, kh, vh = _qkv_heads(qkv, n_heads)
     scores = arena.alloc((b, n_heads, l, l), dt)
-    K.gemm(qh, kh, trans_b=True, out=scores, alpha=1.0 / math.sqrt(hd))
-    K.softmax_forward(scores, mask=mask, out=scores)
-    stash.push(p + "probs", scores)
-    ctxm = arena.alloc((b, l, d), dt)
-    K.gemm(scores, vh, out=_heads(ctxm, n_heads))
+    if ATT.fused_ok(dt, l, l, hd, mask):
+        ctxm = arena.alloc((b, l, d), dt)
+        ATT.forward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
+                    scores, ctxm, d, b, n_heads, l, l, hd, mask, 1.0 / math.sqrt(hd))
+        stash.push(p + "probs", scores)
+    else:
+        qh, kh, vh = _qkv_heads(qkv, n_heads)
+        K.gemm(qh, kh, trans_b=True, out=scores, alpha=1.0 / math.sqrt(hd))
+        K.softmax_forward(scores, mask=mask, out=scores)
+        stash.push(p + "probs", scores)
+        ctxm = arena.alloc((b, l, d), dt)
+        K.gemm(scores, vh, out=_heads(ctxm, n_heads))
     stash.push(p + "ctxm", ctxm)
     proj = arena.alloc((b, l, d), dt)
     _linear(ctxm.view(r, d), w.wo, None, proj.view(r, d))
@@ -637,17 +644,25 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp):
     K.gemm(dproj.view(r, d), _as_dt(w.wo, dt), out=dctxm.view(r, d))
     _wgrad(sink, pp + "attn.wo", dproj.view(r, d), ctxm.view(r, d))
     arena.free(dproj); arena.free(ctxm)
-    dctx = _heads(dctxm, n_heads)
-    qh, kh, vh = _qkv_heads(qkv, n_heads)
-    dscores = arena.alloc((b, n_heads, l, l), dt)
-    K.gemm(dctx, vh, trans_b=True, out=dscores)
-    G.softmax_backward(dscores, SoftmaxCache(probs), out=dscores, out_scale=1.0 / math.sqrt(hd))
-    dqkv = arena.alloc((b, l, 3 * d), dt)
-    dq, dk, dv = _qkv_heads(dqkv, n_heads)
-    K.gemm(dscores, kh, out=dq)
-    K.gemm(dscores, qh, trans_a=True, out=dk)
-    K.gemm(probs, dctx, trans_a=True, out=dv)
-    arena.free(dscores); arena.free(probs); arena.free(dctxm); arena.free(qkv)
+    if ATT.fused_ok(dt, l, l, hd, AttentionMask("none")):
+        dqkv = arena.alloc((b, l, 3 * d), dt)
+        ATT.backward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
+                     probs, dctxm, d, dqkv[..., :d], 3 * d, dqkv[..., d:2 * d], 3 * d,
+                     dqkv[..., 2 * d:], 3 * d, b, n_heads, l, l, hd, 1.0 / math.sqrt(hd))
+        arena.free(probs); arena.free(dctxm); arena.free(qkv)
+    else:
+        dctx = _heads(dctxm, n_heads)
+        qh, kh, vh = _qkv_heads(qkv, n_heads)
+        dscores = arena.alloc((b, n_heads, l, l), dt)
+        K.gemm(dctx, vh, trans_b=True, out=dscores)
+        G.softmax_backward(dscores, SoftmaxCache(probs), out=dscores,
+                           out_scale=1.0 / math.sqrt(hd))
+        dqkv = arena.alloc((b, l, 3 * d), dt)
+        dq, dk, dv = _qkv_heads(dqkv, n_heads)
+        K.gemm(dscores, kh, out=dq)
+        K.gemm(dscores, qh, trans_a=True, out=dk)
+        K.gemm(probs, dctx, trans_a=True, out=dv)
+        arena.free(dscores); arena.free(probs); arena.free(dctxm); arena.free(qkv)
     du1 = arena.alloc((b, l, d), dt)
     K.gemm(dqkv.view(r, 3 * d), _as_dt(w.wqkv, dt), out=du1.view(r, d))
     _wgrad(sink, pp + "attn.wqkv", dqkv.view(r, 3 * d), u1.view(r, d))
@@ -696,12 +711,18 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     _linear(u2.view(r, d), w.cross_wq, w.cross_bq, qc.view(r, d))
     stash.push(p + "qc", qc)
     scores_x = arena.alloc((b, n_heads, l, ls), dt)
-    K.gemm(_heads(qc, n_heads), _heads(_as_dt(k_i, dt), n_heads), trans_b=True, out=scores_x,
-           alpha=1.0 / math.sqrt(hd))
-    K.softmax_forward(scores_x, mask=cross_mask, out=scores_x)
-    stash.push(p + "probs_x", scores_x)
-    ctxm_x = arena.alloc((b, l, d), dt)
-    K.gemm(scores_x, _heads(_as_dt(v_i, dt), n_heads), out=_heads(ctxm_x, n_heads))
+    if ATT.fused_ok(dt, l, ls, hd, cross_mask) and k_i.dtype == dt and v_i.dtype == dt:
+        ctxm_x = arena.alloc((b, l, d), dt)
+        ATT.forward(qc, d, k_i, k_i.stride(1), v_i, v_i.stride(1), scores_x, ctxm_x, d, b,
+                    n_heads, l, ls, hd, cross_mask, 1.0 / math.sqrt(hd))
+        stash.push(p + "probs_x", scores_x)
+    else:
+        K.gemm(_heads(qc, n_heads), _heads(_as_dt(k_i, dt), n_heads), trans_b=True,
+               out=scores_x, alpha=1.0 / math.sqrt(hd))
+        K.softmax_forward(scores_x, mask=cross_mask, out=scores_x)
+        stash.push(p + "probs_x", scores_x)
+        ctxm_x = arena.alloc((b, l, d), dt)
+        K.gemm(scores_x, _heads(_as_dt(v_i, dt), n_heads), out=_heads(ctxm_x, n_heads))
     stash.push(p + "ctxm_x", ctxm_x)
     proj_x = arena.alloc((b, l, d), dt)
     _linear(ctxm_x.view(r, d), w.cross_wo, None, proj_x.view(r, d))
@@ -744,21 +765,33 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     K.gemm(dproj_x.view(r, d), _as_dt(w.cross_wo, dt), out=dctxm_x.view(r, d))
     _wgrad(sink, pp + "cross.wo", dproj_x.view(r, d), ctxm_x.view(r, d))
     arena.free(dproj_x); arena.free(ctxm_x)
-    dctx_x = _heads(dctxm_x, n_heads)
-    kh, vh = _heads(_as_dt(k_i, dt), n_heads), _heads(_as_dt(v_i, dt), n_heads)
-    dscores_x = arena.alloc((b, n_heads, l, ls), dt)
-    K.gemm(dctx_x, vh, trans_b=True, out=dscores_x)
-    G.softmax_backward(dscores_x, SoftmaxCache(probs_x), out=dscores_x,
-                       out_scale=1.0 / math.sqrt(hd))
-    dqc = arena.alloc((b, l, d), dt)
-    K.gemm(dscores_x, kh, out=_heads(dqc, n_heads))
-    if dkv_out is not None:
-        dk_i, dv_i = dkv_out
+    if ATT.fused_ok(dt, l, ls, hd, AttentionMask("none")) and k_i.dtype == dt and \
+            v_i.dtype == dt and (dkv_out is None or dkv_out[0].dtype == dt):
+        dqc = arena.alloc((b, l, d), dt)
+        if dkv_out is not None:
+            dk_i, dv_i = dkv_out
+        else:
+            dk_i, dv_i = arena.alloc((b, ls, d), dt), arena.alloc((b, ls, d), dt)
+        ATT.backward(qc, d, k_i, k_i.stride(1), v_i, v_i.stride(1), probs_x, dctxm_x, d,
+                     dqc, d, dk_i, dk_i.stride(1), dv_i, dv_i.stride(1), b, n_heads, l, ls, hd,
+                     1.0 / math.sqrt(hd))
+        arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
     else:
-        dk_i, dv_i = arena.alloc((b, ls, d), dt), arena.alloc((b, ls, d), dt)
-    K.gemm(dscores_x, _heads(qc, n_heads), trans_a=True, out=_heads(dk_i, n_heads))
-    K.gemm(probs_x, dctx_x, trans_a=True, out=_heads(dv_i, n_heads))
-    arena.free(dscores_x); arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
+        dctx_x = _heads(dctxm_x, n_heads)
+        kh, vh = _heads(_as_dt(k_i, dt), n_heads), _heads(_as_dt(v_i, dt), n_heads)
+        dscores_x = arena.alloc((b, n_heads, l, ls), dt)
+        K.gemm(dctx_x, vh, trans_b=True, out=dscores_x)
+        G.softmax_backward(dscores_x, SoftmaxCache(probs_x), out=dscores_x,
+                           out_scale=1.0 / math.sqrt(hd))
+        dqc = arena.alloc((b, l, d), dt)
+        K.gemm(dscores_x, kh, out=_heads(dqc, n_heads))
+        if dkv_out is not None:
+            dk_i, dv_i = dkv_out
+        else:
+            dk_i, dv_i = arena.alloc((b, ls, d), dt), arena.alloc((b, ls, d), dt)
+        K.gemm(dscores_x, _heads(qc, n_heads), trans_a=True, out=_heads(dk_i, n_heads))
+        K.gemm(probs_x, dctx_x, trans_a=True, out=_heads(dv_i, n_heads))
+        arena.free(dscores_x); arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
     du2 = arena.alloc((b, l, d), dt)
     K.gemm(dqc.view(r, d), _as_dt(w.cross_wq, dt), out=du2.view(r, d))
     _wgrad(sink, pp + "cross.wq", dqc.view(r, d), u2.view(r, d))
