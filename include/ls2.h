@@ -110,6 +110,23 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
                       int tparam, int beta_param, void* ws, int64_t rows, int64_t cols,
                       int tin, int tout, int tstat, void* stream);
 
+/* fused bias+dropout+residual -> LayerNorm (F/kernels.py:367-382 then :235-270):
+ * yres = keep*(x+bias)*dscale + res (stored), u = LN(yres) with (mu, sigma);
+ * needs cols % 8 == 0, cols <= 1024, 16-byte aligned operands (else LS2_ERR_SHAPE). */
+int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void* yres,
+                          uint8_t* keep_bits, const void* w, const void* b, void* u, void* mu,
+                          void* sigma, int64_t rows, int64_t cols, double eps, int use_drop,
+                          uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, double dscale,
+                          int tin, int tout, int tstat, void* stream);
+/* fused LayerNorm backward (+ dres) -> bias+dropout+residual backward
+ * (F/gradients.py:103-144 then :147-159): dx = LN'(dy) + dres (stored), dproj =
+ * keep*dx*dscale (stored), and dw, db, dbias column sums (bit k of beta_mask: accumulate) */
+int ls2_layernorm_bwd_bdr(const void* dy, const void* x, const void* w, const void* mu,
+                          const void* sigma, const void* dres, void* dx, const uint8_t* keep_bits,
+                          void* dproj, int use_drop, double dscale, void* dw, void* db,
+                          void* dbias, int tparam, int beta_mask, void* ws, int64_t rows,
+                          int64_t cols, int tin, int tout, int tstat, void* stream);
+
 /* ---- softmax family: F/kernels.py:277-331 / F/gradients.py:77-100 ----
  * x rows are the flattened leading dims; mask per LS2_MASK_*.  in_scale
  * multiplies x before the softmax (folds 1/sqrt(hd)); out may alias x.

@@ -48,6 +48,8 @@ _SIGS = {
     "ls2_layernorm_fwd": [P, P, P, P, P, P, P, L, L, D, I, I, I, P],
     "ls2_layernorm_bwd_ws_bytes": [L, L],
     "ls2_layernorm_bwd": [P, P, P, P, P, P, P, P, P, I, I, P, L, L, I, I, I, P],
+    "ls2_bdr_layernorm_fwd": [P, P, P, P, P, P, P, P, P, P, L, L, D, I, U, P, U, D, I, I, I, P],
+    "ls2_layernorm_bwd_bdr": [P, P, P, P, P, P, P, P, P, I, D, P, P, P, I, I, P, L, L, I, I, I, P],
     "ls2_softmax_fwd": [P, P, L, L, I, L, L, P, P, D, P, I, I, P],
     "ls2_softmax_bwd": [P, P, P, L, L, D, I, I, P],
     "ls2_log_softmax_fwd": [P, P, L, L, I, I, P],

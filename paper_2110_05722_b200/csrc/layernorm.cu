@@ -100,6 +100,97 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_warp(
   }
 }
 
+// Fused bias+dropout+residual -> LayerNorm (F/kernels.py:367-382 then :235-270):
+//   yres = keep*(x+bias)*dscale + res  (stored: it is the next residual stream),
+//   u    = LN(yres)  with (mu, sigma) cached.
+// The LayerNorm consumes the stored (rounded) yres, so results equal the
+// unfused pair exactly; one launch and one pass instead of two.
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool DROP>
+__global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_bdr_warp(
+    const Tin* __restrict__ x, const Tin* __restrict__ bias, const Tin* __restrict__ res,
+    Tout* __restrict__ yres, uint8_t* __restrict__ bits, const Tin* __restrict__ w,
+    const Tin* __restrict__ b, Tout* __restrict__ u, Tstat* __restrict__ mu,
+    Tstat* __restrict__ sigma, int64_t rows, int64_t cols, double eps, uint64_t seed,
+    const uint64_t* seed_ptr, uint64_t thresh, typename CompOf<Tin>::type dscale) {
+  using C = typename CompOf<Tin>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t cgs = cols / 8;
+  if (seed_ptr) seed = *seed_ptr;
+  C wv[ITERS][8], bv[ITERS][8], cb[ITERS][8];
+#pragma unroll
+  for (int it = 0; it < ITERS; ++it) {
+    const int64_t g = lane + 32 * it;
+    if (g < cgs) {
+      ld_group(w + g * 8, wv[it]);
+      ld_group(b + g * 8, bv[it]);
+      ld_group(bias + g * 8, cb[it]);
+    }
+  }
+  const double inv_m = 1.0 / (double)cols;
+  for (int64_t r = (int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5); r < rows;
+       r += (int64_t)gridDim.x * kLnWarps) {
+    C v[ITERS][8];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t g = lane + 32 * it;
+      if (g < cgs) {
+        C xv[8], rv[8];
+        ld_group(x + r * cols + g * 8, xv);
+        ld_group(res + r * cols + g * 8, rv);
+        uint32_t kb = 0xFF;
+        if (DROP) {
+          kb = keep_byte(seed, (uint64_t)(r * cgs + g) * 8, thresh);
+          bits[r * cgs + g] = (uint8_t)kb;
+        }
+        Pack8<Tout> q;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          C a = add_rn(xv[e], cb[it][e]);
+          if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), dscale);
+          q.v[e] = cvt<Tout>(add_rn(a, rv[e]));
+          v[it][e] = cvt<C>(q.v[e]);
+        }
+        st8(yres + r * cols + g * 8, q);
+      }
+    }
+    const C pivot = __shfl_sync(0xffffffffu, v[0][0], 0);
+    C s1 = 0, s2 = 0;
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      if (lane + 32 * it < cgs) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          v[it][e] -= pivot;
+          s1 += v[it][e];
+          s2 += v[it][e] * v[it][e];
+        }
+      }
+    }
+    const double S1 = warp_sum((double)s1);
+    const double S2 = warp_sum((double)s2);
+    const double mean_sh = S1 * inv_m;
+    double var = S2 * inv_m - mean_sh * mean_sh;
+    if (var < 0.0) var = 0.0;
+    const double sg = sqrt(var + eps);
+    const C rs = (C)(1.0 / sg);
+    const C msh = (C)mean_sh;
+    if (lane == 0) {
+      mu[r] = (Tstat)((double)pivot + mean_sh);
+      sigma[r] = (Tstat)sg;
+    }
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t g = lane + 32 * it;
+      if (g < cgs) {
+        C o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = (v[it][e] - msh) * rs * wv[it][e] + bv[it][e];
+        st_group(u + r * cols + g * 8, o);
+      }
+    }
+  }
+}
+
 // generic: CTA per row, any cols
 template <typename Tin, typename Tout, typename Tstat>
 __global__ void ln_fwd_block(const Tin* __restrict__ x, const Tin* __restrict__ w,
@@ -144,45 +235,75 @@ __global__ void ln_fwd_block(const Tin* __restrict__ x, const Tin* __restrict__ 
 // ---------------------------------------------------------------------------
 // backward
 // ---------------------------------------------------------------------------
-template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES>
+// Warp per row, row in registers, next row prefetched while the current one is
+// reduced (memory-level parallelism for these short, latency-bound passes).
+// BDR: the LN input gradient (+ residual) dyo is also pushed through the
+// preceding bias+dropout+residual backward (F/gradients.py:147-159):
+//   dproj = keep * dyo * dscale,  dbias = column sums of dproj
+// so one pass yields dyo (residual stream gradient), dproj, and the column
+// partials of (dw, db[, dbias]) as partial[block][NP][cols].
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP>
 __global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
     const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
     const Tstat* __restrict__ mu, const Tstat* __restrict__ sigma, const Tin* __restrict__ dres,
-    Tout* __restrict__ dx, double* __restrict__ partial, int64_t rows, int64_t cols) {
+    Tout* __restrict__ dx, const uint8_t* __restrict__ bits, Tout* __restrict__ dproj,
+    typename CompOf<Tin>::type dscale, double* __restrict__ partial, int64_t rows, int64_t cols) {
   using C = typename CompOf<Tin>::type;
-  __shared__ double red[kLnBwdWarps][2][256];  // per-warp column partials, one chunk at a time
+  constexpr int NP = BDR ? 3 : 2;
+  __shared__ C red[kLnBwdWarps][NP][256];  // per-warp column partials, one chunk at a time
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t cgs = cols / 8;
-  C wv[ITERS][8], adw[ITERS][8], adb[ITERS][8];
+  C wv[ITERS][8], acc[NP][ITERS][8];
 #pragma unroll
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) { adw[it][e] = 0; adb[it][e] = 0; }
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) acc[k][it][e] = 0;
     const int64_t g = lane + 32 * it;
     if (g < cgs) ld_group(w + g * 8, wv[it]);
   }
   const C inv_m = (C)(1.0 / (double)cols);
-  for (int64_t r = (int64_t)blockIdx.x * kLnBwdWarps + wid; r < rows;
-       r += (int64_t)gridDim.x * kLnBwdWarps) {
-    const C m_r = (C)mu[r];
-    const C rs = (C)(1.0 / (double)sigma[r]);
-    C xh[ITERS][8], gg[ITERS][8];
-    C r1 = 0, r3 = 0;
+  const int64_t stride = (int64_t)gridDim.x * kLnBwdWarps;
+  int64_t r = (int64_t)blockIdx.x * kLnBwdWarps + wid;
+  Pack8<Tin> nd[ITERS], nx[ITERS], nr[ITERS];   // prefetched row
+  auto fetch = [&](int64_t rr) {
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
-      if (g < cgs) {
-        C d[8];
-        ld_group(dy + r * cols + g * 8, d);
-        ld_group(x + r * cols + g * 8, xh[it]);
+      if (rr < rows && g < cgs) {
+        nd[it] = ld8(dy + rr * cols + g * 8);
+        nx[it] = ld8(x + rr * cols + g * 8);
+        if (RES) nr[it] = ld8(dres + rr * cols + g * 8);
+      }
+    }
+  };
+  fetch(r);
+  for (; r < rows; r += stride) {
+    // current row stays packed in its storage type; values are re-derived on use
+    Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      cd[it] = nd[it];
+      cx[it] = nx[it];
+      if (RES) cr[it] = nr[it];
+    }
+    const C m_r = (C)mu[r];
+    const C rs = (C)(1.0 / (double)sigma[r]);
+    fetch(r + stride);
+    C r1 = 0, r3 = 0;
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      if (lane + 32 * it < cgs) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          xh[it][e] = (xh[it][e] - m_r) * rs;
-          gg[it][e] = wv[it][e] * d[e];
-          r1 += gg[it][e];
-          r3 += gg[it][e] * xh[it][e];
-          adw[it][e] += d[e] * xh[it][e];
-          adb[it][e] += d[e];
+          const C dv = cvt<C>(cd[it].v[e]);
+          const C xh = (cvt<C>(cx[it].v[e]) - m_r) * rs;
+          const C gg = wv[it][e] * dv;
+          r1 += gg;
+          r3 += gg * xh;
+          acc[0][it][e] += dv * xh;
+          acc[1][it][e] += dv;
         }
       }
     }
@@ -192,16 +313,28 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
       if (g < cgs) {
-        C o[8];
+        Pack8<Tout> o;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (gg[it][e] - r1 - xh[it][e] * r3) * rs;
-        if (RES) {
-          C rr[8];
-          ld_group(dres + r * cols + g * 8, rr);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] += rr[e];
+        for (int e = 0; e < 8; ++e) {
+          const C xh = (cvt<C>(cx[it].v[e]) - m_r) * rs;
+          const C gg = wv[it][e] * cvt<C>(cd[it].v[e]);
+          C v = (gg - r1 - xh * r3) * rs;
+          if (RES) v += cvt<C>(cr[it].v[e]);
+          o.v[e] = cvt<Tout>(v);
         }
-        st_group(dx + r * cols + g * 8, o);
+        st8(dx + r * cols + g * 8, o);
+        if (BDR) {
+          const uint32_t kb = DROP ? bits[r * cgs + g] : 0xFF;
+          Pack8<Tout> pj;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            C v = cvt<C>(o.v[e]);
+            if (DROP) v = mul_rn(mul_rn(v, (C)((kb >> e) & 1)), dscale);
+            acc[NP - 1][it][e] += v;
+            pj.v[e] = cvt<Tout>(v);
+          }
+          st8(dproj + r * cols + g * 8, pj);
+        }
       }
     }
   }
@@ -211,19 +344,19 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
     const int64_t g = lane + 32 * it;
     if (g < cgs) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        red[wid][0][lane * 8 + e] = (double)adw[it][e];
-        red[wid][1][lane * 8 + e] = (double)adb[it][e];
-      }
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int k = 0; k < NP; ++k) red[wid][k][lane * 8 + e] = acc[k][it][e];
     }
     __syncthreads();
     const int64_t base = (int64_t)it * 256;
-    for (int c = threadIdx.x; c < 256 && base + c < cols; c += blockDim.x) {
-      double sw = 0, sb = 0;
+    for (int c = threadIdx.x; c < NP * 256; c += blockDim.x) {
+      const int k = c / 256, cc = c % 256;
+      if (base + cc >= cols) continue;
+      double s = 0;
 #pragma unroll
-      for (int k = 0; k < kLnBwdWarps; ++k) { sw += red[k][0][c]; sb += red[k][1][c]; }
-      partial[((int64_t)blockIdx.x * 2 + 0) * cols + base + c] = sw;
-      partial[((int64_t)blockIdx.x * 2 + 1) * cols + base + c] = sb;
+      for (int q = 0; q < kLnBwdWarps; ++q) s += (double)red[q][k][cc];
+      partial[((int64_t)blockIdx.x * NP + k) * cols + base + cc] = s;
     }
     __syncthreads();
   }
@@ -287,38 +420,35 @@ __global__ void ln_param_partial(const Tin* __restrict__ dy, const Tin* __restri
 
 // CTA = 32 warps x 32 columns, warp w reduces partial blocks w, w+32, ...;
 // fixed-order combination of the warp sums (deterministic).
-template <typename Tp>
+template <typename Tp, int NP>
 __global__ void __launch_bounds__(1024) ln_param_finish(const double* __restrict__ partial,
                                                         int nblk, int64_t cols,
-                                                        Tp* __restrict__ dw, Tp* __restrict__ db,
-                                                        int beta) {
-  __shared__ double red[2][32][33];
+                                                        Tp* __restrict__ o0, Tp* __restrict__ o1,
+                                                        Tp* __restrict__ o2, int beta_mask) {
+  __shared__ double red[NP][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
-  double sw0 = 0, sw1 = 0, sb0 = 0, sb1 = 0;
+  double s[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) s[k] = 0;
   if (c < cols) {
-    int g = w;
-    for (; g + 32 < nblk; g += 64) {
-      sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
-      sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
-      sw1 += partial[((int64_t)(g + 32) * 2 + 0) * cols + c];
-      sb1 += partial[((int64_t)(g + 32) * 2 + 1) * cols + c];
-    }
-    for (; g < nblk; g += 32) {
-      sw0 += partial[((int64_t)g * 2 + 0) * cols + c];
-      sb0 += partial[((int64_t)g * 2 + 1) * cols + c];
-    }
+    for (int g = w; g < nblk; g += 32)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) s[k] += partial[((int64_t)g * NP + k) * cols + c];
   }
-  red[0][w][lane] = sw0 + sw1;
-  red[1][w][lane] = sb0 + sb1;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) red[k][w][lane] = s[k];
   __syncthreads();
   if (w == 0 && c < cols) {
-    double sw = 0, sb = 0;
+    Tp* outs[3] = {o0, o1, o2};
 #pragma unroll
-    for (int k = 0; k < 32; ++k) { sw += red[0][k][lane]; sb += red[1][k][lane]; }
-    if (beta) { sw += cvt<double>(dw[c]); sb += cvt<double>(db[c]); }
-    dw[c] = cvt<Tp>(sw);
-    db[c] = cvt<Tp>(sb);
+    for (int k = 0; k < NP; ++k) {
+      double t = 0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) t += red[k][q][lane];
+      if (beta_mask & (1 << k)) t += cvt<double>(outs[k][c]);
+      outs[k][c] = cvt<Tp>(t);
+    }
   }
 }
 
@@ -376,7 +506,84 @@ int ls2_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void
 
 int64_t ls2_layernorm_bwd_ws_bytes(int64_t rows, int64_t cols) {
   (void)rows;
-  return (int64_t)kLnMaxBlocks * 2 * cols * (int64_t)sizeof(double);
+  return (int64_t)kLnMaxBlocks * 3 * cols * (int64_t)sizeof(double);
+}
+
+int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void* yres,
+                          uint8_t* keep_bits, const void* w, const void* b, void* u, void* mu,
+                          void* sigma, int64_t rows, int64_t cols, double eps, int use_drop,
+                          uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, double dscale,
+                          int tin, int tout, int tstat, void* stream) {
+  if (rows <= 0) return LS2_OK;
+  if (!ln_vec_ok(cols, {x, bias, res, yres, w, b, u}))
+    return fail(LS2_ERR_SHAPE, "bdr_layernorm_fwd: needs cols % 8 == 0, <= 1024, aligned");
+  cudaStream_t st = as_stream(stream);
+  return LS2_DISPATCH_IO(tin, tout, "bdr_layernorm_fwd", [&] {
+    return LS2_DISPATCH_STAT(tstat, [&] {
+      using C = typename CompOf<Tin>::type;
+      const int grid = (int)std::min<int64_t>(ceil_div(rows, kLnWarps), kNumSMs * 16);
+      auto go = [&](auto iters, auto drop) {
+        constexpr int I = decltype(iters)::value;
+        constexpr bool D = decltype(drop)::value;
+        ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D><<<grid, kLnWarps * 32, 0, st>>>(
+            (const Tin*)x, (const Tin*)bias, (const Tin*)res, (Tout*)yres, keep_bits,
+            (const Tin*)w, (const Tin*)b, (Tout*)u, (Tstat*)mu, (Tstat*)sigma, rows, cols, eps,
+            seed, seed_ptr, thresh, (C)dscale);
+        return check_launch("bdr_layernorm_fwd");
+      };
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I4 = std::integral_constant<int, 4>;
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      const int it = ln_iters(cols);
+      if (use_drop) return it == 1 ? go(I1{}, T_{}) : it == 2 ? go(I2{}, T_{}) : go(I4{}, T_{});
+      return it == 1 ? go(I1{}, F_{}) : it == 2 ? go(I2{}, F_{}) : go(I4{}, F_{});
+    });
+  });
+}
+
+int ls2_layernorm_bwd_bdr(const void* dy, const void* x, const void* w, const void* mu,
+                          const void* sigma, const void* dres, void* dx, const uint8_t* keep_bits,
+                          void* dproj, int use_drop, double dscale, void* dw, void* db,
+                          void* dbias, int tparam, int beta_mask, void* ws, int64_t rows,
+                          int64_t cols, int tin, int tout, int tstat, void* stream) {
+  if (rows <= 0) return LS2_OK;
+  if (!ln_vec_ok(cols, {dy, x, w, dres, dx, dproj}))
+    return fail(LS2_ERR_SHAPE, "layernorm_bwd_bdr: needs cols % 8 == 0, <= 1024, aligned");
+  cudaStream_t st = as_stream(stream);
+  const int nblk = ln_bwd_blocks(rows);
+  int rc = LS2_DISPATCH_IO(tin, tout, "layernorm_bwd_bdr", [&] {
+    return LS2_DISPATCH_STAT(tstat, [&] {
+      using C = typename CompOf<Tin>::type;
+      auto go = [&](auto iters, auto res, auto drop) {
+        constexpr int I = decltype(iters)::value;
+        constexpr bool R = decltype(res)::value, D = decltype(drop)::value;
+        ln_bwd_warp<Tin, Tout, Tstat, I, R, true, D><<<nblk, kLnBwdWarps * 32, 0, st>>>(
+            (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
+            (const Tin*)dres, (Tout*)dx, keep_bits, (Tout*)dproj, (C)dscale, (double*)ws, rows,
+            cols);
+        return check_launch("layernorm_bwd_bdr");
+      };
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I4 = std::integral_constant<int, 4>;
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      const int it = ln_iters(cols);
+      auto by_iters = [&](auto res, auto drop) {
+        return it == 1 ? go(I1{}, res, drop) : it == 2 ? go(I2{}, res, drop) : go(I4{}, res, drop);
+      };
+      if (dres) return use_drop ? by_iters(T_{}, T_{}) : by_iters(T_{}, F_{});
+      return use_drop ? by_iters(F_{}, T_{}) : by_iters(F_{}, F_{});
+    });
+  });
+  if (rc) return rc;
+  return LS2_DISPATCH_ONE(tparam, "layernorm_bwd_bdr_finish", [&] {
+    ln_param_finish<Tx, 3><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>(
+        (const double*)ws, nblk, cols, (Tx*)dw, (Tx*)db, (Tx*)dbias, beta_mask);
+    return check_launch("layernorm_bwd_bdr_finish");
+  });
 }
 
 int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mu,
@@ -391,12 +598,13 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
   int rc = LS2_DISPATCH_IO(tin, tout, "layernorm_bwd", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
       if (vec) {
+        using C = typename CompOf<Tin>::type;
         auto go = [&](auto iters, auto res) {
           constexpr int I = decltype(iters)::value;
           constexpr bool R = decltype(res)::value;
-          ln_bwd_warp<Tin, Tout, Tstat, I, R><<<nblk, kLnBwdWarps * 32, 0, st>>>(
+          ln_bwd_warp<Tin, Tout, Tstat, I, R, false, false><<<nblk, kLnBwdWarps * 32, 0, st>>>(
               (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
-              (const Tin*)dres, (Tout*)dx, (double*)ws, rows, cols);
+              (const Tin*)dres, (Tout*)dx, nullptr, nullptr, (C)1, (double*)ws, rows, cols);
           return check_launch("layernorm_bwd");
         };
         using I1 = std::integral_constant<int, 1>;
@@ -423,8 +631,8 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
   if (rc) return rc;
   if (!dw || !db) return LS2_OK;
   return LS2_DISPATCH_ONE(tparam, "layernorm_param_finish", [&] {
-    ln_param_finish<Tx><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>((const double*)ws, nblk, cols, (Tx*)dw,
-                                                         (Tx*)db, beta_param);
+    ln_param_finish<Tx, 2><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>(
+        (const double*)ws, nblk, cols, (Tx*)dw, (Tx*)db, nullptr, beta_param ? 3 : 0);
     return check_launch("layernorm_param_finish");
   });
 }

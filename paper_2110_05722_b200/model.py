@@ -514,6 +514,47 @@ def _nbits(n: int) -> int:
 # encoder layer (F/model.py:335-510)
 # ---------------------------------------------------------------------------
 
+def _fusable_rows(*ts) -> bool:
+    """Row-fused kernels need 16-bit/f32 storage, d % 8 == 0, d <= 1024, 16-B alignment."""
+    t0 = ts[0]
+    if t0.dtype not in (torch.float16, torch.bfloat16, torch.float32):
+        return False
+    d = t0.shape[-1]
+    if d % 8 or d > 1024:
+        return False
+    return all(t is None or (t.is_contiguous() and t.data_ptr() % 16 == 0) for t in ts)
+
+
+def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p, keep_tag,
+                 y_tag, ln):
+    """y = bias_dropout_residual(proj, bias, res) and u = LN(y): one fused pass when
+    possible (ls2_bdr_layernorm_fwd), else the two reference-shaped ops.
+    Pushes keep, y, mu, sg, u (in that order) and returns (y, u)."""
+    b, l, d = proj.shape
+    r, dt = b * l, proj.dtype
+    sdt = _stat_dtype(dt)
+    y = arena.alloc((b, l, d), dt)
+    keep = arena.alloc((_nbits(r * d),), torch.uint8)
+    mu, sg = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
+    u = arena.alloc((b, l, d), dt)
+    bb, lw, lb = _as_dt(bias, dt), _as_dt(ln_w, dt), _as_dt(ln_b, dt)
+    if _fusable_rows(proj, bb, res, y, lw, lb, u) and res.dtype == dt:
+        use, thresh, ds = K._drop_args(p_drop)
+        sv, sp = K._seed_args(seed)
+        _lib.call("ls2_bdr_layernorm_fwd", proj.data_ptr(), bb.data_ptr(), res.data_ptr(),
+                  y.data_ptr(), keep.data_ptr(), lw.data_ptr(), lb.data_ptr(), u.data_ptr(),
+                  mu.data_ptr(), sg.data_ptr(), r, d, float(eps), use, sv, sp, thresh, ds,
+                  _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.dtype_code(sdt),
+                  _lib.stream_handle())
+    else:
+        K.bias_dropout_residual(proj, bb, res, p_drop, seed, out=y, bits_out=keep)
+        K.layernorm_forward(y, lw, lb, eps, out=u, mu_out=mu, sigma_out=sg,
+                            check_degenerate=False)
+    stash.push(p + keep_tag, keep); stash.push(p + y_tag, y)
+    stash.push(p + "mu" + ln, mu); stash.push(p + "sg" + ln, sg); stash.push(p + "u" + ln, u)
+    return y, u
+
+
 def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, p):
     b, l, d = x.shape
     r, dt, hd = b * l, x.dtype, d // n_heads
@@ -543,25 +584,18 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     stash.push(p + "ctxm", ctxm)
     proj = arena.alloc((b, l, d), dt)
     _linear(ctxm.view(r, d), w.wo, None, proj.view(r, d))
-    y1 = arena.alloc((b, l, d), dt)
-    keep1 = arena.alloc((_nbits(r * d),), torch.uint8)
-    K.bias_dropout_residual(proj, _as_dt(w.bo, dt), x, p_drop, _site_seed(seed, site, 0),
-                            out=y1, bits_out=keep1)
+    # attention tail fused with the LayerNorm that follows it (ln2 in both layer kinds)
+    y1, u2 = _tail_ln_fwd(proj, w.bo, x, p_drop, _site_seed(seed, site, 0), w.ln2_w, w.ln2_b,
+                          eps, arena, stash, p, "keep1", "y1", "2")
     arena.free(proj)
-    stash.push(p + "keep1", keep1); stash.push(p + "y1", y1)
-    return y1
+    return y1, u2
 
 
-def _ffn_fwd(y_in, w, ln_w, ln_b, p_drop, seed, site, k_relu, k_tail, eps, arena, stash, p, ln):
+def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p):
+    """FFN sublayer on the already-normalized input u = LN(y_in)."""
     b, l, d = y_in.shape
     r, dt = b * l, y_in.dtype
-    sdt = _stat_dtype(dt)
     dff = w.w1.shape[0]
-    mu, sg = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
-    u = arena.alloc((b, l, d), dt)
-    K.layernorm_forward(y_in, _as_dt(ln_w, dt), _as_dt(ln_b, dt), eps, out=u, mu_out=mu,
-                        sigma_out=sg, check_degenerate=False)
-    stash.push(p + "mu" + ln, mu); stash.push(p + "sg" + ln, sg); stash.push(p + "u" + ln, u)
     a1 = arena.alloc((b, l, dff), dt)
     _linear(u.view(r, d), w.w1, None, a1.view(r, dff))
     z = arena.alloc((b, l, dff), dt)
@@ -588,12 +622,50 @@ def encoder_layer_forward(x, w: EncoderLayerWeights, mask, p_drop, seed, *, n_he
     arena = arena or NullArena()
     stash = stash if stash is not None else ActivationStash()
     x = x if isinstance(x, torch.Tensor) else K.dev(x)
-    y1 = _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, prefix)
-    y2 = _ffn_fwd(y1, w, w.ln2_w, w.ln2_b, p_drop, seed, site, 1, 2, eps, arena, stash, prefix, "2")
+    y1, u2 = _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash,
+                                 prefix)
+    y2 = _ffn_fwd(y1, u2, w, p_drop, seed, site, 1, 2, arena, stash, prefix)
     return y2, stash
 
 
-def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag):
+def _ln_bwd_tail(sink, pp, ln, du, y_in, w_ln, mu, sg, dyo, dres, keep, p_drop, bias_name,
+                 dproj) -> bool:
+    """LayerNorm backward (+ dres) fused with the preceding bias+dropout+residual
+    backward (ls2_layernorm_bwd_bdr): writes dyo and dproj and the ln.w / ln.b /
+    bias gradients in one pass.  Returns False when the shapes need the unfused ops."""
+    dt = du.dtype
+    lw = _as_dt(w_ln, dt)
+    if not (_fusable_rows(du, y_in, lw, dres, dyo, dproj) and y_in.dtype == dt
+            and mu.dtype == torch.float32):
+        return False
+    b, l, d = du.shape
+    r = b * l
+    names = (pp + ln + ".w", pp + ln + ".b", bias_name)
+    tg = [sink.target(nm) for nm in names]
+    if all(t is not None for t in tg) and len({t[0].dtype for t in tg}) == 1:
+        outs = [t[0] for t in tg]
+        mask = sum(int(t[1]) << k for k, t in enumerate(tg))
+        staged = False
+    else:
+        outs = [torch.empty(d, dtype=torch.float32, device=du.device) for _ in names]
+        mask, staged = 0, True
+    ws = _lib.context().scratch("reduce", _lib.call_i64("ls2_layernorm_bwd_ws_bytes", r, d))
+    use, _, ds = K._drop_args(p_drop)
+    _lib.call("ls2_layernorm_bwd_bdr", du.data_ptr(), y_in.data_ptr(), lw.data_ptr(),
+              mu.data_ptr(), sg.data_ptr(), _lib.ptr(dres), dyo.data_ptr(), keep.data_ptr(),
+              dproj.data_ptr(), use, ds, outs[0].data_ptr(), outs[1].data_ptr(),
+              outs[2].data_ptr(), _lib.dtype_code(outs[0]), mask, ws.data_ptr(), r, d,
+              _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.dtype_code(mu), _lib.stream_handle())
+    if staged:
+        for nm, o in zip(names, outs):
+            sink.add(nm, o)
+    return True
+
+
+def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag, tail=None):
+    """FFN sublayer backward.  tail=(bias_name, keep_tag): also run the preceding
+    attention tail's bias+dropout+residual backward in the LayerNorm pass and
+    return (dyo, dproj); otherwise return (dyo, None)."""
     b, l, d = dy.shape
     r, dt = b * l, dy.dtype
     dff = w.w1.shape[0]
@@ -620,16 +692,29 @@ def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag):
     _wgrad(sink, pp + "ffn.w1", da1.view(r, dff), u.view(r, d))
     arena.free(da1); arena.free(u)
     dyo = arena.alloc((b, l, d), dt)
-    _ln_bwd(sink, pp, "ln" + ln, du, y_in, getattr(w, f"ln{ln}_w"), mu, sg, dyo, dy)
+    dproj = None
+    if tail is not None:
+        keep = stash.pop(p + tail[1])
+        dproj = arena.alloc((b, l, d), dt)
+        if not _ln_bwd_tail(sink, pp, "ln" + ln, du, y_in, getattr(w, f"ln{ln}_w"), mu, sg, dyo,
+                            dy, keep, p_drop, tail[0], dproj):
+            _ln_bwd(sink, pp, "ln" + ln, du, y_in, getattr(w, f"ln{ln}_w"), mu, sg, dyo, dy)
+            _bdr_bwd(sink, tail[0], dyo, keep, p_drop, dproj)
+        arena.free(keep)
+    else:
+        _ln_bwd(sink, pp, "ln" + ln, du, y_in, getattr(w, f"ln{ln}_w"), mu, sg, dyo, dy)
     arena.free(du); arena.free(mu); arena.free(sg); arena.free(y_in)
     arena.free(dy)
-    return dyo
+    return dyo, dproj
 
 
-def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp):
+def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dproj=None):
+    """Self-attention sublayer backward.  dproj: the attention-tail gradient when
+    the caller already produced it (fused into the LayerNorm backward)."""
     b, l, d = dy1.shape
     r, dt, hd = b * l, dy1.dtype, d // n_heads
-    keep1 = stash.pop(p + "keep1")
+    if dproj is None:
+        keep1 = stash.pop(p + "keep1")
     ctxm = stash.pop(p + "ctxm")
     probs = stash.pop(p + "probs")
     qkv = stash.pop(p + "qkv")
@@ -637,9 +722,10 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp):
     sg1 = stash.pop(p + "sg1")
     mu1 = stash.pop(p + "mu1")
     x_in = stash.pop(p + "x_in")
-    dproj = arena.alloc((b, l, d), dt)
-    _bdr_bwd(sink, pp + "attn.bo", dy1, keep1, p_drop, dproj)
-    arena.free(keep1)
+    if dproj is None:
+        dproj = arena.alloc((b, l, d), dt)
+        _bdr_bwd(sink, pp + "attn.bo", dy1, keep1, p_drop, dproj)
+        arena.free(keep1)
     dctxm = arena.alloc((b, l, d), dt)
     K.gemm(dproj.view(r, d), _as_dt(w.wo, dt), out=dctxm.view(r, d))
     _wgrad(sink, pp + "attn.wo", dproj.view(r, d), ctxm.view(r, d))
@@ -680,8 +766,10 @@ def encoder_layer_backward(dy, w: EncoderLayerWeights, stash: ActivationStash, s
     """Backward of one encoder layer. Takes ownership of dy, returns dx."""
     arena = arena or NullArena()
     dy = dy if isinstance(dy, torch.Tensor) else K.dev(dy)
-    dy1 = _ffn_bwd(dy, w, stash, sink, p_drop, arena, prefix, param_prefix, "2", "y1")
-    return _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, prefix, param_prefix)
+    dy1, dproj = _ffn_bwd(dy, w, stash, sink, p_drop, arena, prefix, param_prefix, "2", "y1",
+                          tail=(param_prefix + "attn.bo", "keep1"))
+    return _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, prefix, param_prefix,
+                               dproj=dproj)
 
 
 # ---------------------------------------------------------------------------
@@ -699,14 +787,9 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     b, l, d = x.shape
     r, dt, hd = b * l, x.dtype, d // n_heads
     ls = k_i.shape[1]
-    sdt = _stat_dtype(dt)
     p = prefix
-    y1 = _self_attention_fwd(x, w, self_mask, p_drop, seed, site, n_heads, eps, arena, stash, p)
-    mu2, sg2 = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
-    u2 = arena.alloc((b, l, d), dt)
-    K.layernorm_forward(y1, _as_dt(w.ln2_w, dt), _as_dt(w.ln2_b, dt), eps, out=u2, mu_out=mu2,
-                        sigma_out=sg2, check_degenerate=False)
-    stash.push(p + "mu2", mu2); stash.push(p + "sg2", sg2); stash.push(p + "u2", u2)
+    y1, u2 = _self_attention_fwd(x, w, self_mask, p_drop, seed, site, n_heads, eps, arena, stash,
+                                 p)
     qc = arena.alloc((b, l, d), dt)
     _linear(u2.view(r, d), w.cross_wq, w.cross_bq, qc.view(r, d))
     stash.push(p + "qc", qc)
@@ -726,13 +809,10 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     stash.push(p + "ctxm_x", ctxm_x)
     proj_x = arena.alloc((b, l, d), dt)
     _linear(ctxm_x.view(r, d), w.cross_wo, None, proj_x.view(r, d))
-    y2 = arena.alloc((b, l, d), dt)
-    keep2 = arena.alloc((_nbits(r * d),), torch.uint8)
-    K.bias_dropout_residual(proj_x, _as_dt(w.cross_bo, dt), y1, p_drop, _site_seed(seed, site, 1),
-                            out=y2, bits_out=keep2)
+    y2, u3 = _tail_ln_fwd(proj_x, w.cross_bo, y1, p_drop, _site_seed(seed, site, 1), w.ln3_w,
+                          w.ln3_b, eps, arena, stash, p, "keep2", "y2", "3")
     arena.free(proj_x)
-    stash.push(p + "keep2", keep2); stash.push(p + "y2", y2)
-    y3 = _ffn_fwd(y2, w, w.ln3_w, w.ln3_b, p_drop, seed, site, 2, 3, eps, arena, stash, p, "3")
+    y3 = _ffn_fwd(y2, u3, w, p_drop, seed, site, 2, 3, arena, stash, p)
     return y3, stash
 
 
@@ -750,17 +830,14 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     r, dt, hd = b * l, dy.dtype, d // n_heads
     ls = k_i.shape[1]
     p, pp = prefix, param_prefix
-    dy2 = _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, "3", "y2")
-    keep2 = stash.pop(p + "keep2")
+    dy2, dproj_x = _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, "3", "y2",
+                            tail=(pp + "cross.bo", "keep2"))
     ctxm_x = stash.pop(p + "ctxm_x")
     probs_x = stash.pop(p + "probs_x")
     qc = stash.pop(p + "qc")
     u2 = stash.pop(p + "u2")
     sg2 = stash.pop(p + "sg2")
     mu2 = stash.pop(p + "mu2")
-    dproj_x = arena.alloc((b, l, d), dt)
-    _bdr_bwd(sink, pp + "cross.bo", dy2, keep2, p_drop, dproj_x)
-    arena.free(keep2)
     dctxm_x = arena.alloc((b, l, d), dt)
     K.gemm(dproj_x.view(r, d), _as_dt(w.cross_wo, dt), out=dctxm_x.view(r, d))
     _wgrad(sink, pp + "cross.wo", dproj_x.view(r, d), ctxm_x.view(r, d))
@@ -798,11 +875,17 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     _colsum_grad(sink, pp + "cross.bq", dqc.view(r, d))
     arena.free(dqc); arena.free(u2)
     y1 = stash.pop(p + "y1")
+    keep1 = stash.pop(p + "keep1")
     dy1 = arena.alloc((b, l, d), dt)
-    _ln_bwd(sink, pp, "ln2", du2, y1, w.ln2_w, mu2, sg2, dy1, dy2)
+    dproj = arena.alloc((b, l, d), dt)
+    if not _ln_bwd_tail(sink, pp, "ln2", du2, y1, w.ln2_w, mu2, sg2, dy1, dy2, keep1, p_drop,
+                        pp + "attn.bo", dproj):
+        _ln_bwd(sink, pp, "ln2", du2, y1, w.ln2_w, mu2, sg2, dy1, dy2)
+        _bdr_bwd(sink, pp + "attn.bo", dy1, keep1, p_drop, dproj)
+    arena.free(keep1)
     arena.free(du2); arena.free(mu2); arena.free(sg2); arena.free(y1)
     arena.free(dy2)
-    dx = _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp)
+    dx = _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dproj=dproj)
     return dx, dk_i, dv_i
 
 

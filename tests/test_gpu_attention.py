@@ -32,13 +32,13 @@ def _ref(q, k, v, keep, dout, scale):
         np.einsum("bhqk,bhqd->bhkd", p, dout)
 
 
-@pytest.mark.parametrize("B,H,Lq,Lk,kind", [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"),
+@pytest.mark.parametrize("B,NH,Lq,Lk,kind", [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"),
                                              (3, 2, 37, 37, "causal"), (4, 16, 128, 128, "padding"),
                                              (5, 3, 20, 52, "padding"), (2, 4, 7, 100, "none"),
                                              (2, 2, 128, 16, "none")])
-def test_fused_attention_vs_oracle(B, H, Lq, Lk, kind):
+def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind):
     rng = np.random.default_rng(B * 100 + Lq)
-    d = 64 * H
+    d = 64 * NH
     # self-attention style packed [B, L, 3d] for q/k/v when Lq == Lk, separate otherwise
     qd = (rng.normal(size=(B, Lq, d)) * 0.8).astype(np.float16)
     kd = (rng.normal(size=(B, Lk, d)) * 0.8).astype(np.float16)
@@ -52,17 +52,17 @@ def test_fused_attention_vs_oracle(B, H, Lq, Lk, kind):
     kv = torch.tensor(np.concatenate([kd, vd], axis=-1), device="cuda")   # strided K/V views
     q = torch.tensor(qd, device="cuda")
     k, v = kv[..., :d], kv[..., d:]
-    probs = torch.empty((B, H, Lq, Lk), dtype=torch.float16, device="cuda")
+    probs = torch.empty((B, NH, Lq, Lk), dtype=torch.float16, device="cuda")
     o = torch.empty((B, Lq, d), dtype=torch.float16, device="cuda")
     scale = 1.0 / math.sqrt(64)
     assert ATT.fused_ok(torch.float16, Lq, Lk, 64, mask)
-    ATT.forward(q, d, k, 2 * d, v, 2 * d, probs, o, d, B, H, Lq, Lk, 64, mask, scale)
+    ATT.forward(q, d, k, 2 * d, v, 2 * d, probs, o, d, B, NH, Lq, Lk, 64, mask, scale)
     dq = torch.empty_like(q)
     dkv = torch.zeros((B, Lk, 2 * d), dtype=torch.float16, device="cuda")
     dout = torch.tensor(dod, device="cuda")
     ATT.backward(q, d, k, 2 * d, v, 2 * d, probs, dout, d, dq, d, dkv[..., :d], 2 * d,
-                 dkv[..., d:], 2 * d, B, H, Lq, Lk, 64, scale)
-    hs = lambda x, L: x.astype(np.float32).reshape(B, L, H, 64).transpose(0, 2, 1, 3)  # noqa
+                 dkv[..., d:], 2 * d, B, NH, Lq, Lk, 64, scale)
+    hs = lambda x, L: x.astype(np.float32).reshape(B, L, NH, 64).transpose(0, 2, 1, 3)  # noqa
     p, oo, dqq, dkk, dvv = _ref(hs(qd, Lq), hs(kd, Lk), hs(vd, Lk), keep, hs(dod, Lq), scale)
     merge = lambda x: x.transpose(0, 2, 1, 3).reshape(B, x.shape[2], d)  # noqa
     assert np.abs(H(probs).astype(np.float32) - p).max() <= 2e-3
