@@ -208,6 +208,16 @@ int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_s
                      const double* out3, int64_t count_host, float post, int* nonfinite,
                      void* stream);
 int ls2_count_nonfinite_f16(const uint16_t* g16, int64_t n, int* nonfinite, void* stream);
+/* deferred column-sum finishes fused with the narrow: desc rows {dst, cols, part, nblk,
+ * stride, k} (int64), chunks {desc index, first column} (int32, one CTA per 32 columns);
+ * g16[dst + c] = RNE(f32(sum_g partial[part + g*stride + k*cols + c]) * scale) */
+int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chunks,
+                      const double* partial_base, uint16_t* g16, double loss_scale,
+                      const double* out3, int64_t count_host, float post, int* nonfinite,
+                      void* stream);
+/* number of partial rows the column-sum producers write (0: shape not deferrable) */
+int ls2_colsum_nblk(int64_t rows, int64_t cols, int dtype);
+int ls2_layernorm_bwd_nblk(int64_t rows, int64_t cols);
 
 /* ---- GEMM on cuBLAS (F/kernels.py:413-447), row-major semantics ----
  * C[b] = alpha * op(A[b]) @ op(B[b]) + beta * C[b], batch index b = (i, j) with

@@ -66,6 +66,9 @@ _SIGS = {
     "ls2_step_commit": [P, P, P, P, P],
     "ls2_scale_narrow": [P, P, L, D, P, L, Fl, P, P],
     "ls2_count_nonfinite_f16": [P, L, P, P],
+    "ls2_finish_narrow": [P, P, L, P, P, D, P, L, Fl, P, P],
+    "ls2_colsum_nblk": [L, L, I],
+    "ls2_layernorm_bwd_nblk": [L, L],
     "ls2_blas_create": [],
     "ls2_blas_destroy": [P],
     "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, I, P],
@@ -74,7 +77,8 @@ _SIGS = {
 }
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,
              "ls2_colsum_ws_bytes": L, "ls2_layernorm_bwd_ws_bytes": L,
-             "ls2_attention_supported": ctypes.c_int,
+             "ls2_attention_supported": ctypes.c_int, "ls2_colsum_nblk": ctypes.c_int,
+             "ls2_layernorm_bwd_nblk": ctypes.c_int,
              "ls2_gemm_scratch_bytes": L}
 
 _lib = None

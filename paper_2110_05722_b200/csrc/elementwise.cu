@@ -479,7 +479,7 @@ inline int colsum_generic(const void* x, int tin, int64_t rows, int64_t cols, vo
                                                   t.rpp);
       return check_launch("colsum_vec");
     });
-    if (rc) return rc;
+    if (rc || !out) return rc;
     return colsum_finish((const double*)ws, grid, cols, out, tout, beta, st);
   }
   const int nblk = colsum_blocks(ceil_div(rows, 16));
@@ -513,6 +513,11 @@ int masked_colsum(const Tin* dy, const uint8_t* kbits, const uint8_t* rbits, int
 using namespace ls2;
 
 extern "C" {
+
+int ls2_colsum_nblk(int64_t rows, int64_t cols, int dtype) {
+  if (cols % 8 != 0 || cols / 8 > 1024 || cols > 6144 || rows <= 0) return 0;
+  return colsum_blocks(tiling_cs(rows, cols, dtype == LS2_F64).passes);
+}
 
 int64_t ls2_colsum_ws_bytes(int64_t rows, int64_t cols) {
   (void)rows;
@@ -577,7 +582,7 @@ int ls2_bias_dropout_residual_bwd(const void* dy, const uint8_t* keep_bits, void
   const int64_t n = rows * cols;
   if (n <= 0) return LS2_OK;
   cudaStream_t st = as_stream(stream);
-  const bool vec = vec_ok(cols, {dy, dx}) && dbias != nullptr;
+  const bool vec = vec_ok(cols, {dy, dx});
   int rc = LS2_DISPATCH_IO(tin, tout, "bias_dropout_residual_bwd", [&] {
     auto sc = cscale<Tin>(scale);
     if (vec) {
@@ -591,7 +596,7 @@ int ls2_bias_dropout_residual_bwd(const void* dy, const uint8_t* keep_bits, void
         bdr_bwd_vec<Tin, Tout, false><<<grid, t.threads, sm, st>>>(
             (const Tin*)dy, keep_bits, (Tout*)dx, (double*)ws, rows, cols, t.cgs, t.rpp, sc);
       int r = check_launch("bias_dropout_residual_bwd");
-      if (r) return r;
+      if (r || !dbias) return r;  // dbias == NULL: partials stay in ws (deferred finish)
       return colsum_finish((const double*)ws, grid, cols, dbias, tbias, beta_bias, st);
     }
     if (use_drop)
@@ -647,7 +652,7 @@ int ls2_bias_relu_dropout_bwd(const void* dy, const uint8_t* keep_bits, const ui
   const int64_t n = rows * cols;
   if (n <= 0) return LS2_OK;
   cudaStream_t st = as_stream(stream);
-  const bool vec = vec_ok(cols, {dy, dx}) && dbias != nullptr;
+  const bool vec = vec_ok(cols, {dy, dx});
   return LS2_DISPATCH_IO(tin, tout, "bias_relu_dropout_bwd", [&] {
     auto sc = cscale<Tin>(scale);
     if (vec) {
@@ -663,7 +668,7 @@ int ls2_bias_relu_dropout_bwd(const void* dy, const uint8_t* keep_bits, const ui
             (const Tin*)dy, keep_bits, relu_bits, (Tout*)dx, (double*)ws, rows, cols, t.cgs,
             t.rpp, sc);
       int r = check_launch("bias_relu_dropout_bwd");
-      if (r) return r;
+      if (r || !dbias) return r;  // dbias == NULL: partials stay in ws (deferred finish)
       return colsum_finish((const double*)ws, grid, cols, dbias, tbias, beta_bias, st);
     }
     if (use_drop)

@@ -504,6 +504,10 @@ int ls2_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void
   });
 }
 
+int ls2_layernorm_bwd_nblk(int64_t rows, int64_t cols) {
+  return (cols % 8 == 0 && cols <= 1024 && cols >= 8) ? ln_bwd_blocks(rows) : 0;
+}
+
 int64_t ls2_layernorm_bwd_ws_bytes(int64_t rows, int64_t cols) {
   (void)rows;
   return (int64_t)kLnMaxBlocks * 3 * cols * (int64_t)sizeof(double);
@@ -578,7 +582,7 @@ int ls2_layernorm_bwd_bdr(const void* dy, const void* x, const void* w, const vo
       return use_drop ? by_iters(F_{}, T_{}) : by_iters(F_{}, F_{});
     });
   });
-  if (rc) return rc;
+  if (rc || !dw) return rc;   // dw == NULL: partials stay in ws (deferred finish)
   return LS2_DISPATCH_ONE(tparam, "layernorm_bwd_bdr_finish", [&] {
     ln_param_finish<Tx, 3><<<(unsigned)ceil_div(cols, 32), 1024, 0, st>>>(
         (const double*)ws, nblk, cols, (Tx*)dw, (Tx*)db, (Tx*)dbias, beta_mask);

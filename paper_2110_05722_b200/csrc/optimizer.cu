@@ -161,6 +161,55 @@ __global__ void scale_narrow_kernel(const float* __restrict__ acc, uint16_t* __r
   }
 }
 
+// Deferred column-sum finishes fused with the narrow pass.  Every bias / LayerNorm
+// parameter gradient of the step was left as per-block partial column sums
+// (partial[g][k][c], g < nblk) by its producing kernel; one launch reduces them
+// all in fixed order, scales like scale_narrow and writes the fp16 gradients.
+// desc row: {dst (element offset in the workspace), cols, part (double offset),
+//            nblk, stride (doubles per block), k}
+__global__ void __launch_bounds__(1024) finish_narrow_kernel(
+    const int64_t* __restrict__ desc, const int32_t* __restrict__ chunks,
+    const double* __restrict__ part_base, uint16_t* __restrict__ g16, double loss_scale,
+    const double* out3, int64_t count_host, float post, int* nonfinite) {
+  __shared__ double red[32][33];
+  const int di = chunks[2 * blockIdx.x], c0 = chunks[2 * blockIdx.x + 1];
+  const int64_t* d = desc + 6 * di;
+  const int64_t dst = d[0], cols = d[1], part = d[2], stride = d[4], k = d[5];
+  const int nblk = (int)d[3];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = c0 + lane;
+  const double* p = part_base + part + k * cols + c;
+  double s0 = 0, s1 = 0;
+  if (c < cols) {
+    int g = w;
+    for (; g + 32 < nblk; g += 64) {
+      s0 += p[(int64_t)g * stride];
+      s1 += p[(int64_t)(g + 32) * stride];
+    }
+    for (; g < nblk; g += 32) s0 += p[(int64_t)g * stride];
+  }
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0) {
+    int bad = 0;
+    if (c < cols) {
+      double s = 0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) s += red[q][lane];
+      double cnt = count_host >= 0 ? (double)count_host : out3[1];
+      if (cnt < 1.0) cnt = 1.0;
+      const float sc = __fmul_rn((float)(loss_scale / cnt), post);
+      const uint16_t h = f2h(__fmul_rn((float)s, sc));
+      g16[dst + c] = h;
+      bad = h_nonfinite(h);
+    }
+    if (nonfinite) {
+      bad = warp_count(bad);
+      if (lane == 0 && bad) atomicAdd(nonfinite, bad);
+    }
+  }
+}
+
 __global__ void count_nonfinite_kernel(const uint16_t* __restrict__ g16, int64_t n, int* nonfinite) {
   int bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -216,6 +265,17 @@ int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_s
   scale_narrow_kernel<<<stream_grid(vec ? ceil_div(n, 8) : n), 256, 0, as_stream(stream)>>>(
       acc32, g16, n, loss_scale, out3, count_host, post, nonfinite, vec);
   return check_launch("scale_narrow");
+}
+
+int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chunks,
+                      const double* partial_base, uint16_t* g16, double loss_scale,
+                      const double* out3, int64_t count_host, float post, int* nonfinite,
+                      void* stream) {
+  if (n_chunks <= 0) return LS2_OK;
+  if (count_host < 0 && !out3) return fail(LS2_ERR_SHAPE, "finish_narrow: no token count");
+  finish_narrow_kernel<<<(unsigned)n_chunks, 1024, 0, as_stream(stream)>>>(
+      desc, chunks, partial_base, g16, loss_scale, out3, count_host, post, nonfinite);
+  return check_launch("finish_narrow");
 }
 
 int ls2_count_nonfinite_f16(const uint16_t* g16, int64_t n, int* nonfinite, void* stream) {

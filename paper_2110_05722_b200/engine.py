@@ -130,6 +130,7 @@ class TrainingEngine:
         self._io: dict = {}
         self._graphs: dict = {}
         self._launches: dict = {}
+        self._finish_tables: dict = {}
         self.use_graphs = bool(t.cuda_graphs)
         self.last_out3 = None
 
@@ -143,7 +144,7 @@ class TrainingEngine:
 
     def _record_shape(self, batch: Batch, compute_grads: bool):
         rec = RecordingArena(self.device)
-        sink = _ViewSink(self.gviews) if compute_grads else None
+        sink = _ViewSink(self.gviews, defer=True) if compute_grads else None
         self.model.forward_backward(self.pviews, batch,
                                     p_drop=self.cfg.train.p_drop if compute_grads else 0.0,
                                     alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
@@ -187,13 +188,13 @@ class TrainingEngine:
         if upload:
             io.upload()
         self.arena.begin(key)
-        sink = _ViewSink(self.gviews)
+        sink = _ViewSink(self.gviews, defer=True)
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
             arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
             upload_seeds=upload)
         self.arena.end()
-        return out.out3
+        return out.out3, sink
 
     def capture_device_graph(self, key):
         """Graph of one step with device-resident inputs (no H2D/D2H): the
@@ -205,8 +206,8 @@ class TrainingEngine:
         n0 = _lib.launches()
         with _no_gc():
             with torch.cuda.graph(g):
-                out3 = self._fwd_bwd(io, key, 0, upload=False)
-                self._update(out3, host_copy=False)
+                out3, sink = self._fwd_bwd(io, key, 0, upload=False)
+                self._update(out3, sink, host_copy=False)
         self._launches[key] = _lib.launches() - n0
         torch.cuda.synchronize()
         return g
@@ -218,10 +219,31 @@ class TrainingEngine:
         """One eager step on already-resident inputs (DP fallback for timing)."""
         io = self._io_for(key[1], key[2])
         n0 = _lib.launches()
-        self._update(self._fwd_bwd(io, key, step, upload=False), host_copy=False)
+        self._update(*self._fwd_bwd(io, key, step, upload=False), host_copy=False)
         self._launches[key] = _lib.launches() - n0
 
-    def _update(self, out3: torch.Tensor, host_copy: bool = True):
+    def _finish_deferred(self, sink, out3, nonfinite_ptr):
+        """One launch finishing every deferred bias / LayerNorm gradient (partials
+        left by their producers) straight into the fp16 workspace."""
+        if sink is None or not sink.deferred:
+            return
+        key = tuple((n, buf.data_ptr(), nb, st, k, c) for n, buf, nb, st, k, c in sink.deferred)
+        tab = self._finish_tables.get(key)
+        if tab is None:
+            desc, chunks = [], []
+            for i, (n, ptr, nb, st, k, c) in enumerate(key):
+                off, _ = self.ws.resolve(n)
+                desc.append([off, c, ptr // 8, nb, st, k])
+                chunks += [(i, c0) for c0 in range(0, c, 32)]
+            tab = (torch.tensor(desc, dtype=torch.int64, device=self.device),
+                   torch.tensor(chunks, dtype=torch.int32, device=self.device), len(chunks))
+            self._finish_tables[key] = tab
+        t = self.cfg.train
+        _lib.call("ls2_finish_narrow", tab[0].data_ptr(), tab[1].data_ptr(), tab[2], None,
+                  self.ws.grads16.data_ptr(), float(t.loss_scale), out3.data_ptr(), -1,
+                  float(1.0 / t.act_grad_scale), nonfinite_ptr, _lib.stream_handle())
+
+    def _update(self, out3: torch.Tensor, sink=None, host_copy: bool = True):
         """narrow(+scale) -> [all-reduce] -> non-finite count -> Adam/SGD -> commit."""
         st = _lib.stream_handle()
         t = self.cfg.train
@@ -233,6 +255,7 @@ class TrainingEngine:
                   ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
                   float(1.0 / t.act_grad_scale),
                   None if self.dp.active else self._nonfinite.data_ptr(), st)
+        self._finish_deferred(sink, out3, None if self.dp.active else self._nonfinite.data_ptr())
         if self.dp.active:
             self.dp.allreduce_grads(ws.grads16)
             _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr(), ws.n_elements,
@@ -262,12 +285,9 @@ class TrainingEngine:
             if g is not None:
                 g.replay()
                 return
-        out3 = self._fwd_bwd(io, key, step)
+        out3, sink = self._fwd_bwd(io, key, step)
         self.last_out3 = out3
-        if not self.dp.active or not graphed:
-            self._update(out3)
-        else:
-            self._update(out3)
+        self._update(out3, sink)
 
     def _capture(self, io, key, step):
         """Capture fwd/bwd + update of this bucket into one CUDA graph."""
@@ -276,8 +296,8 @@ class TrainingEngine:
         g = torch.cuda.CUDAGraph()
         with _no_gc():
             with torch.cuda.graph(g):
-                out3 = self._fwd_bwd(io, key, step)
-                self._update(out3)
+                out3, sink = self._fwd_bwd(io, key, step)
+                self._update(out3, sink)
         self._graphs[key] = g
         torch.cuda.synchronize()
 

@@ -82,7 +82,7 @@ def softmax_backward(dy, cache: SoftmaxCache, out=None, out_scale: float = 1.0):
 
 
 def layernorm_backward(dy, x, w, cache: LNCache, out=None, dres=None, dw_out=None, db_out=None,
-                       beta: int = 0):
+                       beta: int = 0, partials_out=None):
     """Rearranged LayerNorm backward: dx plus affine parameter grads (dw, db).
 
     dres (optional) is added to dx in the same pass (the residual branch of
@@ -99,66 +99,87 @@ def layernorm_backward(dy, x, w, cache: LNCache, out=None, dres=None, dw_out=Non
     mu = dev(mu, tstat).reshape(-1)
     sg = dev(sg, tstat).reshape(-1)
     dx, orig = _out(out, xt.shape, tout, xt.device)
-    dw = dw_out if dw_out is not None else torch.empty(m, dtype=pdt, device=xt.device)
-    db = db_out if db_out is not None else torch.empty(m, dtype=pdt, device=xt.device)
-    if dw.dtype != db.dtype:
-        raise ShapeMismatch("dw/db dtypes differ")
-    ws = _scratch("reduce", _lib.call_i64("ls2_layernorm_bwd_ws_bytes", r, m))
+    if partials_out is not None:      # deferred finish: partial[blk][2][m] stays in partials_out
+        dw = db = None
+        ws = partials_out
+    else:
+        dw = dw_out if dw_out is not None else torch.empty(m, dtype=pdt, device=xt.device)
+        db = db_out if db_out is not None else torch.empty(m, dtype=pdt, device=xt.device)
+        if dw.dtype != db.dtype:
+            raise ShapeMismatch("dw/db dtypes differ")
+        ws = _scratch("reduce", _lib.call_i64("ls2_layernorm_bwd_ws_bytes", r, m))
     _lib.call("ls2_layernorm_bwd", d_.data_ptr(), xt.data_ptr(), wt.data_ptr(), mu.data_ptr(),
-              sg.data_ptr(), _lib.ptr(rt), dx.data_ptr(), dw.data_ptr(), db.data_ptr(),
-              _lib.dtype_code(dw), int(beta), ws.data_ptr(), r, m, _lib.dtype_code(tin),
-              _lib.dtype_code(tout), _lib.dtype_code(tstat), _lib.stream_handle())
+              sg.data_ptr(), _lib.ptr(rt), dx.data_ptr(), _lib.ptr(dw), _lib.ptr(db),
+              _lib.dtype_code(dw if dw is not None else pdt), int(beta), ws.data_ptr(), r, m,
+              _lib.dtype_code(tin), _lib.dtype_code(tout), _lib.dtype_code(tstat),
+              _lib.stream_handle())
     return _finish(dx, orig), dw, db
 
 
 def bias_dropout_residual_backward(dy, mask: DropoutMask, out=None, dbias_out=None,
-                                   beta: int = 0):
-    """dx = keep * dy / (1 - p); dbias = column sums of dx; dresidual IS dy."""
+                                   beta: int = 0, partials_out=None):
+    """dx = keep * dy / (1 - p); dbias = column sums of dx; dresidual IS dy.
+
+    partials_out: leave dbias as per-block partial sums there (deferred finish);
+    dbias is then returned as None."""
     tout = out.dtype if out is not None else compute_dtype(dy)
     (d_,), tin = io_tensors([dy], tout)
     cols = d_.shape[-1]
     rows = d_.numel() // cols
     dx, orig = _out(out, d_.shape, tout, d_.device)
     pdt = compute_dtype(dy)
-    db = dbias_out if dbias_out is not None else torch.empty(cols, dtype=pdt, device=d_.device)
+    if partials_out is not None:
+        db, ws = None, partials_out
+    else:
+        db = dbias_out if dbias_out is not None else torch.empty(cols, dtype=pdt, device=d_.device)
+        ws = _scratch("reduce", _lib.call_i64("ls2_colsum_ws_bytes", rows, cols))
     use = 1 if mask.p > 0.0 else 0
     bits = mask.bitmask() if use else None
-    ws = _scratch("reduce", _lib.call_i64("ls2_colsum_ws_bytes", rows, cols))
     _lib.call("ls2_bias_dropout_residual_bwd", d_.data_ptr(), _lib.ptr(bits), dx.data_ptr(),
-              db.data_ptr(), _lib.dtype_code(db), int(beta), ws.data_ptr(), rows, cols, use,
-              1.0 / (1.0 - mask.p) if use else 1.0, _lib.dtype_code(tin), _lib.dtype_code(tout),
-              _lib.stream_handle())
+              _lib.ptr(db), _lib.dtype_code(db if db is not None else pdt), int(beta),
+              ws.data_ptr(), rows, cols, use, 1.0 / (1.0 - mask.p) if use else 1.0,
+              _lib.dtype_code(tin), _lib.dtype_code(tout), _lib.stream_handle())
     return _finish(dx, orig), db, dy
 
 
 def bias_relu_dropout_backward(dy, dropmask: DropoutMask, relu_mask, out=None, dbias_out=None,
-                               beta: int = 0):
-    """dx = relu_mask * keep * dy / (1 - p); dbias reduces dx over rows."""
+                               beta: int = 0, partials_out=None):
+    """dx = relu_mask * keep * dy / (1 - p); dbias reduces dx over rows.
+
+    partials_out: deferred finish, as in bias_dropout_residual_backward."""
     tout = out.dtype if out is not None else compute_dtype(dy)
     (d_,), tin = io_tensors([dy], tout)
     cols = d_.shape[-1]
     rows = d_.numel() // cols
     dx, orig = _out(out, d_.shape, tout, d_.device)
     pdt = compute_dtype(dy)
-    db = dbias_out if dbias_out is not None else torch.empty(cols, dtype=pdt, device=d_.device)
+    if partials_out is not None:
+        db, ws = None, partials_out
+    else:
+        db = dbias_out if dbias_out is not None else torch.empty(cols, dtype=pdt, device=d_.device)
+        ws = _scratch("reduce", _lib.call_i64("ls2_colsum_ws_bytes", rows, cols))
     use = 1 if dropmask.p > 0.0 else 0
     kb = dropmask.bitmask() if use else None
     rb = as_bits(relu_mask, d_.shape)
-    ws = _scratch("reduce", _lib.call_i64("ls2_colsum_ws_bytes", rows, cols))
     _lib.call("ls2_bias_relu_dropout_bwd", d_.data_ptr(), _lib.ptr(kb), rb.data_ptr(),
-              dx.data_ptr(), db.data_ptr(), _lib.dtype_code(db), int(beta), ws.data_ptr(), rows,
-              cols, use, 1.0 / (1.0 - dropmask.p) if use else 1.0, _lib.dtype_code(tin),
-              _lib.dtype_code(tout), _lib.stream_handle())
+              dx.data_ptr(), _lib.ptr(db), _lib.dtype_code(db if db is not None else pdt),
+              int(beta), ws.data_ptr(), rows, cols, use, 1.0 / (1.0 - dropmask.p) if use else 1.0,
+              _lib.dtype_code(tin), _lib.dtype_code(tout), _lib.stream_handle())
     return _finish(dx, orig), db
 
 
-def column_sum(x, out=None, beta: int = 0):
-    """Deterministic float64-accumulated column sums of x[..., c] (bias grads)."""
+def column_sum(x, out=None, beta: int = 0, partials_out=None):
+    """Deterministic float64-accumulated column sums of x[..., c] (bias grads).
+    partials_out: leave per-block partials there (deferred finish), return None."""
     xt = x if isinstance(x, torch.Tensor) else dev(x)
     if not xt.is_contiguous():
         xt = xt.contiguous()
     cols = xt.shape[-1]
     rows = xt.numel() // cols
+    if partials_out is not None:
+        _lib.call("ls2_colsum", xt.data_ptr(), _lib.dtype_code(xt), None, _lib.F32, 0,
+                  partials_out.data_ptr(), rows, cols, _lib.stream_handle())
+        return None
     o = out if out is not None else torch.empty(cols, dtype=compute_dtype(xt), device=xt.device)
     ws = _scratch("reduce", _lib.call_i64("ls2_colsum_ws_bytes", rows, cols))
     _lib.call("ls2_colsum", xt.data_ptr(), _lib.dtype_code(xt), o.data_ptr(), _lib.dtype_code(o),

@@ -342,9 +342,14 @@ class _ViewSink(GradSink):
     """Writes into preallocated views of the fp32 gradient workspace; the first
     producer of a name overwrites (beta=0), later producers accumulate."""
 
-    def __init__(self, store: dict):
+    def __init__(self, store: dict, defer: bool = False):
         super().__init__(store)
         self.written: set = set()
+        # deferred column sums: the producer leaves per-block partials in an arena
+        # buffer and the engine finishes them all inside the fp16 narrow pass
+        self.defer_enabled = defer
+        self.deferred: list = []          # (name, buf, nblk, stride, k, cols)
+        self.arena = None
 
     def add(self, name: str, value):
         if name in self.written:
@@ -358,6 +363,40 @@ class _ViewSink(GradSink):
         self.written.add(name)
         return self.store[name], beta
 
+    def defer_buffer(self, names, nblk: int, np_: int, cols: int):
+        """Arena buffer for nblk x np_ x cols partials of `names`, or None."""
+        if not self.defer_enabled or self.arena is None or nblk <= 0 or \
+                any(n in self.written for n in names):
+            return None
+        buf = self.arena.alloc((nblk * np_ * cols,), torch.float64)
+        for k, n in enumerate(names):
+            self.written.add(n)
+            self.deferred.append((n, buf, nblk, np_ * cols, k, cols))
+        return buf
+
+    def deferred_buffers(self):
+        seen, out = set(), []
+        for _, buf, *_ in self.deferred:
+            if id(buf) not in seen:
+                seen.add(id(buf))
+                out.append(buf)
+        return out
+
+
+def _defer(sink, names, nblk, np_, cols):
+    fn = getattr(sink, "defer_buffer", None)
+    return fn(names, nblk, np_, cols) if fn is not None else None
+
+
+def _aligned(*ts) -> bool:
+    return all(t is None or (t.is_contiguous() and t.data_ptr() % 16 == 0) for t in ts)
+
+
+def _colsum_nblk(rows, cols, t) -> int:
+    if t.dtype == torch.float64:
+        return 0
+    return int(_lib._lib.ls2_colsum_nblk(rows, cols, _lib.dtype_code(t)))
+
 
 def _wgrad(sink, name, dy2d, x2d):
     """dW = dy^T x straight into the sink (cuBLAS, fp32 output)."""
@@ -370,6 +409,12 @@ def _wgrad(sink, name, dy2d, x2d):
 
 
 def _colsum_grad(sink, name, x2d):
+    rows, cols = x2d.shape
+    if _aligned(x2d):
+        buf = _defer(sink, [name], _colsum_nblk(rows, cols, x2d), 1, cols)
+        if buf is not None:
+            G.column_sum(x2d, partials_out=buf)
+            return
     tgt = sink.target(name)
     if tgt is None:
         sink.add(name, G.column_sum(x2d))
@@ -391,8 +436,17 @@ def _ln_targets(sink, pp, ln):
 
 
 def _ln_bwd(sink, pp, ln, du, x_in, w, mu, sg, out, dres):
+    wt = _as_dt(w, du.dtype)
+    rows, cols = du.numel() // du.shape[-1], du.shape[-1]
+    if du.dtype != torch.float64 and _aligned(du, x_in, wt, out, dres):
+        nblk = int(_lib._lib.ls2_layernorm_bwd_nblk(rows, cols))
+        buf = _defer(sink, [pp + ln + ".w", pp + ln + ".b"], nblk, 2, cols)
+        if buf is not None:
+            G.layernorm_backward(du, x_in, wt, LNCache(mu, sg), out=out, dres=dres,
+                                 partials_out=buf)
+            return
     dwv, dbv, beta = _ln_targets(sink, pp, ln)
-    _, dw, db = G.layernorm_backward(du, x_in, _as_dt(w, du.dtype), LNCache(mu, sg), out=out,
+    _, dw, db = G.layernorm_backward(du, x_in, wt, LNCache(mu, sg), out=out,
                                      dres=dres, dw_out=dwv, db_out=dbv, beta=beta)
     if dwv is None:
         sink.add(pp + ln + ".w", dw)
@@ -400,19 +454,30 @@ def _ln_bwd(sink, pp, ln, du, x_in, w, mu, sg, out, dres):
 
 
 def _bdr_bwd(sink, name, dy, keep_bits, p_drop, out):
+    mask = DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dy.shape))
+    rows, cols = dy.numel() // dy.shape[-1], dy.shape[-1]
+    if _aligned(dy, out):
+        buf = _defer(sink, [name], _colsum_nblk(rows, cols, dy), 1, cols)
+        if buf is not None:
+            G.bias_dropout_residual_backward(dy, mask, out=out, partials_out=buf)
+            return
     dv, beta, direct = _bias_target(sink, name)
-    _, db, _ = G.bias_dropout_residual_backward(
-        dy, DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dy.shape)), out=out,
-        dbias_out=dv, beta=beta)
+    _, db, _ = G.bias_dropout_residual_backward(dy, mask, out=out, dbias_out=dv, beta=beta)
     if not direct:
         sink.add(name, db)
 
 
 def _brd_bwd(sink, name, dz, keep_bits, relu_bits, p_drop, out):
+    mask = DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dz.shape))
+    relu = ReluMask(bits=relu_bits, shape=tuple(dz.shape))
+    rows, cols = dz.numel() // dz.shape[-1], dz.shape[-1]
+    if _aligned(dz, out):
+        buf = _defer(sink, [name], _colsum_nblk(rows, cols, dz), 1, cols)
+        if buf is not None:
+            G.bias_relu_dropout_backward(dz, mask, relu, out=out, partials_out=buf)
+            return
     dv, beta, direct = _bias_target(sink, name)
-    _, db = G.bias_relu_dropout_backward(
-        dz, DropoutMask(p=p_drop, bits=keep_bits, shape=tuple(dz.shape)),
-        ReluMask(bits=relu_bits, shape=tuple(dz.shape)), out=out, dbias_out=dv, beta=beta)
+    _, db = G.bias_relu_dropout_backward(dz, mask, relu, out=out, dbias_out=dv, beta=beta)
     if not direct:
         sink.add(name, db)
 
@@ -641,20 +706,24 @@ def _ln_bwd_tail(sink, pp, ln, du, y_in, w_ln, mu, sg, dyo, dres, keep, p_drop, 
     b, l, d = du.shape
     r = b * l
     names = (pp + ln + ".w", pp + ln + ".b", bias_name)
-    tg = [sink.target(nm) for nm in names]
-    if all(t is not None for t in tg) and len({t[0].dtype for t in tg}) == 1:
-        outs = [t[0] for t in tg]
-        mask = sum(int(t[1]) << k for k, t in enumerate(tg))
-        staged = False
+    ws = _defer(sink, list(names), int(_lib._lib.ls2_layernorm_bwd_nblk(r, d)), 3, d)
+    if ws is not None:                    # partials only; finished inside the narrow pass
+        outs, mask, staged = [None, None, None], 0, False
     else:
-        outs = [torch.empty(d, dtype=torch.float32, device=du.device) for _ in names]
-        mask, staged = 0, True
-    ws = _lib.context().scratch("reduce", _lib.call_i64("ls2_layernorm_bwd_ws_bytes", r, d))
+        tg = [sink.target(nm) for nm in names]
+        if all(t is not None for t in tg) and len({t[0].dtype for t in tg}) == 1:
+            outs = [t[0] for t in tg]
+            mask = sum(int(t[1]) << k for k, t in enumerate(tg))
+            staged = False
+        else:
+            outs = [torch.empty(d, dtype=torch.float32, device=du.device) for _ in names]
+            mask, staged = 0, True
+        ws = _lib.context().scratch("reduce", _lib.call_i64("ls2_layernorm_bwd_ws_bytes", r, d))
     use, _, ds = K._drop_args(p_drop)
     _lib.call("ls2_layernorm_bwd_bdr", du.data_ptr(), y_in.data_ptr(), lw.data_ptr(),
               mu.data_ptr(), sg.data_ptr(), _lib.ptr(dres), dyo.data_ptr(), keep.data_ptr(),
-              dproj.data_ptr(), use, ds, outs[0].data_ptr(), outs[1].data_ptr(),
-              outs[2].data_ptr(), _lib.dtype_code(outs[0]), mask, ws.data_ptr(), r, d,
+              dproj.data_ptr(), use, ds, _lib.ptr(outs[0]), _lib.ptr(outs[1]),
+              _lib.ptr(outs[2]), _lib.F32, mask, ws.data_ptr(), r, d,
               _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.dtype_code(mu), _lib.stream_handle())
     if staged:
         for nm, o in zip(names, outs):
@@ -1025,6 +1094,8 @@ class Transformer:
         arena = arena or NullArena(ctx.device)
         stash = ActivationStash()
         sink = GradSink() if sink is None else sink
+        if isinstance(sink, _ViewSink):
+            sink.arena = arena
         emit = trace.append if trace is not None else (lambda ev: None)
         if validate:
             validate_batch(batch, cfg)
@@ -1171,6 +1242,10 @@ class Transformer:
         arena.free(dh); arena.free(keep_src)
         if len(stash):
             raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")
+        # deferred gradient partials are consumed by the engine's narrow pass, which
+        # is stream-ordered after this step and before any reuse of the arena
+        for buf in getattr(sink, "deferred_buffers", lambda: [])():
+            arena.free(buf)
         return out
 
     def _embedding_grads(self, sink, dy, tokens, keep_bits, p_drop, emb_cfg):
