@@ -47,6 +47,32 @@ __device__ MaxIdx block_argmax(MaxIdx m) {
   return r;
 }
 
+__device__ float block_max(float v) {
+  __shared__ float s[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s[wid] = v;
+  __syncthreads();
+  float r = s[0];
+  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) r = fmaxf(r, s[k]);
+  __syncthreads();
+  return r;
+}
+
+__device__ int block_min(int v) {
+  __shared__ int s[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s[wid] = v;
+  __syncthreads();
+  int r = s[0];
+  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) r = min(r, s[k]);
+  __syncthreads();
+  return r;
+}
+
 template <typename T>
 __device__ T block_sum(T v) {
   __shared__ T s[32];
@@ -60,10 +86,16 @@ __device__ T block_sum(T v) {
   return r;
 }
 
+// exp(h - max) in (0, 1] is cached in the logits' storage type; for fp16 it is
+// scaled by 2^15 so values down to ~1e-9 stay normal (fp16 subnormals would
+// cost the gradient precision of the smallest probabilities)
+template <typename T> struct ExCache { static constexpr float kScale = 1.f, kInv = 1.f; };
+template <> struct ExCache<__half> { static constexpr float kScale = 32768.f, kInv = 1.f / 32768.f; };
+
 // ITERS > 0: register-cached single pass (8*ITERS elements per thread);
 // ITERS == 0: two passes over the row.
 template <typename T, int ITERS>
-__global__ void __launch_bounds__(kCeThreads, 2) criterion_kernel(
+__global__ void __launch_bounds__(kCeThreads, ITERS >= 4 ? 1 : 2) criterion_kernel(
     const T* __restrict__ logits, const int64_t* __restrict__ targets, T* dlogits, T* logq_out,
     double* __restrict__ row_stats, int* __restrict__ bad_target, int64_t rows, int64_t V,
     double alpha, int64_t pad_id, int has_pad, double grad_scale) {
@@ -80,45 +112,101 @@ __global__ void __launch_bounds__(kCeThreads, 2) criterion_kernel(
   MaxIdx mi{-INFINITY, INT64_MAX};
   float sh = 0.f;
   if (ITERS > 0) {
+    // pass 1: max and sum of logits (fp32 max only; the argmax index is found
+    // afterwards as the first position holding the row max: numpy's tie rule)
+    float m = -INFINITY;
 #pragma unroll
     for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
-      const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
+      const int c0 = (it * kCeThreads + (int)threadIdx.x) * 8;
       if (c0 < V) cache[it] = ld8_stream(h + c0);
     }
 #pragma unroll
     for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
-      const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
+      const int c0 = (it * kCeThreads + (int)threadIdx.x) * 8;
       if (c0 < V) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float v = cvt<float>(cache[it].v[e]);
           sh += v;
-          mi_merge(mi, MaxIdx{v, c0 + e});
+          m = fmaxf(m, v);
         }
       }
     }
-  } else {
-    for (int64_t c = threadIdx.x; c < V; c += kCeThreads) {
-      const float v = cvt<float>(h[c]);
-      sh += v;
-      mi_merge(mi, MaxIdx{v, c});
+    const float mx = block_max(m);
+    // pass 2: first index of the max, and e = exp(h - max) (kept in the cache in
+    // place of h unless log-probabilities are requested)
+    int first = INT32_MAX;
+    float z = 0.f;
+    const float l2e = 1.4426950408889634f, mxl = mx * l2e;
+#pragma unroll
+    for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
+      const int c0 = (it * kCeThreads + (int)threadIdx.x) * 8;
+      if (c0 < V) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = cvt<float>(cache[it].v[e]);
+          if (v == mx && c0 + e < first) first = c0 + e;
+          const float ex = exp2f(fmaf(v, l2e, -mxl));
+          z += ex;
+          if (!logq_out) cache[it].v[e] = cvt<T>(ex * ExCache<T>::kScale);
+        }
+      }
     }
+    first = block_min(first);
+    z = block_sum(z);
+    const double shd = block_sum((double)sh);
+    const double lse = (double)mx + log((double)z);
+    if (threadIdx.x == 0) {
+      double loss = 0.0;
+      if (valid && tgt_ok) {
+        const double ht = (double)cvt<float>(h[tgt]);
+        loss = -(1.0 - alpha) * (ht - lse) - (alpha / (double)V) * (shd - (double)V * lse);
+      }
+      row_stats[2 * r] = loss;
+      row_stats[2 * r + 1] = (valid && tgt_ok && first == tgt) ? 1.0 : 0.0;
+    }
+    const float rz = 1.f / z;
+    const float lz = (float)log((double)z);
+    const float a_v = (float)(alpha / (double)V);
+    const float one_m_a = (float)(1.0 - alpha);
+    const float gs = (float)grad_scale;
+    __syncthreads();  // all reads of h[tgt] are done before the in-place overwrite
+#pragma unroll
+    for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
+      const int c0 = (it * kCeThreads + (int)threadIdx.x) * 8;
+      if (c0 < V) {
+        if (logq_out) {
+          Pack8<T> q;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) q.v[e] = cvt<T>((cvt<float>(cache[it].v[e]) - mx) - lz);
+          st8(logq_out + r * V + c0, q);
+        }
+        if (dlogits) {
+          Pack8<T> q;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float ex = logq_out ? exp2f(fmaf(cvt<float>(cache[it].v[e]), l2e, -mxl))
+                                      : cvt<float>(cache[it].v[e]) * ExCache<T>::kInv;
+            float g = ex * rz - a_v;
+            if (c0 + e == tgt) g -= one_m_a;
+            q.v[e] = cvt<T>(valid ? g * gs : 0.f);
+          }
+          st8(dlogits + r * V + c0, q);
+        }
+      }
+    }
+    return;
+  }
+  // two-pass fallback for rows that do not fit in registers (second read hits L2)
+  for (int64_t c = threadIdx.x; c < V; c += kCeThreads) {
+    const float v = cvt<float>(h[c]);
+    sh += v;
+    mi_merge(mi, MaxIdx{v, c});
   }
   mi = block_argmax(mi);
   const float mx = mi.v;
   float z = 0.f;
-  if (ITERS > 0) {
-#pragma unroll
-    for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
-      const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
-      if (c0 < V) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) z += __expf(cvt<float>(cache[it].v[e]) - mx);
-      }
-    }
-  } else {
-    for (int64_t c = threadIdx.x; c < V; c += kCeThreads) z += __expf(cvt<float>(h[c]) - mx);
-  }
+  for (int64_t c = threadIdx.x; c < V; c += kCeThreads) z += __expf(cvt<float>(h[c]) - mx);
   z = block_sum(z);
   const double shd = block_sum((double)sh);
   const double lse = (double)mx + log((double)z);
@@ -137,38 +225,13 @@ __global__ void __launch_bounds__(kCeThreads, 2) criterion_kernel(
   const float one_m_a = (float)(1.0 - alpha);
   const float gs = (float)grad_scale;
   __syncthreads();  // all reads of h[tgt] are done before the in-place overwrite
-  if (ITERS > 0) {
-#pragma unroll
-    for (int it = 0; it < (ITERS > 0 ? ITERS : 1); ++it) {
-      const int64_t c0 = ((int64_t)it * kCeThreads + threadIdx.x) * 8;
-      if (c0 < V) {
-        if (logq_out) {
-          Pack8<T> q;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) q.v[e] = cvt<T>((cvt<float>(cache[it].v[e]) - mx) - lz);
-          st8(logq_out + r * V + c0, q);
-        }
-        if (dlogits) {
-          Pack8<T> q;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            float g = __expf(cvt<float>(cache[it].v[e]) - mx) * rz - a_v;
-            if (c0 + e == tgt) g -= one_m_a;
-            q.v[e] = cvt<T>(valid ? g * gs : 0.f);
-          }
-          st8(dlogits + r * V + c0, q);
-        }
-      }
-    }
-  } else {
-    for (int64_t c = threadIdx.x; c < V; c += kCeThreads) {
-      const float sv = cvt<float>(h[c]) - mx;
-      if (logq_out) logq_out[r * V + c] = cvt<T>(sv - lz);
-      if (dlogits) {
-        float g = __expf(sv) * rz - a_v;
-        if (c == tgt) g -= one_m_a;
-        dlogits[r * V + c] = cvt<T>(valid ? g * gs : 0.f);
-      }
+  for (int64_t c = threadIdx.x; c < V; c += kCeThreads) {
+    const float sv = cvt<float>(h[c]) - mx;
+    if (logq_out) logq_out[r * V + c] = cvt<T>(sv - lz);
+    if (dlogits) {
+      float g = __expf(sv) * rz - a_v;
+      if (c == tgt) g -= one_m_a;
+      dlogits[r * V + c] = cvt<T>(valid ? g * gs : 0.f);
     }
   }
 }
