@@ -7,6 +7,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <type_traits>
 
@@ -164,6 +167,31 @@ __device__ __forceinline__ T warp_max(T v, int width = 32) {
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// grid = min(work blocks, every resident slot on the chip): one full wave of a
+// grid-stride kernel instead of 1.x waves with an idle tail
+inline int resident_grid(const void* fn, int threads, size_t smem, int64_t want) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto key = std::make_tuple(fn, threads, smem);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 1;
+      }
+      if (per_sm < 1) per_sm = 1;
+      cache[key] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
+  const int64_t cap = (int64_t)kNumSMs * per_sm;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
 
 inline int grid_for(int64_t work, int tpb = 256) {
   int64_t g = ceil_div(work, tpb);

@@ -558,7 +558,7 @@ int ls2_bias_dropout_residual_fwd(const void* x, const void* bias, const void* r
       constexpr bool D = decltype(drop)::value, G = decltype(genc)::value;
       if (vec) {
         Tiling t = tiling(rows, cols);
-        int grid = (int)std::min<int64_t>(t.passes, kNumSMs * 8);
+        int grid = resident_grid((const void*)bdr_fwd_vec<Tin, Tout, D, G>, t.threads, 0, t.passes);
         bdr_fwd_vec<Tin, Tout, D, G><<<grid, t.threads, 0, st>>>(
             (const Tin*)x, (const Tin*)bias, (const Tin*)res, (Tout*)y, keep_bits, rows, cols,
             t.cgs, t.rpp, seed, seed_ptr, thresh, sc);
@@ -627,7 +627,7 @@ int ls2_bias_relu_dropout_fwd(const void* x, const void* bias, void* y, uint8_t*
       constexpr bool D = decltype(drop)::value, G = decltype(genc)::value;
       if (vec) {
         Tiling t = tiling(rows, cols);
-        int grid = (int)std::min<int64_t>(t.passes, kNumSMs * 8);
+        int grid = resident_grid((const void*)brd_fwd_vec<Tin, Tout, D, G>, t.threads, 0, t.passes);
         brd_fwd_vec<Tin, Tout, D, G><<<grid, t.threads, 0, st>>>(
             (const Tin*)x, (const Tin*)bias, (Tout*)y, keep_bits, relu_bits, rows, cols, t.cgs,
             t.rpp, seed, seed_ptr, thresh, sc);

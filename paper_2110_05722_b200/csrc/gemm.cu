@@ -11,6 +11,8 @@
 #include <cublasLt.h>
 #include <cublas_v2.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -25,6 +27,7 @@ struct LtPlan {
   cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
   cublasLtMatmulAlgo_t algo;
   bool ok = false;
+  char tag[96] = {0};
 };
 
 using LtKey = std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
@@ -116,12 +119,110 @@ void ls2_blas_destroy(void* p) {
   delete b;
 }
 
+}  // extern "C"
+
+namespace ls2 {
+
+// Time the heuristic's candidates on the real operands once per key (outside
+// graph capture) and keep the fastest.  With beta != 0 the candidates write a
+// scratch D so C is left untouched.  Set LS2_GEMM_TUNE=0 to take the
+// heuristic's first choice.  Reduction schemes are restricted to fp32
+// workspace reductions (no fp16 split-K partial sums, no in-place atomics).
+static bool tuning_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("LS2_GEMM_TUNE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// Candidates are timed as a CUDA graph of kTuneReps back-to-back launches on a
+// private stream, so the number is device time (the step replays graphs too),
+// not the few microseconds of host overhead per cublasLtMatmul call.
+constexpr int kTuneReps = 8;
+
+static void lt_tune(Blas* bl, LtPlan* plan, const cublasLtMatmulHeuristicResult_t* res, int found,
+                    const void* A, const void* B, double beta, void* C, int64_t m, int64_t ldc,
+                    int tc, cudaStream_t st) {
+  plan->algo = res[0].algo;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (found <= 1 || !tuning_enabled() || cap != cudaStreamCaptureStatusNone) return;
+  cudaStreamSynchronize(st);
+  cudaStream_t ts;
+  if (cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); return; }
+  void* D = C;
+  void* tmp = nullptr;
+  if (beta != 0.0) {
+    const size_t bytes = (size_t)m * (size_t)ldc * esize(tc);
+    if (cudaMalloc(&tmp, bytes) != cudaSuccess) { cudaGetLastError(); cudaStreamDestroy(ts); return; }
+    D = tmp;
+  }
+  const float af = 1.f, bf = (float)beta;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f, first_ms = -1.f;
+  for (int i = 0; i < found; ++i) {
+    if (res[i].workspaceSize > bl->ws_bytes) continue;
+    auto run = [&]() {
+      return cublasLtMatmul(bl->lt, plan->op, &af, B, plan->a, A, plan->b, &bf, C, plan->c, D,
+                            plan->c, &res[i].algo, bl->ws, bl->ws_bytes, ts);
+    };
+    if (run() != CUBLAS_STATUS_SUCCESS || cudaStreamSynchronize(ts) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    bool ok = cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    for (int r = 0; ok && r < kTuneReps; ++r) ok = run() == CUBLAS_STATUS_SUCCESS;
+    if (cudaStreamEndCapture(ts, &g) != cudaSuccess) ok = false;
+    if (ok && cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) ok = false;
+    if (ok) {
+      cudaGraphLaunch(ge, ts);  // warm
+      cudaEventRecord(e0, ts);
+      cudaGraphLaunch(ge, ts);
+      cudaGraphLaunch(ge, ts);
+      cudaEventRecord(e1, ts);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 2 * kTuneReps;
+      if (i == 0) first_ms = ms;
+      if (ms < best) {
+        best = ms;
+        plan->algo = res[i].algo;
+      }
+    }
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  static const bool log = getenv("LS2_GEMM_LOG") != nullptr;
+  if (log) {
+    int tile = 0, splitk = 0;
+    size_t w = 0;
+    cublasLtMatmulAlgoConfigGetAttribute(&plan->algo, CUBLASLT_ALGO_CONFIG_TILE_ID, &tile, sizeof(tile), &w);
+    cublasLtMatmulAlgoConfigGetAttribute(&plan->algo, CUBLASLT_ALGO_CONFIG_SPLITK_NUM, &splitk, sizeof(splitk), &w);
+    fprintf(stderr, "[ls2 gemm] %s beta=%g candidates=%d best=%.2f us (heuristic #0 %.2f us) tile=%d splitk=%d\n",
+            plan->tag, beta, found, best * 1e3f, first_ms * 1e3f, tile, splitk);
+  }
+  cudaStreamSynchronize(ts);
+  if (tmp) cudaFree(tmp);
+  cudaStreamDestroy(ts);
+  cudaGetLastError();
+}
+
 /* C = alpha*op(A)@op(B) + beta*C (+ bias[n] broadcast over rows) on cuBLASLt, row-major.
  * Returns LS2_ERR_CUBLAS when no Lt algorithm supports the combination (caller falls back). */
-int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
-                const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
-                int64_t ldc, const void* bias, int tab, int tc, void* stream) {
-  Blas* bl = reinterpret_cast<Blas*>(hp);
+static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                     double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     double beta, void* C, int64_t ldc, const void* bias, int tab, int tc,
+                     cudaStream_t st) {
   if (!bl || !bl->lt) return fail(LS2_ERR_CUBLAS, "gemm_lt: no cublasLt handle");
   if (m <= 0 || n <= 0) return LS2_OK;
   if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_CUBLAS, "gemm_lt: f64 not routed to Lt");
@@ -143,7 +244,10 @@ int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_
         cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof(ep));
         cudaDataType_t bt = cuda_type(tc);
         cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt));
+        cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
       }
+      snprintf(plan->tag, sizeof(plan->tag), "ta=%d tb=%d m=%lld n=%lld k=%lld tab=%d tc=%d bias=%d",
+               trans_a, trans_b, (long long)m, (long long)n, (long long)k, tab, tc, bias != nullptr);
       const cudaDataType_t tAB = cuda_type(tab), tC = cuda_type(tc);
       cublasLtMatrixLayoutCreate(&plan->a, tAB, trans_b ? k : n, trans_b ? n : k, ldb);
       cublasLtMatrixLayoutCreate(&plan->b, tAB, trans_a ? m : k, trans_a ? k : m, lda);
@@ -157,13 +261,15 @@ int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_
       cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &a32, sizeof(a32));
       cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &a32, sizeof(a32));
       cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &a32, sizeof(a32));
-      cublasLtMatmulHeuristicResult_t res;
+      uint32_t red = CUBLASLT_REDUCTION_SCHEME_NONE | CUBLASLT_REDUCTION_SCHEME_COMPUTE_TYPE;
+      cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_REDUCTION_SCHEME_MASK, &red, sizeof(red));
+      cublasLtMatmulHeuristicResult_t res[32];
       int found = 0;
       cublasStatus_t s = cublasLtMatmulAlgoGetHeuristic(bl->lt, plan->op, plan->a, plan->b, plan->c,
-                                                        plan->c, pref, 1, &res, &found);
+                                                        plan->c, pref, 32, res, &found);
       cublasLtMatmulPreferenceDestroy(pref);
       plan->ok = (s == CUBLAS_STATUS_SUCCESS && found > 0);
-      if (plan->ok) plan->algo = res.algo;
+      if (plan->ok) lt_tune(bl, plan, res, found, A, B, beta, C, m, ldc, tc, st);
     }
   }
   if (!plan->ok) return fail(LS2_ERR_CUBLAS, "gemm_lt: no algorithm for this combination");
@@ -171,9 +277,19 @@ int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_
     cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
   const float af = (float)alpha, bf = (float)beta;
   cublasStatus_t s = cublasLtMatmul(bl->lt, plan->op, &af, B, plan->a, A, plan->b, &bf, C, plan->c,
-                                    C, plan->c, &plan->algo, bl->ws, bl->ws_bytes,
-                                    as_stream(stream));
+                                    C, plan->c, &plan->algo, bl->ws, bl->ws_bytes, st);
   return s == CUBLAS_STATUS_SUCCESS ? LS2_OK : blas_fail(s, "cublasLtMatmul");
+}
+
+}  // namespace ls2
+
+extern "C" {
+
+int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+                const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                int64_t ldc, const void* bias, int tab, int tc, void* stream) {
+  return lt_matmul(reinterpret_cast<Blas*>(hp), trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb,
+                   beta, C, ldc, bias, tab, tc, as_stream(stream));
 }
 
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2) { return 3 * n1 * n2 * (int64_t)sizeof(void*); }
@@ -199,6 +315,12 @@ int ls2_gemm(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k
   const cudaDataType_t tAB = cuda_type(tab), tC = cuda_type(tc);
   const int64_t total = n1 * n2;
   cublasStatus_t s;
+  if (total == 1 && !f64 && b->lt) {
+    // single GEMMs go through the tuned cuBLASLt plans; GemmEx only if Lt has no algorithm
+    if (lt_matmul(b, trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr,
+                  tab, tc, as_stream(stream)) == LS2_OK)
+      return LS2_OK;
+  }
   if (total == 1) {
     s = cublasGemmEx(b->h, opB, opA, (int)n, (int)m, (int)k, pa, B, tAB, (int)ldb, A, tAB,
                      (int)lda, pb, C, tC, (int)ldc, ct, CUBLAS_GEMM_DEFAULT);

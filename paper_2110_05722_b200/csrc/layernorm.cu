@@ -34,42 +34,42 @@ __device__ __forceinline__ void st_group(T* p, const C (&v)[8]) {
 }
 
 template <typename Tin, typename Tout, typename Tstat, int ITERS>
-__global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_warp(
+__global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_warp(
     const Tin* __restrict__ x, const Tin* __restrict__ w, const Tin* __restrict__ b,
     Tout* __restrict__ y, Tstat* __restrict__ mu, Tstat* __restrict__ sigma,
     int* __restrict__ degenerate, int64_t rows, int64_t cols, double eps) {
   using C = typename CompOf<Tin>::type;
   const int lane = threadIdx.x & 31;
   const int64_t cgs = cols / 8;
-  C wv[ITERS][8], bv[ITERS][8];
-#pragma unroll
-  for (int it = 0; it < ITERS; ++it) {
-    const int64_t g = lane + 32 * it;
-    if (g < cgs) {
-      ld_group(w + g * 8, wv[it]);
-      ld_group(b + g * 8, bv[it]);
-    }
+  // affine parameters staged in shared memory (registers decide occupancy here)
+  extern __shared__ __align__(16) unsigned char ln_par[];
+  Pack8<Tin>* sw = reinterpret_cast<Pack8<Tin>*>(ln_par);
+  Pack8<Tin>* sb = sw + cgs;
+  for (int64_t g = threadIdx.x; g < cgs; g += blockDim.x) {
+    sw[g] = ld8(w + g * 8);
+    sb[g] = ld8(b + g * 8);
   }
+  __syncthreads();
   const double inv_m = 1.0 / (double)cols;
   for (int64_t r = (int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5); r < rows;
        r += (int64_t)gridDim.x * kLnWarps) {
     const Tin* xr = x + r * cols;
-    C v[ITERS][8];
+    Pack8<Tin> v[ITERS];   // row kept packed; (x - pivot) is recomputed on use
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
-      if (g < cgs) ld_group(xr + g * 8, v[it]);
+      if (g < cgs) v[it] = ld8(xr + g * 8);
     }
-    const C pivot = __shfl_sync(0xffffffffu, v[0][0], 0);
+    const C pivot = __shfl_sync(0xffffffffu, cvt<C>(v[0].v[0]), 0);
     C s1 = 0, s2 = 0;
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       if (lane + 32 * it < cgs) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          v[it][e] -= pivot;
-          s1 += v[it][e];
-          s2 += v[it][e] * v[it][e];
+          const C d = cvt<C>(v[it].v[e]) - pivot;
+          s1 += d;
+          s2 += d * d;
         }
       }
     }
@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_warp(
       const int64_t g = lane + 32 * it;
       if (g < cgs) {
         C o[8];
+        const Pack8<Tin> wq = sw[g], bq = sb[g];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (v[it][e] - msh) * rs * wv[it][e] + bv[it][e];
+        for (int e = 0; e < 8; ++e)
+          o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
         st_group(yr + g * 8, o);
       }
     }
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_warp(
 // The LayerNorm consumes the stored (rounded) yres, so results equal the
 // unfused pair exactly; one launch and one pass instead of two.
 template <typename Tin, typename Tout, typename Tstat, int ITERS, bool DROP>
-__global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_bdr_warp(
+__global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
     const Tin* __restrict__ x, const Tin* __restrict__ bias, const Tin* __restrict__ res,
     Tout* __restrict__ yres, uint8_t* __restrict__ bits, const Tin* __restrict__ w,
     const Tin* __restrict__ b, Tout* __restrict__ u, Tstat* __restrict__ mu,
@@ -116,20 +118,20 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_bdr_warp(
   const int lane = threadIdx.x & 31;
   const int64_t cgs = cols / 8;
   if (seed_ptr) seed = *seed_ptr;
-  C wv[ITERS][8], bv[ITERS][8], cb[ITERS][8];
-#pragma unroll
-  for (int it = 0; it < ITERS; ++it) {
-    const int64_t g = lane + 32 * it;
-    if (g < cgs) {
-      ld_group(w + g * 8, wv[it]);
-      ld_group(b + g * 8, bv[it]);
-      ld_group(bias + g * 8, cb[it]);
-    }
+  extern __shared__ __align__(16) unsigned char ln_par[];
+  Pack8<Tin>* sw = reinterpret_cast<Pack8<Tin>*>(ln_par);
+  Pack8<Tin>* sb = sw + cgs;
+  Pack8<Tin>* sc = sb + cgs;
+  for (int64_t g = threadIdx.x; g < cgs; g += blockDim.x) {
+    sw[g] = ld8(w + g * 8);
+    sb[g] = ld8(b + g * 8);
+    sc[g] = ld8(bias + g * 8);
   }
+  __syncthreads();
   const double inv_m = 1.0 / (double)cols;
   for (int64_t r = (int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5); r < rows;
        r += (int64_t)gridDim.x * kLnWarps) {
-    C v[ITERS][8];
+    Pack8<Tout> v[ITERS];   // the stored yres, packed; LN statistics read it back
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
@@ -143,26 +145,27 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_bdr_warp(
           bits[r * cgs + g] = (uint8_t)kb;
         }
         Pack8<Tout> q;
+        const Pack8<Tin> cq = sc[g];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          C a = add_rn(xv[e], cb[it][e]);
+          C a = add_rn(xv[e], cvt<C>(cq.v[e]));
           if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), dscale);
           q.v[e] = cvt<Tout>(add_rn(a, rv[e]));
-          v[it][e] = cvt<C>(q.v[e]);
         }
+        v[it] = q;
         st8(yres + r * cols + g * 8, q);
       }
     }
-    const C pivot = __shfl_sync(0xffffffffu, v[0][0], 0);
+    const C pivot = __shfl_sync(0xffffffffu, cvt<C>(v[0].v[0]), 0);
     C s1 = 0, s2 = 0;
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       if (lane + 32 * it < cgs) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          v[it][e] -= pivot;
-          s1 += v[it][e];
-          s2 += v[it][e] * v[it][e];
+          const C d = cvt<C>(v[it].v[e]) - pivot;
+          s1 += d;
+          s2 += d * d;
         }
       }
     }
@@ -183,8 +186,10 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_fwd_bdr_warp(
       const int64_t g = lane + 32 * it;
       if (g < cgs) {
         C o[8];
+        const Pack8<Tin> wq = sw[g], bq = sb[g];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (v[it][e] - msh) * rs * wv[it][e] + bv[it][e];
+        for (int e = 0; e < 8; ++e)
+          o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
         st_group(u + r * cols + g * 8, o);
       }
     }
@@ -362,6 +367,138 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
   }
 }
 
+// One-wave variant (fp32 compute): a CTA of RW warps takes RW rows per round,
+// one row per warp held in registers, so every row of a 4096-token batch is in
+// flight at once (maximum memory-level parallelism, no per-warp row loop).  The
+// warps' per-element contributions (dy*xhat, dy[, dproj]) are staged in shared
+// memory as stg[RW][NP][cols] and column-reduced in warp order by all threads
+// (fixed order -> deterministic); each thread carries up to kLnPairs column
+// sums across rounds and leaves partial[block][NP][cols] for the finish.
+constexpr int kLnStageMaxWarps = 28;   // 896 threads -> up to 72 registers per thread
+constexpr int kLnStageWideWarps = 15;  // rows of 513..1024 columns: 480 threads, 128 registers
+
+inline int ln_stage_rw(int64_t rows, int64_t cols) {
+  // stg[rw][3][cols] + acc[3][cols] floats within 200 KB
+  int64_t rw = (200 * 1024) / (3 * cols * 4) - 1;
+  rw = rw < 1 ? 1 : (rw > kLnStageMaxWarps ? kLnStageMaxWarps : rw);
+  if (cols > 512 && rw > kLnStageWideWarps) rw = kLnStageWideWarps;  // ITERS == 4 kernels
+  const int64_t need = ceil_div(rows, (int64_t)kLnMaxBlocks);
+  if (need < rw) rw = need < 1 ? 1 : need;
+  return (int)rw;
+}
+
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP>
+__global__ void __launch_bounds__((ITERS >= 4 ? kLnStageWideWarps : kLnStageMaxWarps) * 32, 1)
+ln_bwd_stage(
+    const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
+    const Tstat* __restrict__ mu, const Tstat* __restrict__ sigma, const Tin* __restrict__ dres,
+    Tout* __restrict__ dx, const uint8_t* __restrict__ bits, Tout* __restrict__ dproj,
+    float dscale, double* __restrict__ partial, int64_t rows, int64_t cols) {
+  constexpr int NP = BDR ? 3 : 2;
+  extern __shared__ __align__(16) float stg[];   // [rw][NP][cols], then acc[NP][cols]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rw = blockDim.x >> 5;
+  const int64_t cgs = cols / 8;
+  const int npairs = NP * (int)cols;
+  float* accs = stg + (int64_t)rw * npairs;
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x) accs[p] = 0.f;
+  Pack8<Tin> wv[ITERS];
+#pragma unroll
+  for (int it = 0; it < ITERS; ++it) {
+    const int64_t g = lane + 32 * it;
+    if (g < cgs) wv[it] = ld8(w + g * 8);
+  }
+  const float inv_m = (float)(1.0 / (double)cols);
+  for (int64_t base = (int64_t)blockIdx.x * rw; base < rows; base += (int64_t)gridDim.x * rw) {
+    const int64_t r = base + wid;
+    float* my = stg + (int64_t)wid * npairs;
+    if (r < rows) {
+      Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const int64_t g = lane + 32 * it;
+        if (g < cgs) {
+          cd[it] = ld8_stream(dy + r * cols + g * 8);
+          cx[it] = ld8_stream(x + r * cols + g * 8);
+          if (RES) cr[it] = ld8_stream(dres + r * cols + g * 8);
+        }
+      }
+      const float m_r = (float)mu[r];
+      const float rs = (float)(1.0 / (double)sigma[r]);
+      float r1 = 0.f, r3 = 0.f;
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const int64_t g = lane + 32 * it;
+        if (g < cgs) {
+          float c0[8], c1[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float dv = cvt<float>(cd[it].v[e]);
+            const float xh = (cvt<float>(cx[it].v[e]) - m_r) * rs;
+            const float gg = cvt<float>(wv[it].v[e]) * dv;
+            r1 += gg;
+            r3 += gg * xh;
+            c0[e] = dv * xh;
+            c1[e] = dv;
+          }
+          float4* d0 = reinterpret_cast<float4*>(my + g * 8);
+          d0[0] = make_float4(c0[0], c0[1], c0[2], c0[3]);
+          d0[1] = make_float4(c0[4], c0[5], c0[6], c0[7]);
+          float4* d1 = reinterpret_cast<float4*>(my + cols + g * 8);
+          d1[0] = make_float4(c1[0], c1[1], c1[2], c1[3]);
+          d1[1] = make_float4(c1[4], c1[5], c1[6], c1[7]);
+        }
+      }
+      r1 = warp_sum(r1) * inv_m;
+      r3 = warp_sum(r3) * inv_m;
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        const int64_t g = lane + 32 * it;
+        if (g < cgs) {
+          Pack8<Tout> o;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float dv = cvt<float>(cd[it].v[e]);
+            const float xh = (cvt<float>(cx[it].v[e]) - m_r) * rs;
+            const float gg = cvt<float>(wv[it].v[e]) * dv;
+            float v = (gg - r1 - xh * r3) * rs;
+            if (RES) v += cvt<float>(cr[it].v[e]);
+            o.v[e] = cvt<Tout>(v);
+          }
+          st8(dx + r * cols + g * 8, o);
+          if (BDR) {
+            const uint32_t kb = DROP ? bits[r * cgs + g] : 0xFF;
+            Pack8<Tout> pj;
+            float c2[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float v = cvt<float>(o.v[e]);
+              if (DROP) v = mul_rn(mul_rn(v, (float)((kb >> e) & 1)), dscale);
+              c2[e] = v;
+              pj.v[e] = cvt<Tout>(v);
+            }
+            st8(dproj + r * cols + g * 8, pj);
+            float4* d2 = reinterpret_cast<float4*>(my + 2 * cols + g * 8);
+            d2[0] = make_float4(c2[0], c2[1], c2[2], c2[3]);
+            d2[1] = make_float4(c2[4], c2[5], c2[6], c2[7]);
+          }
+        }
+      }
+    } else {
+      for (int c = lane; c < npairs; c += 32) my[c] = 0.f;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      float s = 0.f;
+      for (int q = 0; q < rw; ++q) s += stg[(int64_t)q * npairs + p];
+      accs[p] += s;
+    }
+    __syncthreads();
+  }
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x)
+    partial[(int64_t)blockIdx.x * npairs + p] = (double)accs[p];
+}
+
 // generic backward: CTA per row for dx; param partials by a column-parallel kernel
 template <typename Tin, typename Tout, typename Tstat>
 __global__ void ln_bwd_block(const Tin* __restrict__ dy, const Tin* __restrict__ x,
@@ -452,6 +589,11 @@ __global__ void __launch_bounds__(1024) ln_param_finish(const double* __restrict
   }
 }
 
+inline int ln_generic_blocks(int64_t rows) {
+  const int64_t g = ceil_div(rows, (int64_t)16);
+  return (int)(g < 1 ? 1 : (g > kLnMaxBlocks ? kLnMaxBlocks : g));
+}
+
 inline bool ln_vec_ok(int64_t cols, std::initializer_list<const void*> ptrs) {
   if (cols % 8 != 0 || cols > 1024 || cols < 8) return false;
   for (const void* p : ptrs)
@@ -461,9 +603,40 @@ inline bool ln_vec_ok(int64_t cols, std::initializer_list<const void*> ptrs) {
 
 inline int ln_iters(int64_t cols) { return cols <= 256 ? 1 : cols <= 512 ? 2 : 4; }
 
-inline int ln_bwd_blocks(int64_t rows) {
-  int64_t g = ceil_div(rows, kLnBwdWarps * 2);
+// partial-row count of the vectorised backward (both the fp32 one-wave kernel
+// and the f64 warp kernel use this grid, so the deferred-partial layout depends
+// on (rows, cols) only)
+inline int ln_bwd_blocks(int64_t rows, int64_t cols) {
+  const int64_t g = ceil_div(rows, (int64_t)ln_stage_rw(rows, cols));
   return (int)(g < 1 ? 1 : (g > kLnMaxBlocks ? kLnMaxBlocks : g));
+}
+
+// launch the fp32 one-wave kernel (C == float) or the f64 warp kernel
+template <typename Tin, typename Tout, typename Tstat, int I, bool R, bool B, bool D>
+int ln_bwd_launch(const void* dy, const void* x, const void* w, const void* mu, const void* sigma,
+                  const void* dres, void* dx, const uint8_t* bits, void* dproj, double dscale,
+                  void* ws, int64_t rows, int64_t cols, cudaStream_t st) {
+  using C = typename CompOf<Tin>::type;
+  const int nblk = ln_bwd_blocks(rows, cols);
+  if constexpr (std::is_same<C, double>::value) {
+    ln_bwd_warp<Tin, Tout, Tstat, I, R, B, D><<<nblk, kLnBwdWarps * 32, 0, st>>>(
+        (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
+        (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (C)dscale, (double*)ws, rows, cols);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    constexpr int NP = B ? 3 : 2;
+    const int rw = ln_stage_rw(rows, cols);
+    const size_t smem = (size_t)(rw + 1) * NP * cols * sizeof(float);
+    ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D><<<nblk, rw * 32, smem, st>>>(
+        (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
+        (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows, cols);
+  }
+  return check_launch(B ? "layernorm_bwd_bdr" : "layernorm_bwd");
 }
 
 #define LS2_DISPATCH_STAT(TS, ...)                                                    \
@@ -489,11 +662,17 @@ int ls2_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void
   return LS2_DISPATCH_IO(tin, tout, "layernorm_fwd", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
       if (vec) {
-        const int grid = (int)std::min<int64_t>(ceil_div(rows, kLnWarps), kNumSMs * 16);
-        switch (ln_iters(cols)) {
-          case 1: ln_fwd_warp<Tin, Tout, Tstat, 1><<<grid, kLnWarps * 32, 0, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
-          case 2: ln_fwd_warp<Tin, Tout, Tstat, 2><<<grid, kLnWarps * 32, 0, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
-          default: ln_fwd_warp<Tin, Tout, Tstat, 4><<<grid, kLnWarps * 32, 0, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
+        const int64_t want = ceil_div(rows, kLnWarps);
+        const int it_ = ln_iters(cols);
+        const void* fn = it_ == 1 ? (const void*)ln_fwd_warp<Tin, Tout, Tstat, 1>
+                       : it_ == 2 ? (const void*)ln_fwd_warp<Tin, Tout, Tstat, 2>
+                                  : (const void*)ln_fwd_warp<Tin, Tout, Tstat, 4>;
+        const size_t psm = 2 * (size_t)cols * sizeof(Tin);
+        const int grid = resident_grid(fn, kLnWarps * 32, psm, want);
+        switch (it_) {
+          case 1: ln_fwd_warp<Tin, Tout, Tstat, 1><<<grid, kLnWarps * 32, psm, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
+          case 2: ln_fwd_warp<Tin, Tout, Tstat, 2><<<grid, kLnWarps * 32, psm, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
+          default: ln_fwd_warp<Tin, Tout, Tstat, 4><<<grid, kLnWarps * 32, psm, st>>>((const Tin*)x, (const Tin*)w, (const Tin*)b, (Tout*)y, (Tstat*)mu, (Tstat*)sigma, degenerate, rows, cols, eps); break;
         }
       } else {
         const int grid = (int)std::min<int64_t>(rows, kNumSMs * 16);
@@ -505,7 +684,7 @@ int ls2_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void
 }
 
 int ls2_layernorm_bwd_nblk(int64_t rows, int64_t cols) {
-  return (cols % 8 == 0 && cols <= 1024 && cols >= 8) ? ln_bwd_blocks(rows) : 0;
+  return (cols % 8 == 0 && cols <= 1024 && cols >= 8) ? ln_bwd_blocks(rows, cols) : 0;
 }
 
 int64_t ls2_layernorm_bwd_ws_bytes(int64_t rows, int64_t cols) {
@@ -525,11 +704,13 @@ int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void
   return LS2_DISPATCH_IO(tin, tout, "bdr_layernorm_fwd", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
       using C = typename CompOf<Tin>::type;
-      const int grid = (int)std::min<int64_t>(ceil_div(rows, kLnWarps), kNumSMs * 16);
       auto go = [&](auto iters, auto drop) {
         constexpr int I = decltype(iters)::value;
         constexpr bool D = decltype(drop)::value;
-        ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D><<<grid, kLnWarps * 32, 0, st>>>(
+        const size_t psm = 3 * (size_t)cols * sizeof(Tin);
+        const int grid = resident_grid((const void*)ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D>,
+                                       kLnWarps * 32, psm, ceil_div(rows, kLnWarps));
+        ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D><<<grid, kLnWarps * 32, psm, st>>>(
             (const Tin*)x, (const Tin*)bias, (const Tin*)res, (Tout*)yres, keep_bits,
             (const Tin*)w, (const Tin*)b, (Tout*)u, (Tstat*)mu, (Tstat*)sigma, rows, cols, eps,
             seed, seed_ptr, thresh, (C)dscale);
@@ -556,18 +737,15 @@ int ls2_layernorm_bwd_bdr(const void* dy, const void* x, const void* w, const vo
   if (!ln_vec_ok(cols, {dy, x, w, dres, dx, dproj}))
     return fail(LS2_ERR_SHAPE, "layernorm_bwd_bdr: needs cols % 8 == 0, <= 1024, aligned");
   cudaStream_t st = as_stream(stream);
-  const int nblk = ln_bwd_blocks(rows);
+  const int nblk = ln_bwd_blocks(rows, cols);
   int rc = LS2_DISPATCH_IO(tin, tout, "layernorm_bwd_bdr", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
-      using C = typename CompOf<Tin>::type;
       auto go = [&](auto iters, auto res, auto drop) {
         constexpr int I = decltype(iters)::value;
         constexpr bool R = decltype(res)::value, D = decltype(drop)::value;
-        ln_bwd_warp<Tin, Tout, Tstat, I, R, true, D><<<nblk, kLnBwdWarps * 32, 0, st>>>(
-            (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
-            (const Tin*)dres, (Tout*)dx, keep_bits, (Tout*)dproj, (C)dscale, (double*)ws, rows,
-            cols);
-        return check_launch("layernorm_bwd_bdr");
+        return ln_bwd_launch<Tin, Tout, Tstat, I, R, true, D>(dy, x, w, mu, sigma, dres, dx,
+                                                              keep_bits, dproj, dscale, ws, rows,
+                                                              cols, st);
       };
       using I1 = std::integral_constant<int, 1>;
       using I2 = std::integral_constant<int, 2>;
@@ -598,18 +776,15 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
   cudaStream_t st = as_stream(stream);
   if (rows <= 0) return LS2_OK;
   const bool vec = ln_vec_ok(cols, {dy, x, w, dres, dx});
-  const int nblk = ln_bwd_blocks(rows);
+  const int nblk = vec ? ln_bwd_blocks(rows, cols) : ln_generic_blocks(rows);
   int rc = LS2_DISPATCH_IO(tin, tout, "layernorm_bwd", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
       if (vec) {
-        using C = typename CompOf<Tin>::type;
         auto go = [&](auto iters, auto res) {
           constexpr int I = decltype(iters)::value;
           constexpr bool R = decltype(res)::value;
-          ln_bwd_warp<Tin, Tout, Tstat, I, R, false, false><<<nblk, kLnBwdWarps * 32, 0, st>>>(
-              (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
-              (const Tin*)dres, (Tout*)dx, nullptr, nullptr, (C)1, (double*)ws, rows, cols);
-          return check_launch("layernorm_bwd");
+          return ln_bwd_launch<Tin, Tout, Tstat, I, R, false, false>(
+              dy, x, w, mu, sigma, dres, dx, nullptr, nullptr, 1.0, ws, rows, cols, st);
         };
         using I1 = std::integral_constant<int, 1>;
         using I2 = std::integral_constant<int, 2>;
