@@ -244,7 +244,10 @@ def run_ours(args):
     dp.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof_range = os.environ.get("LS2_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
     with ClockSampler(torch.cuda.current_device()) as clk:
+        if prof_range:
+            torch.cuda.profiler.start()
         e0.record(st)
         if dev_graph is not None:
             for _ in range(args.steps):
@@ -254,6 +257,8 @@ def run_ours(args):
                 eng.device_step(key, args.warmup + s)
         e1.record(st)
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.profiler.stop()
     dp.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     ms = dp.max_scalar(ms, device=eng.device)

@@ -1,0 +1,78 @@
+"""Per-kernel roofline table for the Transformer-base step (T-base, 4096 tokens).
+
+Joins the in-situ kernel times of tools/kineto_step.py (JSON) with each hand-
+written kernel's ALGORITHMIC bytes per launch (the bytes the
+operation must move with fp16 storage, 1-bit masks and fp32 LN statistics), and
+reports achieved GB/s and the fraction of the measured HBM peak.
+
+    python tools/roofline_table.py gpurun_out/kineto.json [--peak 6449.4] [--md out.md]
+"""
+
+import argparse
+import json
+import re
+
+N, D, F, V, B, L, H = 4096, 512, 2048, 32000, 64, 64, 8
+P = 60_655_616          # Transformer-base parameters (learned positions, max_len 256)
+BHL2 = B * H * L * L
+
+# (regex on the kernel name, description, algorithmic bytes per launch)
+ALGO = [
+    (r"bdr_fwd_vec", "bias+dropout+residual fwd", 3 * N * D * 2 + N * D // 8),
+    (r"bdr_bwd_vec", "bias+dropout+residual bwd (+dbias partials)", 2 * N * D * 2 + N * D // 8),
+    (r"brd_fwd_vec", "bias+ReLU+dropout fwd", 2 * N * F * 2 + 2 * N * F // 8),
+    (r"brd_bwd_vec", "bias+ReLU+dropout bwd (+dbias partials)", 2 * N * F * 2 + 2 * N * F // 8),
+    (r"ln_fwd_bdr_warp", "bias+dropout+residual -> LayerNorm fwd", 4 * N * D * 2 + N * D // 8 + 8 * N),
+    (r"ln_fwd_warp", "LayerNorm fwd", 2 * N * D * 2 + 8 * N),
+    (r"ln_bwd_stage<[^>]*, true, true, true>", "LayerNorm bwd + residual + bdr bwd",
+     5 * N * D * 2 + N * D // 8 + 8 * N),
+    (r"ln_bwd_stage<[^>]*, true, false, false>", "LayerNorm bwd + residual", 4 * N * D * 2 + 8 * N),
+    (r"ln_bwd_stage<[^>]*, false, false, false>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
+    (r"attn_fwd_kernel", "fused attention fwd (QK^T, mask, softmax, PV)", 4 * N * D * 2 + BHL2 * 2),
+    (r"attn_bwd_kernel", "fused attention bwd", 7 * N * D * 2 + BHL2 * 2),
+    (r"criterion_tma_kernel|criterion_kernel", "fused LS cross-entropy fwd+bwd (in place)",
+     2 * N * V * 2),
+    (r"adam_kernel", "workspace Adam (22 B/param)", 22 * P),
+    (r"scale_narrow_kernel", "fp32 grad accumulators -> scaled fp16 workspace", 6 * P),
+    (r"emb_fwd_vec", "embedding fwd (gather, scale, pos, dropout)", 8 * N + 3 * N * D * 2 + N * D // 8),
+    (r"emb_bwd_scatter", "embedding bwd scatter (fp32 RMW)", N * D * 2 + 2 * N * D * 4 + N * D // 8),
+    (r"emb_bwd_pos", "positional-table grad", N * D * 2 + N * D // 8),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("json")
+    ap.add_argument("--peak", type=float, default=6449.4)
+    ap.add_argument("--md", default=None)
+    a = ap.parse_args()
+    d = json.load(open(a.json))
+    lines = ["| kernel | what | launches/step | µs/launch (in situ) | algorithmic MB/launch | "
+             "achieved GB/s | frac of HBM peak |", "|---|---|---|---|---|---|---|"]
+    tot_us = tot_bytes = 0.0
+    for k in d["kernels"]:
+        name = k["name"]
+        for pat, what, nbytes in ALGO:
+            if re.search(pat, name):
+                n = max(k["launches_per_step"], 1)
+                us = k["us_per_step"] / n
+                gbs = nbytes / (us * 1e-6) / 1e9
+                short = re.sub(r"\(.*", "", name).replace("void ", "").replace("ls2::", "")
+                lines.append(f"| `{short[:60]}` | {what} | {n} | {us:.2f} | {nbytes / 1e6:.2f} | "
+                             f"{gbs:.0f} | {gbs / a.peak:.2f} |")
+                tot_us += k["us_per_step"]
+                tot_bytes += nbytes * n
+                break
+    lines.append(f"| **all of the above** | | | {tot_us:.0f} µs/step | {tot_bytes / 1e6:.0f} MB/step | "
+                 f"{tot_bytes / (tot_us * 1e-6) / 1e9:.0f} | "
+                 f"{tot_bytes / (tot_us * 1e-6) / 1e9 / a.peak:.2f} |")
+    out = "\n".join(lines)
+    print(f"step {d['step_us']:.0f} µs, kernel busy {d['busy_us']:.0f} µs\n")
+    print(out)
+    if a.md:
+        with open(a.md, "w") as fh:
+            fh.write(out + "\n")
+
+
+if __name__ == "__main__":
+    main()
