@@ -164,6 +164,28 @@ class DeviceContext:
         self._keep: list[torch.Tensor] = []
         self.ptr_cache: dict = {}        # pointer arrays of pointer-array GEMM batches
         self.lt_unsupported: set = set()  # cuBLASLt keys that fell back
+        # side lane for off-critical-path work (weight-gradient GEMMs): lowest
+        # priority, its own cuBLAS handle + workspace so the two streams never
+        # share a GEMM workspace
+        # (torch clamps out-of-range priorities: +100 -> lowest, -100 -> highest)
+        self.side_stream = torch.cuda.Stream(device=device, priority=100)
+        self.compute_stream = torch.cuda.Stream(device=device, priority=-100)
+        self._blas_side = None
+
+    @property
+    def blas_side(self):
+        if self._blas_side is None:
+            with torch.cuda.device(self.device):
+                self._blas_side = _lib.ls2_blas_create()
+            if not self._blas_side:
+                raise DeviceError("cuBLAS init failed: " + _lib.ls2_last_error().decode())
+        return self._blas_side
+
+    def blas_handle(self):
+        """cuBLAS plan/workspace handle for the current stream."""
+        if torch.cuda.current_stream(self.device) == self.side_stream:
+            return self.blas_side
+        return self.blas
 
     def scratch(self, name: str, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)

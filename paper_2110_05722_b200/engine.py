@@ -13,6 +13,7 @@ on the device, so a skipped step needs no extra host round trip.
 from __future__ import annotations
 
 import gc
+import os
 import time
 from dataclasses import dataclass
 
@@ -132,6 +133,10 @@ class TrainingEngine:
         self._launches: dict = {}
         self._finish_tables: dict = {}
         self.use_graphs = bool(t.cuda_graphs)
+        # weight-gradient GEMMs on a low-priority side lane (LS2_WGRAD_LANE=1).  Off
+        # by default: measured 1% slower at T-base, because the one-wave fused
+        # kernels cannot co-reside with a concurrent GEMM's CTAs
+        self.use_lane = os.environ.get("LS2_WGRAD_LANE", "0") == "1"
         self.last_out3 = None
 
     # -- arena setup (F/engine.py:89-103) ----------------------------------------------
@@ -144,7 +149,7 @@ class TrainingEngine:
 
     def _record_shape(self, batch: Batch, compute_grads: bool):
         rec = RecordingArena(self.device)
-        sink = _ViewSink(self.gviews, defer=True) if compute_grads else None
+        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane) if compute_grads else None
         self.model.forward_backward(self.pviews, batch,
                                     p_drop=self.cfg.train.p_drop if compute_grads else 0.0,
                                     alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
@@ -188,7 +193,7 @@ class TrainingEngine:
         if upload:
             io.upload()
         self.arena.begin(key)
-        sink = _ViewSink(self.gviews, defer=True)
+        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
             arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
@@ -205,7 +210,7 @@ class TrainingEngine:
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
         with _no_gc():
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=_lib.context().compute_stream):
                 out3, sink = self._fwd_bwd(io, key, 0, upload=False)
                 self._update(out3, sink, host_copy=False)
         self._launches[key] = _lib.launches() - n0
@@ -295,7 +300,7 @@ class TrainingEngine:
             return  # collectives stay eager under DP
         g = torch.cuda.CUDAGraph()
         with _no_gc():
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=_lib.context().compute_stream):
                 out3, sink = self._fwd_bwd(io, key, step)
                 self._update(out3, sink)
         self._graphs[key] = g

@@ -687,7 +687,7 @@ def gemm(a, b, trans_a: bool = False, trans_b: bool = False, accumulate_into=Non
             ctx.ptr_cache[key] = scratch
         else:
             ready = 1
-    _lib.call("ls2_gemm", ctx.blas, int(la[0]), int(lb[0]), m, n, k, float(alpha),
+    _lib.call("ls2_gemm", ctx.blas_handle(), int(la[0]), int(lb[0]), m, n, k, float(alpha),
               av.data_ptr(), la[1], s1[0], s2[0], bv.data_ptr(), lb[1], s1[1], s2[1],
               float(beta_v), Cw.data_ptr(), lc[1], s1[2], s2[2], n1, n2,
               _lib.dtype_code(av), _lib.dtype_code(tc), _lib.ptr(scratch), ready,

@@ -221,7 +221,7 @@ def _linear(x2d, w, b, out2d):
         key = (m, n, k, dt, bb is not None)
         if key not in ctx.lt_unsupported:
             try:
-                _lib.call("ls2_gemm_lt", ctx.blas, 0, 1, m, n, k, 1.0, x2d.data_ptr(), k,
+                _lib.call("ls2_gemm_lt", ctx.blas_handle(), 0, 1, m, n, k, 1.0, x2d.data_ptr(), k,
                           wt.data_ptr(), k, 0.0, out2d.data_ptr(), n, _lib.ptr(bb),
                           _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.stream_handle())
                 return out2d
@@ -342,14 +342,16 @@ class _ViewSink(GradSink):
     """Writes into preallocated views of the fp32 gradient workspace; the first
     producer of a name overwrites (beta=0), later producers accumulate."""
 
-    def __init__(self, store: dict, defer: bool = False):
+    def __init__(self, store: dict, defer: bool = False, lane: bool = False):
         super().__init__(store)
+        self.use_lane = bool(lane)
         self.written: set = set()
         # deferred column sums: the producer leaves per-block partials in an arena
         # buffer and the engine finishes them all inside the fp16 narrow pass
         self.defer_enabled = defer
         self.deferred: list = []          # (name, buf, nblk, stride, k, cols)
         self.arena = None
+        self.lane = None                  # _Lane for weight-gradient GEMMs (engine path)
 
     def add(self, name: str, value):
         if name in self.written:
@@ -383,6 +385,69 @@ class _ViewSink(GradSink):
         return out
 
 
+class _Lane:
+    """Side-stream lane for weight-gradient GEMMs (off the critical path).
+
+    dW = dy^T x is only consumed by the optimizer, so it runs on a low-priority
+    stream with its own cuBLAS workspace while the main stream continues with
+    the data-gradient chain.  Arena buffers such a GEMM reads are held: their
+    frees are deferred to the next join(), where the main stream first waits for
+    the lane.  The same alloc/free sequence happens in the arena's dry run, so
+    the planned lifetimes include the hold."""
+
+    def __init__(self, arena):
+        ctx = _lib.context()
+        self.main = torch.cuda.current_stream()
+        self.side = ctx.side_stream
+        self.arena = arena
+        self.held: set = set()
+        self.deferred: list = []
+        self.pending = False
+
+    def run(self, fn, *reads):
+        ev = torch.cuda.Event()
+        ev.record(self.main)
+        self.side.wait_event(ev)
+        with torch.cuda.stream(self.side):
+            fn()
+        for t in reads:
+            self.held.add(t.data_ptr())
+        self.pending = True
+
+    def free(self, t):
+        if t.data_ptr() in self.held:
+            self.deferred.append(t)
+        else:
+            self.arena.free(t)
+
+    def join(self):
+        if self.pending:
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+            self.main.wait_event(ev)
+            self.pending = False
+        self.held.clear()
+        for t in self.deferred:
+            self.arena.free(t)
+        self.deferred.clear()
+
+
+class _LaneArena:
+    """Arena facade whose frees respect the lane's holds."""
+
+    def __init__(self, arena, lane: _Lane):
+        self._arena, self._lane = arena, lane
+
+    def alloc(self, shape, dtype):
+        return self._arena.alloc(shape, dtype)
+
+    def free(self, t):
+        self._lane.free(t)
+
+    def __getattr__(self, name):
+        return getattr(self._arena, name)
+
+
 def _defer(sink, names, nblk, np_, cols):
     fn = getattr(sink, "defer_buffer", None)
     return fn(names, nblk, np_, cols) if fn is not None else None
@@ -399,13 +464,20 @@ def _colsum_nblk(rows, cols, t) -> int:
 
 
 def _wgrad(sink, name, dy2d, x2d):
-    """dW = dy^T x straight into the sink (cuBLAS, fp32 output)."""
+    """dW = dy^T x straight into the sink (cuBLAS, fp32 output); on the sink's
+    side lane when it has one."""
     tgt = sink.target(name)
     if tgt is None:
         sink.add(name, K.gemm(dy2d, x2d, trans_a=True))
+        return
+    v, beta = tgt
+    go = lambda: K.gemm(dy2d, x2d, trans_a=True, out=v.view(dy2d.shape[1], x2d.shape[1]),  # noqa: E731
+                        beta=float(beta))
+    lane = getattr(sink, "lane", None)
+    if lane is not None:
+        lane.run(go, dy2d, x2d)
     else:
-        v, beta = tgt
-        K.gemm(dy2d, x2d, trans_a=True, out=v.view(dy2d.shape[1], x2d.shape[1]), beta=float(beta))
+        go()
 
 
 def _colsum_grad(sink, name, x2d):
@@ -1194,6 +1266,15 @@ class Transformer:
             return out
 
         # --- backward: output projection ---
+        # weight-gradient GEMMs go to the side lane (engine path); frees of the
+        # buffers they read are held until the lane joins after each layer
+        lane = None
+        main_arena = arena
+        if getattr(sink, "use_lane", False) and dt != torch.float64:
+            lane = _Lane(arena)
+            sink.lane = lane
+            arena = _LaneArena(arena, lane)
+        join = lane.join if lane is not None else (lambda: None)
         dlogits = logits
         dec_out = stash.pop("dec_out")
         ddec = arena.alloc((b, lt, d), dt)
@@ -1217,6 +1298,7 @@ class Transformer:
             dg, dks[i], dvs[i] = decoder_layer_backward(
                 dg, dec_w[i], kv_pairs[i], stash, sink, n_heads=n, p_drop=p_drop, arena=arena,
                 prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest)
+            join()
             emit(("dec_layer_backward_done", i))
         keep_tgt = stash.pop("tgt_keep")
         self._embedding_grads(sink, dg, tgt_in, keep_tgt, p_drop, emb_cfg)
@@ -1234,12 +1316,18 @@ class Transformer:
         dh = arena.alloc((b, ls, d), dt)
         _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
         arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
+        join()
         for i in reversed(range(cfg.n_enc)):
             dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
                                         arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
+            join()
         keep_src = stash.pop("src_keep")
         self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
         arena.free(dh); arena.free(keep_src)
+        join()
+        if lane is not None:
+            sink.lane = None
+        arena = main_arena
         if len(stash):
             raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")
         # deferred gradient partials are consumed by the engine's narrow pass, which
