@@ -240,6 +240,19 @@ int ls2_gemm_lt(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t
                 const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
                 int64_t ldc, const void* bias, int tab, int tc, void* stream);
 
+/* ---- data-parallel exchange: NCCL over NVLink/NVSwitch ----
+ * Replaces the reference's "already-reduced gradients" contract (F/engine.py:4-7,
+ * SPEC.md:569).  libnccl.so.2 is bound at run time (the copy already loaded by
+ * torch.distributed when present).  ls2_comm_allreduce is a stream-ordered sum
+ * (in place when send == recv) and may be captured into a CUDA graph. */
+int ls2_comm_load(const char* path);
+int ls2_comm_version(int* out);
+int ls2_comm_unique_id(uint8_t* out128);
+int ls2_comm_init(void** comm_out, int nranks, int rank, const uint8_t* id128, int device);
+int ls2_comm_allreduce(void* comm, const void* send, void* recv, int64_t count, int dtype,
+                       void* stream);
+int ls2_comm_destroy(void* comm);
+
 #ifdef __cplusplus
 }
 #endif

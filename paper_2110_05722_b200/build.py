@@ -60,7 +60,7 @@ def _link_flags():
             break
     lib = ["-Xlinker", "-l:" + os.path.basename(cublas)] if cublas else ["-lcublas"]
     lib += ["-Xlinker", "-l:libcublasLt.so.12"]
-    return rp + ldirs + lib + ["-cudart", "shared"]
+    return rp + ldirs + lib + ["-ldl", "-cudart", "shared"]
 
 
 def _sources():

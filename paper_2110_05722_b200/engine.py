@@ -124,6 +124,11 @@ class TrainingEngine:
         self._dev_out = torch.zeros(5, dtype=torch.float64, device=self.device)
         self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
         self.dp = dp if dp is not None else DataParallel()
+        self._xplan = None
+        if self.dp.active:
+            self.dp.setup_device(self.device)
+            self._xplan = self.dp.exchange_plan(
+                [(lk.name, lk.offset, lk.length) for lk in self.ws.links], n)
         self.applied_steps = 0
         self.skip_count = 0
         self.arena: PlannedArena | None = None
@@ -194,6 +199,13 @@ class TrainingEngine:
             io.upload()
         self.arena.begin(key)
         sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
+        if self.dp.active:
+            # buckets are narrowed / all-reduced on the comm stream while the
+            # backward pass is still running (dist.py)
+            self._nonfinite.zero_()
+            self._xplan.reset()
+            self._totals_sent = False
+            sink.on_ready = lambda names, _s=sink: self._on_ready(_s, names)
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
             arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
@@ -210,12 +222,16 @@ class TrainingEngine:
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
         with _no_gc():
-            with torch.cuda.graph(g, stream=_lib.context().compute_stream):
+            with torch.cuda.graph(g, stream=_lib.context().compute_stream, **self._capture_kw()):
                 out3, sink = self._fwd_bwd(io, key, 0, upload=False)
                 self._update(out3, sink, host_copy=False)
         self._launches[key] = _lib.launches() - n0
         torch.cuda.synchronize()
         return g
+
+    def _capture_kw(self) -> dict:
+        # NCCL's proxy thread may touch the CUDA API while our stream captures
+        return {"capture_error_mode": "thread_local"} if self.dp.active else {}
 
     def launches_per_step(self, key) -> int:
         return int(self._launches.get(key, 0))
@@ -227,12 +243,44 @@ class TrainingEngine:
         self._update(*self._fwd_bwd(io, key, step, upload=False), host_copy=False)
         self._launches[key] = _lib.launches() - n0
 
-    def _finish_deferred(self, sink, out3, nonfinite_ptr):
+    # -- data-parallel exchange overlapped with backward (dist.py) ----------------------
+
+    def _on_ready(self, sink, names):
+        spans = self._xplan.finish_all() if names is None else self._xplan.ready(names)
+        for span in spans:
+            self._exchange_bucket(sink, *span)
+
+    def _exchange_bucket(self, sink, start: int, stop: int):
+        """On the comm stream, after everything the compute stream has enqueued so
+        far: narrow [start, stop) (+ its deferred column sums), sum-all-reduce it
+        and count non-finite values of the reduced bucket."""
+        t = self.cfg.train
+        cs = self.dp.comm_stream
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            out3 = sink.totals
+            if not self._totals_sent:
+                self.dp.allreduce_totals(out3, stream=cs)
+                self._totals_sent = True
+            ws = self.ws
+            _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr() + 4 * start,
+                      ws.grads16.data_ptr() + 2 * start, stop - start, float(t.loss_scale),
+                      out3.data_ptr(), -1, float(1.0 / t.act_grad_scale), None, cs.cuda_stream)
+            entries = [e for e in sink.deferred if start <= self.ws.resolve(e[0])[0] < stop]
+            self._finish_deferred(sink, out3, None, entries=entries)
+            self.dp.allreduce_span(ws.grads16, start, stop, stream=cs)
+            _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr() + 2 * start, stop - start,
+                      self._nonfinite.data_ptr(), cs.cuda_stream)
+
+    def _finish_deferred(self, sink, out3, nonfinite_ptr, entries=None):
         """One launch finishing every deferred bias / LayerNorm gradient (partials
         left by their producers) straight into the fp16 workspace."""
-        if sink is None or not sink.deferred:
+        entries = sink.deferred if (entries is None and sink is not None) else entries
+        if not entries:
             return
-        key = tuple((n, buf.data_ptr(), nb, st, k, c) for n, buf, nb, st, k, c in sink.deferred)
+        key = tuple((n, buf.data_ptr(), nb, st, k, c) for n, buf, nb, st, k, c in entries)
         tab = self._finish_tables.get(key)
         if tab is None:
             desc, chunks = [], []
@@ -254,17 +302,16 @@ class TrainingEngine:
         t = self.cfg.train
         ws = self.ws
         if self.dp.active:
-            self.dp.allreduce_totals(out3)
-        self._nonfinite.zero_()
-        _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr(), ws.grads16.data_ptr(),
-                  ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
-                  float(1.0 / t.act_grad_scale),
-                  None if self.dp.active else self._nonfinite.data_ptr(), st)
-        self._finish_deferred(sink, out3, None if self.dp.active else self._nonfinite.data_ptr())
-        if self.dp.active:
-            self.dp.allreduce_grads(ws.grads16)
-            _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr(), ws.n_elements,
-                      self._nonfinite.data_ptr(), st)
+            # every bucket was narrowed + reduced + checked on the comm stream
+            ev = torch.cuda.Event()
+            ev.record(self.dp.comm_stream)
+            torch.cuda.current_stream().wait_event(ev)
+        else:
+            self._nonfinite.zero_()
+            _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr(), ws.grads16.data_ptr(),
+                      ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
+                      float(1.0 / t.act_grad_scale), self._nonfinite.data_ptr(), st)
+            self._finish_deferred(sink, out3, self._nonfinite.data_ptr())
         loss_ptr = out3.data_ptr()
         if self.optim.algorithm == "adam":
             _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
@@ -296,11 +343,9 @@ class TrainingEngine:
 
     def _capture(self, io, key, step):
         """Capture fwd/bwd + update of this bucket into one CUDA graph."""
-        if self.dp.active:
-            return  # collectives stay eager under DP (see DESIGN.md)
         g = torch.cuda.CUDAGraph()
         with _no_gc():
-            with torch.cuda.graph(g, stream=_lib.context().compute_stream):
+            with torch.cuda.graph(g, stream=_lib.context().compute_stream, **self._capture_kw()):
                 out3, sink = self._fwd_bwd(io, key, step)
                 self._update(out3, sink)
         self._graphs[key] = g

@@ -352,6 +352,16 @@ class _ViewSink(GradSink):
         self.deferred: list = []          # (name, buf, nblk, stride, k, cols)
         self.arena = None
         self.lane = None                  # _Lane for weight-gradient GEMMs (engine path)
+        self.on_ready = None              # engine hook: gradients of these names are final
+        self.totals = None                # (loss, count, correct) once the criterion ran
+
+    def ready(self, prefixes):
+        """Backward has finished every parameter whose name starts with one of
+        `prefixes` (None: all remaining) — the data-parallel exchange may start."""
+        if self.on_ready is not None:
+            names = None if prefixes is None else \
+                [n for n in self.store if any(n.startswith(p) for p in prefixes)]
+            self.on_ready(names)
 
     def add(self, name: str, value):
         if name in self.written:
@@ -446,6 +456,12 @@ class _LaneArena:
 
     def __getattr__(self, name):
         return getattr(self._arena, name)
+
+
+def _ready(sink, *prefixes):
+    fn = getattr(sink, "ready", None)
+    if fn is not None:
+        fn(list(prefixes) if prefixes != (None,) else None)
 
 
 def _defer(sink, names, nblk, np_, cols):
@@ -1256,6 +1272,8 @@ class Transformer:
                       int(batch.pad_id), 1, float(grad_scale), _lib.dtype_code(logits),
                       _lib.stream_handle())
         arena.free(row_stats)
+        if isinstance(sink, _ViewSink):
+            sink.totals = out3            # the exchange all-reduces these first
         out = ModelOutput(out3)
         if capture is not None:
             capture["logq"] = logq.view(b, lt, v)
@@ -1287,6 +1305,7 @@ class Transformer:
         dg = arena.alloc((b, lt, d), dt)
         _ln_bwd(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg, None)
         arena.free(ddec); arena.free(mu_d); arena.free(sg_d); arena.free(g_in)
+        _ready(sink, "dec_ln.", "out_proj.")
 
         # --- backward: decoder stack; dK_i/dV_i land in one packed buffer ---
         dkv = arena.alloc((b, ls, 2 * cfg.n_dec * d), dt)
@@ -1299,6 +1318,7 @@ class Transformer:
                 dg, dec_w[i], kv_pairs[i], stash, sink, n_heads=n, p_drop=p_drop, arena=arena,
                 prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest)
             join()
+            _ready(sink, f"dec{i}.")
             emit(("dec_layer_backward_done", i))
         keep_tgt = stash.pop("tgt_keep")
         self._embedding_grads(sink, dg, tgt_in, keep_tgt, p_drop, emb_cfg)
@@ -1317,14 +1337,17 @@ class Transformer:
         _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
         arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
         join()
+        _ready(sink, "cross_kv.", "enc_ln.")
         for i in reversed(range(cfg.n_enc)):
             dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
                                         arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
             join()
+            _ready(sink, f"enc{i}.")
         keep_src = stash.pop("src_keep")
         self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
         arena.free(dh); arena.free(keep_src)
         join()
+        _ready(sink, None)
         if lane is not None:
             sink.lane = None
         arena = main_arena

@@ -69,12 +69,24 @@ def _worker(rank, world, port, out_q):
     dp.allreduce_totals(totals)
     scale = np.float32(4.0 / totals[1].item())          # loss_scale 4 / global count
     g16 = torch.from_numpy(O.to_half(acc * scale))
-    dp.allreduce_grads(g16)
+    # the engine's overlapped recipe: backward finishes parameters in reverse
+    # layout order; each finished suffix bucket is all-reduced as it appears
+    links, off = [], 0
+    for name, shp in shapes:
+        links.append((name, off, int(np.prod(shp))))
+        off += int(np.prod(shp))
+    plan = dp.exchange_plan(links, off, elem_bytes=2)
+    spans = []
+    for name, _, _ in reversed(links):
+        spans += plan.ready([name])
+    spans += plan.flush()
+    for s, e in spans:
+        dp.allreduce_span(g16, s, e)
     m = np.zeros(p16.size, np.float32)
     v = np.zeros(p16.size, np.float32)
     bad = O.adam_flat(p16, g16.numpy(), m, v, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0,
                       loss_scale=4.0, t=1)
-    out_q.put((rank, totals.numpy().tolist(), p16.copy(), bad, dp.buckets(p16.size)))
+    out_q.put((rank, totals.numpy().tolist(), p16.copy(), bad, spans))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -110,3 +122,34 @@ def test_two_rank_step_equals_one_rank_step():
     diff = np.abs(p0.astype(np.float32) - p16.astype(np.float32))
     assert diff.max() <= 2e-2 * max(1.0, np.abs(p16.astype(np.float32)).max())
     assert np.mean(p0 != p16) < 0.2
+
+
+def test_grad_exchange_plan_reverse_suffix_buckets():
+    from paper_2110_05722_b200.dist import GradExchange
+    links = [("a", 0, 10), ("b", 10, 5), ("c", 15, 20), ("d", 35, 5)]
+    x = GradExchange(links, 40, bucket_elems=8)
+    assert x.ready(["d"]) == []                 # 5 pending < 8
+    assert x.ready(["b"]) == []                 # not a suffix yet (c missing)
+    assert x.ready(["c"]) == [(10, 40)]          # c and b join the suffix
+    with pytest.raises(RuntimeError):
+        GradExchange(links, 40, 8).flush()       # nothing finished
+    x.reset()
+    out = x.ready(["d", "c", "b", "a"])
+    assert out == [(0, 40)] and x.flush() == []
+
+
+def test_grad_exchange_plan_small_buckets_cover_exactly():
+    from paper_2110_05722_b200.dist import GradExchange
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(1, 50, 30)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    links = [(f"p{i}", int(o), int(s)) for i, (o, s) in enumerate(zip(offs, sizes))]
+    n = int(sizes.sum())
+    x = GradExchange(links, n, bucket_elems=40)
+    spans = []
+    for i in reversed(range(30)):
+        spans += x.ready([f"p{i}"])
+    spans += x.flush()
+    assert spans[0][1] == n and spans[-1][0] == 0
+    assert all(a[0] == b[1] for a, b in zip(spans, spans[1:]))
+    assert all(e - s >= 40 for s, e in spans[:-1])
