@@ -12,9 +12,13 @@
 // over the same row (in place).  Longer rows take a two-pass variant whose
 // second read hits L2.  Per-row (loss, correct) partials are reduced in a fixed
 // order by a single-CTA kernel, so the loss is bit-reproducible.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ls2 {
 
@@ -237,16 +241,26 @@ __global__ void __launch_bounds__(kCeThreads, ITERS >= 4 ? 1 : 2) criterion_kern
 }
 
 // ---------------------------------------------------------------------------
-// Persistent TMA-pipelined variant (16-bit logits, V % 8 == 0, 2 rows fit in smem).
-// One 1024-thread CTA per SM walks rows blockIdx.x, +gridDim.x, ...; row k+1 is
-// bulk-copied (cp.async.bulk, mbarrier completion) into the other smem buffer
-// while row k is reduced, so the HBM read of the next row overlaps the ALU work
-// and the (fire-and-forget) gradient stores of the current one.  Per row:
-//   pass 1  sum(h) and max(h)                      (smem reads)
-//   pass 2  e = exp(h - max), Z = sum(e), first argmax; e (scaled) overwrites h
-//   pass 3  dlogits = (e/Z - a/V - (1-a)[i==k]) * grad_scale  -> HBM, in place
-// The CTA accumulates its rows' (loss, correct, count) in row order and leaves
-// one triple per CTA for the fixed-order final reduce (deterministic).
+// ---------------------------------------------------------------------------
+// Persistent row kernel (16-bit logits, V % 8 == 0).  A cluster of C CTAs owns
+// a row (C = 1 while two rows fit in one SM's shared memory; C = 2..16 for
+// V up to 512k, SURVEY §7 hard part 7): CTA q holds columns [q*S, q*S+len_q).
+// Each CTA walks rows cid, cid+ncl, ...; its slice of row k+2 is bulk-copied
+// (cp.async.bulk, mbarrier completion) into the buffer row k has just left,
+// so two row loads are in flight while row k is reduced.  Every logit is read
+// from HBM once and its gradient written once.  Per row, per thread:
+//   load     its CH 16-byte chunks from shared memory into registers (the only
+//            shared-memory pass; the buffer is released right after)
+//   pass 1   packed max, fp32x2 sum of h
+//   pass 2   e = 2^(log2e (h - m_q) + log2 scale) in registers, Z_q, first argmax
+//   pass 3   dlogits = (e s_q / Z - a/V - (1-a)[i==k]) * grad_scale -> HBM, in place
+// where m_q is the slice max.  With C > 1 the CTAs push (m_q, Z_q, sum h,
+// first, h[target]) into every cluster CTA's shared memory (DSMEM) and after
+// ONE cluster barrier per row merge them online-softmax style,
+//   M = max m_q,  Z = sum_q Z_q 2^(log2e (m_q - M)),  s_q = 2^(log2e (m_q - M)),
+// with the same fixed shuffle tree in every CTA: identical M and Z everywhere,
+// deterministic results.  Rank 0 of each cluster accumulates the rows'
+// (loss, correct, count) in row order for the fixed-order final reduce.
 // ---------------------------------------------------------------------------
 constexpr int kCeTmaThreads = 1024;
 constexpr int kCeTmaWarps = kCeTmaThreads / 32;
@@ -318,167 +332,298 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return y;
 }
 
-// CH = 16-byte chunks per thread per row (compile-time, fully unrolled)
-template <typename T, int CH>
-__global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_tma_kernel(
+
+// G row groups per CTA (1024/G threads each, named barriers): with G = 2 the
+// two halves of the SM work on different rows, so one half's exp pass (MUFU)
+// overlaps the other's gradient stores instead of every warp hitting the same
+// pipe at once.  G = 1 double-buffers (row k+2 loads while k is reduced); G = 2
+// gives each group one buffer, refilled with the group's next row as soon as
+// the current one is in registers.  Clusters (C > 1) use G = 1.
+template <int G>
+__device__ __forceinline__ void group_sync(int g) {
+  if constexpr (G == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kCeTmaThreads / G) : "memory");
+  }
+}
+
+template <typename T, int CH, int G>
+__global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
     const T* __restrict__ logits, const int64_t* __restrict__ targets, T* dlogits,
-    double* __restrict__ cta_stats, int* __restrict__ bad_target, int64_t rows, int V,
+    double* __restrict__ cl_stats, int* __restrict__ bad_target, int64_t rows, int V, int S,
     double alpha, int64_t pad_id, int has_pad, double grad_scale) {
   using PT = Pair<T>;
   using P2 = typename PT::P2;
   struct alignas(16) Chunk { P2 h[4]; };
+  constexpr int kMaxC = 16;
+  constexpr int NT = kCeTmaThreads / G;         // threads per row group
+  constexpr int WG = NT / 32;                   // warps per row group
+  constexpr int NB = G == 1 ? 2 : 1;            // row buffers per group
   extern __shared__ __align__(128) uint8_t ce_smem[];
   __shared__ uint64_t bar[2];
-  __shared__ float s_max[kCeTmaWarps], s_z[kCeTmaWarps];
-  __shared__ double s_sh[kCeTmaWarps];
-  __shared__ int s_first[kCeTmaWarps];
-  __shared__ float s_ht;
-  const uint32_t row_bytes = (uint32_t)V * sizeof(T);
-  const uint32_t buf_stride = (row_bytes + 127u) & ~127u;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nchunk = V / 8;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  __shared__ float s_max[G][WG], s_z[G][WG];
+  __shared__ double s_sh[G][WG];
+  __shared__ int s_first[G][WG];
+  __shared__ float s_ht[G];
+  __shared__ double s_acc[G][3];     // per group: (loss, correct, count) in row order
+  // cluster exchange slots [row parity][source rank], pushed by the source CTA
+  __shared__ float x_max[2][kMaxC], x_z[2][kMaxC], x_ht[2][kMaxC];
+  __shared__ double x_sh[2][kMaxC];
+  __shared__ int x_first[2][kMaxC];
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();
+  const int q = C > 1 ? (int)cl.block_rank() : 0;
+  const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
+  const int col0 = q * S;
+  const int len = min(S, V - col0);
+  const uint32_t slice_bytes = (uint32_t)len * sizeof(T);
+  const uint32_t buf_stride = ((uint32_t)S * sizeof(T) + 127u) & ~127u;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = tid / NT, gt = tid % NT, gw = gt >> 5;
+  const int nchunk = len / 8;
+  // group-local row k of group g: cid + (k*G + g) * ncl
+  const int64_t rstride = (int64_t)G * ncl;
+  const int64_t r0 = cid + (int64_t)g * ncl;
+  if (gt == 0) {
+    for (int i = 0; i < NB; ++i) mbar_init(&bar[g * NB + i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if ((int64_t)blockIdx.x < rows)
-      bulk_load(ce_smem, logits + (int64_t)blockIdx.x * V, row_bytes, &bar[0]);
+    for (int i = 0; i < NB; ++i)
+      if (r0 + i * rstride < rows)
+        bulk_load(ce_smem + (g * NB + i) * buf_stride, logits + (r0 + i * rstride) * V + col0,
+                  slice_bytes, &bar[g * NB + i]);
+    s_acc[g][0] = s_acc[g][1] = s_acc[g][2] = 0.0;
   }
   __syncthreads();
   const float l2e = 1.4426950408889634f;
   const float a_v = (float)(alpha / (double)V);
   const float one_m_a = (float)(1.0 - alpha);
-  double acc_loss = 0.0, acc_corr = 0.0, acc_cnt = 0.0;  // thread 0 only
+  int64_t tgt_next = r0 < rows ? targets[r0] : 0;
   int k = 0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++k) {
-    const int b = k & 1;
-    const int64_t rn = r + gridDim.x;
-    const int64_t tgt = targets[r];
-    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
-    if (tid == 0 && rn < rows) {
-      // the other buffer was last read (and written by the generic proxy) in
-      // the previous iteration, which every thread has left (barrier below)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bulk_load(ce_smem + (b ^ 1) * buf_stride, logits + rn * V, row_bytes, &bar[b ^ 1]);
-    }
-    Chunk* row = reinterpret_cast<Chunk*>(ce_smem + b * buf_stride);
+  for (int64_t r = r0; r < rows; r += rstride, ++k) {
+    const int bi = g * NB + (k % NB);
+    const int xb = k & 1;                                  // cluster slot parity
+    const int64_t tgt = tgt_next;
+    if (r + rstride < rows) tgt_next = targets[r + rstride];
     const bool valid = !(has_pad && tgt == pad_id);
     const bool tgt_ok = tgt >= 0 && tgt < V;
-    if (valid && !tgt_ok && tid == 0 && bad_target) *bad_target = 1;
-    const int tchunk = (valid && tgt_ok) ? (int)(tgt >> 3) : -1;
-    if (tchunk >= 0 && tid == tchunk % kCeTmaThreads)
-      s_ht = cvt<float>(reinterpret_cast<const T*>(row)[tgt]);
-    // pass 1: packed max, fp32x2 sum
-    P2 m2 = PT::pack(make_float2(-INFINITY, -INFINITY));
-    float2 s2 = make_float2(0.f, 0.f);
+    if (valid && !tgt_ok && gt == 0 && q == 0 && bad_target) *bad_target = 1;
+    const int64_t lt = tgt - col0;                         // target's local column
+    const bool own_t = valid && tgt_ok && lt >= 0 && lt < len;
+    mbar_wait(&bar[bi], (uint32_t)((k / NB) & 1));
+    const Chunk* row = reinterpret_cast<const Chunk*>(ce_smem + bi * buf_stride);
+    // all CH chunks of this thread in range: straight-line passes (warp-uniform
+    // for every warp but the one straddling the slice end)
+    const bool full = gt + (CH - 1) * NT < nchunk;
+    Chunk hq[CH];
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const int c = tid + j * kCeTmaThreads;
-      if (c < nchunk) {
-        const Chunk q = row[c];
+      for (int j = 0; j < CH; ++j) hq[j] = row[gt + j * NT];
+    } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          m2 = PT::max(m2, q.h[e]);
-          s2 = fadd2(s2, PT::f(q.h[e]));
-        }
+      for (int j = 0; j < CH; ++j) {
+        const int c = gt + j * NT;
+        if (c < nchunk) hq[j] = row[c];
       }
     }
+    if (gt == 0) s_ht[g] = own_t ? cvt<float>(reinterpret_cast<const T*>(row)[lt]) : 0.f;
+    // pass 1 (registers): packed max, fp32x2 sum
+    P2 m2 = PT::pack(make_float2(-INFINITY, -INFINITY));
+    float2 s2 = make_float2(0.f, 0.f);
+    auto pass1 = [&](auto fc) {
+      constexpr bool F = decltype(fc)::value;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (F || gt + j * NT < nchunk) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            m2 = PT::max(m2, hq[j].h[e]);
+            s2 = fadd2(s2, PT::f(hq[j].h[e]));
+          }
+        }
+      }
+    };
+    if (full) pass1(std::true_type{}); else pass1(std::false_type{});
     const float mloc = PT::hi_lo_max(m2);
     float m = mloc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_max[wid] = m;
-    __syncthreads();
-    float mx = s_max[lane];
+    if (lane == 0) s_max[g][gw] = m;
+    group_sync<G>(g);              // the row buffer is consumed: refill it
+    if (gt == 0 && r + NB * rstride < rows) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(ce_smem + bi * buf_stride, logits + (r + NB * rstride) * V + col0, slice_bytes,
+                &bar[bi]);
+    }
+    float mq = lane < WG ? s_max[g][lane] : -INFINITY;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    // pass 2: e = 2^(log2e*(h - max) + log2 scale), Z, e overwrites h.  The
-    // first argmax is searched (on the raw values) only by threads whose own
-    // maximum is the row maximum, in chunk order.
-    const float off = PT::kLog2Scale - mx * l2e;
+    for (int o = 16; o > 0; o >>= 1) mq = fmaxf(mq, __shfl_xor_sync(0xffffffffu, mq, o));
+    // pass 2 (registers): exps relative to the slice max, Z_q, first argmax
+    const float off = PT::kLog2Scale - mq * l2e;
     const float2 l2e2 = make_float2(l2e, l2e), off2 = make_float2(off, off);
-    const bool mine = (mloc == mx);
-    float2 z2 = make_float2(0.f, 0.f);
     int first = INT32_MAX;
+    if (mloc == mq) {
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const int c = tid + j * kCeTmaThreads;
-      if (c < nchunk) {
-        Chunk q = row[c];
-        if (mine && first == INT32_MAX) {
-          const T* hv = reinterpret_cast<const T*>(&q);
+      for (int j = 0; j < CH; ++j) {
+        const int c = gt + j * NT;
+        if (c < nchunk && first == INT32_MAX) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (first == INT32_MAX && cvt<float>(hv[e]) == mx) first = c * 8 + e;
+          for (int e = 0; e < 4; ++e) {
+            const float2 hv = PT::f(hq[j].h[e]);
+            if (first == INT32_MAX && hv.x == mq) first = col0 + c * 8 + 2 * e;
+            if (first == INT32_MAX && hv.y == mq) first = col0 + c * 8 + 2 * e + 1;
+          }
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 a = ffma2(PT::f(q.h[e]), l2e2, off2);
-          const float2 ex = make_float2(ex2_ftz(a.x), ex2_ftz(a.y));
-          z2 = fadd2(z2, ex);
-          q.h[e] = PT::pack(ex);
-        }
-        row[c] = q;
       }
     }
+    float2 z2 = make_float2(0.f, 0.f);
+    auto pass2 = [&](auto fc) {
+      constexpr bool F = decltype(fc)::value;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (F || gt + j * NT < nchunk) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 a = ffma2(PT::f(hq[j].h[e]), l2e2, off2);
+            const float2 ex = make_float2(ex2_ftz(a.x), ex2_ftz(a.y));
+            z2 = fadd2(z2, ex);
+            hq[j].h[e] = PT::pack(ex);
+          }
+        }
+      }
+    };
+    if (full) pass2(std::true_type{}); else pass2(std::false_type{});
     float z = z2.x + z2.y;
-    double shd = (double)s2.x + (double)s2.y;
+    double sh = (double)s2.x + (double)s2.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       z += __shfl_xor_sync(0xffffffffu, z, o);
-      shd += __shfl_xor_sync(0xffffffffu, shd, o);
+      sh += __shfl_xor_sync(0xffffffffu, sh, o);
       first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
     }
-    if (lane == 0) { s_z[wid] = z; s_sh[wid] = shd; s_first[wid] = first; }
-    __syncthreads();
-    float zt = s_z[lane];
-    int ft = s_first[lane];
+    if (lane == 0) { s_z[g][gw] = z; s_sh[g][gw] = sh; s_first[g][gw] = first; }
+    group_sync<G>(g);
+    float M, zt, scale;
+    if (C == 1) {
+      M = mq;
+      zt = lane < WG ? s_z[g][lane] : 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      zt += __shfl_xor_sync(0xffffffffu, zt, o);
-      ft = min(ft, __shfl_xor_sync(0xffffffffu, ft, o));
-    }
-    if (tid == 0) {
-      double sht = 0.0;
-      for (int q = 0; q < kCeTmaWarps; ++q) sht += s_sh[q];
-      // zt = 2^scale * Z
-      const double lse = (double)mx + log((double)zt) - (double)PT::kLog2Scale * 0.6931471805599453;
-      if (valid && tgt_ok) {
-        acc_loss += -(1.0 - alpha) * ((double)s_ht - lse) -
-                    (alpha / (double)V) * (sht - (double)V * lse);
-        acc_corr += (ft == tgt) ? 1.0 : 0.0;
-      }
-      acc_cnt += valid ? 1.0 : 0.0;
-    }
-    // pass 3: gradient (e * gs / Z - gs * a/V) streamed to HBM over the consumed row
-    if (dlogits) {
-      const float gs = valid ? (float)grad_scale : 0.f;
-      const float cz = gs / zt;                 // zt carries the cache scale
-      const float2 cz2 = make_float2(cz, cz), of2 = make_float2(-a_v * gs, -a_v * gs);
-      T* drow = dlogits + r * (int64_t)V;
+      for (int o = 16; o > 0; o >>= 1) zt += __shfl_xor_sync(0xffffffffu, zt, o);
+      scale = 1.f;
+      if (gw == 0) {
+        int ft = lane < WG ? s_first[g][lane] : INT32_MAX;
+        double sht = lane < WG ? s_sh[g][lane] : 0.0;
 #pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        const int c = tid + j * kCeTmaThreads;
-        if (c < nchunk) {
-          Chunk q = row[c];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) q.h[e] = PT::pack(ffma2(PT::f(q.h[e]), cz2, of2));
-          *reinterpret_cast<uint4*>(drow + c * 8) = *reinterpret_cast<const uint4*>(&q);
+        for (int o = 16; o > 0; o >>= 1) {
+          ft = min(ft, __shfl_xor_sync(0xffffffffu, ft, o));
+          sht += __shfl_xor_sync(0xffffffffu, sht, o);
+        }
+        if (lane == 0) {
+          const double lse = (double)M + log((double)zt) - (double)PT::kLog2Scale * 0.6931471805599453;
+          if (valid && tgt_ok) {
+            s_acc[g][0] += -(1.0 - alpha) * ((double)s_ht[g] - lse) -
+                           (alpha / (double)V) * (sht - (double)V * lse);
+            s_acc[g][1] += (ft == tgt) ? 1.0 : 0.0;
+          }
+          s_acc[g][2] += valid ? 1.0 : 0.0;
         }
       }
-      if (tchunk >= 0 && tid == tchunk % kCeTmaThreads) {
-        // same thread, later store: the target element gets its -(1-a) term
-        const float et = cvt<float>(reinterpret_cast<const T*>(row)[tgt]);
-        drow[tgt] = cvt<T>(fmaf(et, cz, -a_v * gs) - one_m_a * gs);
+    } else {
+      if (gw == 0) {
+        float zz = s_z[0][lane];
+        double ss = s_sh[0][lane];
+        int ff = s_first[0][lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          zz += __shfl_xor_sync(0xffffffffu, zz, o);
+          ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          ff = min(ff, __shfl_xor_sync(0xffffffffu, ff, o));
+        }
+        if (lane < C) {
+          *cl.map_shared_rank(&x_max[xb][q], lane) = mq;
+          *cl.map_shared_rank(&x_z[xb][q], lane) = zz;
+          *cl.map_shared_rank(&x_sh[xb][q], lane) = ss;
+          *cl.map_shared_rank(&x_first[xb][q], lane) = ff;
+          *cl.map_shared_rank(&x_ht[xb][q], lane) = s_ht[0];
+        }
+      }
+      cl.sync();                                           // the one exchange per row
+      const float mp = lane < C ? x_max[xb][lane] : -INFINITY;
+      M = mp;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      zt = lane < C ? x_z[xb][lane] * exp2f((mp - M) * l2e) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) zt += __shfl_xor_sync(0xffffffffu, zt, o);
+      scale = exp2f((mq - M) * l2e);
+      if (q == 0 && gw == 0) {
+        int ft = (lane < C && mp == M) ? x_first[xb][lane] : INT32_MAX;
+        double sht = lane < C ? x_sh[xb][lane] : 0.0;
+        float ht = lane < C ? x_ht[xb][lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ft = min(ft, __shfl_xor_sync(0xffffffffu, ft, o));
+          sht += __shfl_xor_sync(0xffffffffu, sht, o);
+          ht += __shfl_xor_sync(0xffffffffu, ht, o);
+        }
+        if (lane == 0) {
+          const double lse = (double)M + log((double)zt) - (double)PT::kLog2Scale * 0.6931471805599453;
+          if (valid && tgt_ok) {
+            s_acc[0][0] += -(1.0 - alpha) * ((double)ht - lse) -
+                           (alpha / (double)V) * (sht - (double)V * lse);
+            s_acc[0][1] += (ft == tgt) ? 1.0 : 0.0;
+          }
+          s_acc[0][2] += valid ? 1.0 : 0.0;
+        }
       }
     }
-    __syncthreads();  // buffer b fully consumed before it is refilled
+    // pass 3 (registers -> HBM): gradient, in place
+    if (dlogits) {
+      const float gs = valid ? (float)grad_scale : 0.f;
+      const float cz = gs * scale / zt;                   // zt carries the cache scale
+      const float2 cz2 = make_float2(cz, cz), of2 = make_float2(-a_v * gs, -a_v * gs);
+      T* drow = dlogits + r * (int64_t)V + col0;
+      auto pass3 = [&](auto fc) {
+        constexpr bool F = decltype(fc)::value;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = gt + j * NT;
+          if (F || c < nchunk) {
+            Chunk o;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o.h[e] = PT::pack(ffma2(PT::f(hq[j].h[e]), cz2, of2));
+            *reinterpret_cast<uint4*>(drow + c * 8) = *reinterpret_cast<const uint4*>(&o);
+          }
+        }
+      };
+      if (full) pass3(std::true_type{}); else pass3(std::false_type{});
+      if (own_t && gt == (int)((lt >> 3) % NT)) {
+        // same thread, later store: the target element gets its -(1-a) term
+        // (its exp re-read from the register chunk with compile-time indices)
+        const int jt = (int)((lt >> 3) / NT), et = (int)(lt & 7);
+        float ev = 0.f;
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (j == jt) {
+              const float2 f = PT::f(hq[j].h[e]);
+              if (2 * e == et) ev = f.x;
+              if (2 * e + 1 == et) ev = f.y;
+            }
+        drow[lt] = cvt<T>(fmaf(ev, cz, -a_v * gs) - one_m_a * gs);
+      }
+    }
   }
-  if (tid == 0) {
-    cta_stats[3 * blockIdx.x + 0] = acc_loss;
-    cta_stats[3 * blockIdx.x + 1] = acc_corr;
-    cta_stats[3 * blockIdx.x + 2] = acc_cnt;
+  __syncthreads();
+  if (tid == 0 && q == 0) {
+    double l = 0.0, c1 = 0.0, n = 0.0;
+    for (int i = 0; i < G; ++i) { l += s_acc[i][0]; c1 += s_acc[i][1]; n += s_acc[i][2]; }
+    cl_stats[3 * cid + 0] = l;
+    cl_stats[3 * cid + 1] = c1;
+    cl_stats[3 * cid + 2] = n;
   }
+  if (C > 1) cl.sync();  // no CTA exits while remote stores into it may be in flight
 }
 
 // fixed-order sum of per-CTA (loss, correct, count) triples: one warp, lane l
@@ -581,6 +726,106 @@ __global__ void ls_ce_bwd_kernel(const Tin* __restrict__ probs, const int64_t* _
   }
 }
 
+// Row ownership for the persistent kernel: C = 1 (S = V) while two rows fit in
+// 200 KB of shared memory, else the smallest cluster whose slices of S <= 32768
+// 16-bit elements (64 KB, double-buffered) cover the row.  0: no fit.
+static int ce_cluster_size(int64_t v, int* slice) {
+  if (2 * (((v * 2 + 127) / 128) * 128) <= 200 * 1024) {
+    *slice = (int)v;
+    return 1;
+  }
+  for (int c = 2; c <= 16; c *= 2) {
+    const int64_t s = ceil_div(ceil_div(v, (int64_t)c), (int64_t)8) * 8;
+    if (s <= 32768 && (c - 1) * s < v) {
+      *slice = (int)s;
+      return c;
+    }
+  }
+  return 0;
+}
+
+template <typename T, int CH, int G>
+static int launch_ce_rows_ch(const T* logits, const int64_t* targets, T* dlogits, double* row_stats,
+                             double* out3, int* bad_target, int64_t rows, int64_t v, int C, int S,
+                             double alpha, int64_t pad_id, int has_pad, double grad_scale,
+                             cudaStream_t st) {
+  auto kern = criterion_rows_kernel<T, CH, G>;
+  const int smem = 2 * (int)(((int64_t)S * 2 + 127) / 128 * 128);   // G*NB == 2 buffers
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, int> max_clusters;   // (dev, C, smem)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kCeTmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  int ncl;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, C, smem);
+    auto it = max_clusters.find(key);
+    if (it == max_clusters.end()) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      int n = kNumSMs;
+      if (C > 1) {
+        if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cfg.gridDim = dim3(C * kNumSMs);
+        if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess || n <= 0) {
+          cudaGetLastError();
+          n = 0;
+        }
+      }
+      it = max_clusters.emplace(key, n).first;
+    }
+    ncl = it->second;
+  }
+  // per-cluster stats triples live in row_stats (3 * clusters <= 2 * rows)
+  ncl = (int)std::min<int64_t>(ncl, (2 * rows) / 3);
+  if (ncl <= 0) return -1;
+  cfg.gridDim = dim3(C * ncl);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, logits, targets, dlogits, row_stats, bad_target,
+                                     rows, (int)v, S, alpha, pad_id, has_pad, grad_scale);
+  if (e != cudaSuccess) return fail(LS2_ERR_CUDA, std::string("criterion_rows: ") + cudaGetErrorString(e));
+  if (int rc = check_launch("criterion_rows")) return rc;
+  criterion_reduce_cta<<<1, 32, 0, st>>>(row_stats, ncl, out3);
+  return check_launch("criterion_reduce");
+}
+
+template <typename T>
+static int launch_ce_rows(const T* logits, const int64_t* targets, T* dlogits, double* row_stats,
+                          double* out3, int* bad_target, int64_t rows, int64_t v, int C, int S,
+                          double alpha, int64_t pad_id, int has_pad, double grad_scale,
+                          cudaStream_t st) {
+#define LS2_CE_GO(CH_, G_)                                                                        \
+  return launch_ce_rows_ch<T, CH_, G_>(logits, targets, dlogits, row_stats, out3, bad_target,     \
+                                       rows, v, C, S, alpha, pad_id, has_pad, grad_scale, st)
+  // two row groups per CTA while a row fits 8 chunks per thread of a 512-thread group
+  static const bool groups2 = [] {
+    const char* e = getenv("LS2_CE_GROUPS");
+    return !(e && e[0] == '1');
+  }();
+  const int need2 = (int)ceil_div((int64_t)S / 8, (int64_t)(kCeTmaThreads / 2));
+  if (C == 1 && groups2 && need2 <= 8) {
+    if (need2 <= 1) LS2_CE_GO(1, 2);
+    if (need2 <= 2) LS2_CE_GO(2, 2);
+    if (need2 <= 4) LS2_CE_GO(4, 2);
+    LS2_CE_GO(8, 2);
+  }
+  const int need = (int)ceil_div((int64_t)S / 8, (int64_t)kCeTmaThreads);
+  if (need <= 1) LS2_CE_GO(1, 1);
+  if (need <= 2) LS2_CE_GO(2, 1);
+  if (need <= 4) LS2_CE_GO(4, 1);
+  LS2_CE_GO(7, 1);
+#undef LS2_CE_GO
+}
+
 }  // namespace ls2
 
 using namespace ls2;
@@ -596,41 +841,20 @@ int ls2_criterion_fused(const void* logits, const int64_t* targets, void* dlogit
   cudaStream_t st = as_stream(stream);
   const bool v8 = v % 8 == 0 && aligned16(logits) && (!dlogits || aligned16(dlogits)) &&
                   (!logq_out || aligned16(logq_out));
-  // persistent TMA path: 16-bit rows, two row buffers in shared memory; the
-  // per-CTA stats triples live in row_stats (needs 3 * grid <= 2 * rows)
-  const int64_t buf = ((v * 2 + 127) / 128) * 128;
-  if (v8 && !logq_out && rows >= 256 && 2 * buf <= 200 * 1024 && v < (1 << 24) &&
+  // persistent row kernel (16-bit rows in shared memory, clusters for long rows)
+  int cslice = 0;
+  const int ccl = ce_cluster_size(v, &cslice);
+  if (v8 && !logq_out && ccl > 0 && rows >= 2 && v < (1 << 24) &&
       (t_logits == LS2_F16 || t_logits == LS2_BF16)) {
-    const int grid = (int)std::min<int64_t>(rows, kNumSMs);
-    const int smem = (int)(2 * buf);
-    const int need = (int)ceil_div(v / 8, (int64_t)kCeTmaThreads);
-    auto go = [&](auto tag) -> int {
-      using T = typename decltype(tag)::type;
-      auto launch = [&](auto ch) -> int {
-        constexpr int CH = decltype(ch)::value;
-        static bool attr_set[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!attr_set[dev & 63]) {
-          cudaFuncSetAttribute(criterion_tma_kernel<T, CH>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          attr_set[dev & 63] = true;
-        }
-        criterion_tma_kernel<T, CH><<<grid, kCeTmaThreads, smem, st>>>(
-            (const T*)logits, targets, (T*)dlogits, row_stats, bad_target, rows, (int)v, alpha,
-            pad_id, has_pad, grad_scale);
-        return check_launch("criterion_fused");
-      };
-      int rc = need <= 1 ? launch(std::integral_constant<int, 1>{})
-             : need <= 2 ? launch(std::integral_constant<int, 2>{})
-             : need <= 4 ? launch(std::integral_constant<int, 4>{})
-                         : launch(std::integral_constant<int, 7>{});
-      if (rc) return rc;
-      criterion_reduce_cta<<<1, 32, 0, st>>>(row_stats, grid, out3);
-      return check_launch("criterion_reduce");
-    };
-    if (t_logits == LS2_F16) return go(std::type_identity<__half>{});
-    return go(std::type_identity<__nv_bfloat16>{});
+    int rc = t_logits == LS2_F16
+                 ? launch_ce_rows<__half>((const __half*)logits, targets, (__half*)dlogits,
+                                          row_stats, out3, bad_target, rows, v, ccl, cslice,
+                                          alpha, pad_id, has_pad, grad_scale, st)
+                 : launch_ce_rows<__nv_bfloat16>(
+                       (const __nv_bfloat16*)logits, targets, (__nv_bfloat16*)dlogits, row_stats,
+                       out3, bad_target, rows, v, ccl, cslice, alpha, pad_id, has_pad, grad_scale,
+                       st);
+    if (rc >= 0) return rc;        // -1: no cluster fits; take the generic path
   }
   int rc = [&]() -> int {
     auto go = [&](auto tag, auto iters) {

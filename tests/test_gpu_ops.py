@@ -200,7 +200,12 @@ def test_criterion_known_answers():
 
 @pytest.mark.parametrize("rows,v,dt", [(4096, 32000, "f16"), (512, 250000, "f16"), (37, 29, "f16"),
                                         (64, 1000, "f16"), (300, 51200, "f16"),
-                                        (1000, 32000, "bf16"), (256, 8, "f16")])
+                                        (1000, 32000, "bf16"), (256, 8, "f16"),
+                                        # cluster path: C = 2, 4, 8, 16 CTAs per row,
+                                        # ragged last slice, 2 rows, bf16
+                                        (300, 64000, "f16"), (257, 100008, "f16"),
+                                        (2, 250000, "f16"), (300, 128000, "bf16"),
+                                        (40, 500000, "f16")])
 def test_fused_criterion_vs_oracle(rows, v, dt):
     """Fused criterion (register, TMA-pipelined and two-pass variants) against the
     oracle: loss 1e-4, count exact, argmax-correct exact, gradient 2e-2 normwise."""

@@ -30,7 +30,7 @@ ALGO = [
     (r"ln_bwd_stage<[^>]*, false, false, false>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
     (r"attn_fwd_kernel", "fused attention fwd (QK^T, mask, softmax, PV)", 4 * N * D * 2 + BHL2 * 2),
     (r"attn_bwd_kernel", "fused attention bwd", 7 * N * D * 2 + BHL2 * 2),
-    (r"criterion_tma_kernel|criterion_kernel", "fused LS cross-entropy fwd+bwd (in place)",
+    (r"criterion_rows_kernel|criterion_kernel", "fused LS cross-entropy fwd+bwd (in place)",
      2 * N * V * 2),
     (r"adam_kernel", "workspace Adam (22 B/param)", 22 * P),
     (r"scale_narrow_kernel", "fp32 grad accumulators -> scaled fp16 workspace", 6 * P),
