@@ -60,6 +60,15 @@ int ls2_num_kernels_launched(int64_t* out);   /* launches since load (host count
  * thresh = ceil(p * 2^53).  Bit-identical to rand_uniform_array(seed,0,n) >= p. */
 int ls2_rand_uniform(double* out, uint64_t seed, int64_t start, int64_t n, void* stream);
 int ls2_dropout_bits(uint8_t* bits, int64_t n, uint64_t seed, const uint64_t* seed_ptr, uint64_t thresh, void* stream);
+/* every dropout site of a step in one launch (mask bank): desc rows {seed slot,
+ * elements, first 32-bit word} (int64, sorted by first word, <= 64 sites); site s
+ * writes the keep bits of its elements [0, n_s) (seed seeds[slot_s]) from word
+ * first_s of `base` (4-byte aligned, bit i&31 of word i>>5), zero past n_s.
+ * stamp/want (optional device scalars): nothing is drawn when *stamp == *want
+ * (the bits of that step were already drawn, e.g. beside the previous Adam). */
+int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
+                           const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
+                           const int64_t* want, void* stream);
 int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream);
 int ls2_dense_to_bits(const void* dense, int dtype, uint8_t* bits, int64_t n, void* stream);
 
@@ -112,6 +121,7 @@ int ls2_layernorm_bwd(const void* dy, const void* x, const void* w, const void* 
 
 /* fused bias+dropout+residual -> LayerNorm (F/kernels.py:367-382 then :235-270):
  * yres = keep*(x+bias)*dscale + res (stored), u = LN(yres) with (mu, sigma);
+ * use_drop: 0 none, 1 draw keep bits into keep_bits, 2 read keep_bits (mask bank);
  * needs cols % 8 == 0, cols <= 1024, 16-byte aligned operands (else LS2_ERR_SHAPE). */
 int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void* yres,
                           uint8_t* keep_bits, const void* w, const void* b, void* u, void* mu,

@@ -36,6 +36,38 @@ __global__ void dropout_bits_kernel(uint8_t* bits, int64_t n, uint64_t seed, con
   }
 }
 
+// Every dropout site of a step in one launch (the mask bank).  desc rows
+// {seed slot, elements, first 32-bit word} (int64), sorted by first word;
+// site s fills words [first_s, first_s + ceil(n_s/32)) of `words` with the
+// keep bits of elements [0, n_s) drawn with seed seeds[slot_s] (bits past n_s
+// are 0).  One thread per 32-element word, grid-stride, coalesced 4-byte stores.
+__global__ void __launch_bounds__(256) dropout_bits_multi_kernel(
+    const int64_t* __restrict__ desc, int nsites, int64_t total_words, uint32_t* __restrict__ words,
+    const uint64_t* __restrict__ seeds, uint64_t thresh, const int64_t* __restrict__ stamp,
+    const int64_t* __restrict__ want) {
+  if (stamp && want && *stamp == *want) return;    // bits already drawn for this step
+  __shared__ int64_t s_first[65];
+  __shared__ int64_t s_n[64];
+  __shared__ uint64_t s_seed[64];
+  for (int i = threadIdx.x; i < nsites; i += blockDim.x) {
+    s_first[i] = desc[4 * i + 2];
+    s_n[i] = desc[4 * i + 1];
+    s_seed[i] = seeds[desc[4 * i]];
+  }
+  if (threadIdx.x == 0) s_first[nsites] = total_words;
+  __syncthreads();
+  int site = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total_words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    while (w >= s_first[site + 1]) ++site;           // w only grows: sites in order
+    const int64_t e0 = (w - s_first[site]) * 32;
+    uint32_t b = keep_bits_n<32>(s_seed[site], (uint64_t)e0, thresh);
+    const int64_t valid = s_n[site] - e0;
+    if (valid < 32) b &= valid <= 0 ? 0u : ((1u << valid) - 1u);
+    words[w] = b;
+  }
+}
+
 template <typename T>
 __global__ void bits_to_dense_kernel(const uint8_t* bits, T* dense, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -79,6 +111,25 @@ int ls2_dropout_bits(uint8_t* bits, int64_t n, uint64_t seed, const uint64_t* se
   dropout_bits_kernel<<<grid_for(ceil_div(n, 8)), 256, 0, as_stream(stream)>>>(bits, n, seed, seed_ptr,
                                                                                 thresh);
   return check_launch("dropout_bits");
+}
+
+int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
+                           const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
+                           const int64_t* want, void* stream) {
+  if (total_words <= 0 || nsites <= 0) return LS2_OK;
+  if (nsites > 64) return fail(LS2_ERR_SHAPE, "dropout_bits_multi: at most 64 sites");
+  if ((reinterpret_cast<uintptr_t>(base) & 3) != 0)
+    return fail(LS2_ERR_SHAPE, "dropout_bits_multi: base must be 4-byte aligned");
+  static int grid = 0;
+  if (!grid) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dropout_bits_multi_kernel, 256, 0);
+    grid = kNumSMs * (per > 0 ? per : 8);
+  }
+  const int g = (int)std::min<int64_t>(grid, ceil_div(total_words, (int64_t)256));
+  dropout_bits_multi_kernel<<<g, 256, 0, as_stream(stream)>>>(
+      desc, nsites, total_words, reinterpret_cast<uint32_t*>(base), seeds, thresh, stamp, want);
+  return check_launch("dropout_bits_multi");
 }
 
 int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream) {

@@ -160,6 +160,74 @@ __global__ void emb_bwd_pos(const Tin* __restrict__ dy, const uint8_t* __restric
   }
 }
 
+// Positional-table gradient, vectorised: one CTA per position l; its 256
+// threads are (d/8 column groups) x (batch groups).  Each thread sums its batch
+// group for 8 columns with 16-byte loads issued ahead of the (sequential)
+// adds, then the batch-group partials are folded in fixed order through shared
+// memory.  Deterministic; positions >= len get 0 (or keep dP when beta).
+template <typename Tin, typename Tg, bool DROP>
+__global__ void __launch_bounds__(256) emb_bwd_pos_vec(
+    const Tin* __restrict__ dy, const uint8_t* __restrict__ bits, Tg* __restrict__ dP,
+    int64_t batch, int64_t len, int64_t d, Tg ds, int beta) {
+  __shared__ Tg part[256 * 8];
+  const int64_t l = blockIdx.x;
+  const int cgs = (int)(d / 8);
+  const int ngrp = 256 / cgs;                  // batch groups
+  const int cg = threadIdx.x % cgs, grp = threadIdx.x / cgs;
+  Tg* out = dP + l * d + cg * 8;
+  if (l >= len) {
+    if (!beta && grp == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) out[e] = (Tg)0;
+    }
+    return;
+  }
+  Tg acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = (Tg)0;
+  if (grp < ngrp) {
+    const int64_t per = (batch + ngrp - 1) / ngrp;
+    const int64_t b0 = grp * per, b1 = min(batch, b0 + per);
+    constexpr int U = 8;
+    for (int64_t bb = b0; bb < b1; bb += U) {
+      Pack8<Tin> v[U];
+      uint32_t kb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (bb + u < b1) {
+          const int64_t k = ((bb + u) * len + l) * d + cg * 8;
+          v[u] = ld8(dy + k);
+          kb[u] = DROP ? bits[k >> 3] : 0xFFu;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (bb + u < b1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            Tg a = cvt<Tg>(v[u].v[e]);
+            if (DROP) a = mul_rn(mul_rn(a, (Tg)((kb[u] >> e) & 1)), ds);
+            acc[e] = add_rn(acc[e], a);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) part[threadIdx.x * 8 + e] = acc[e];
+  __syncthreads();
+  if (grp == 0) {
+    Tg s[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e] = beta ? out[e] : (Tg)0;
+    for (int g2 = 0; g2 < ngrp; ++g2)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = add_rn(s[e], part[(g2 * cgs + cg) * 8 + e]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) out[e] = s[e];
+  }
+}
+
 inline bool vec8(int64_t d, std::initializer_list<const void*> ptrs) {
   if (d % 8 != 0 || d / 8 > 1024) return false;
   for (const void* p : ptrs)
@@ -244,6 +312,15 @@ int ls2_embedding_bwd(const void* dy, const int64_t* tokens, const uint8_t* keep
       if (r) return r;
     }
     if (dP) {
+      if (vec8(d, {dy, dP}) && d / 8 <= 256 && sizeof(Tg) == 4) {
+        if (use_drop)
+          emb_bwd_pos_vec<Tin, Tg, true><<<(unsigned)max_len, 256, 0, st>>>(
+              (const Tin*)dy, keep_bits, (Tg*)dP, batch, len, d, ds, beta_pos);
+        else
+          emb_bwd_pos_vec<Tin, Tg, false><<<(unsigned)max_len, 256, 0, st>>>(
+              (const Tin*)dy, keep_bits, (Tg*)dP, batch, len, d, ds, beta_pos);
+        return check_launch("embedding_bwd_pos");
+      }
       if (use_drop)
         emb_bwd_pos<Tin, Tg, true><<<grid_for(max_len * d), 256, 0, st>>>(
             (const Tin*)dy, keep_bits, (Tg*)dP, batch, len, d, max_len, ds, beta_pos);

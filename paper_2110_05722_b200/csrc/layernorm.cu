@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_warp(
 //   u    = LN(yres)  with (mu, sigma) cached.
 // The LayerNorm consumes the stored (rounded) yres, so results equal the
 // unfused pair exactly; one launch and one pass instead of two.
-template <typename Tin, typename Tout, typename Tstat, int ITERS, bool DROP>
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool DROP, bool GEN = true>
 __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
     const Tin* __restrict__ x, const Tin* __restrict__ bias, const Tin* __restrict__ res,
     Tout* __restrict__ yres, uint8_t* __restrict__ bits, const Tin* __restrict__ w,
@@ -141,8 +141,12 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
         ld_group(res + r * cols + g * 8, rv);
         uint32_t kb = 0xFF;
         if (DROP) {
-          kb = keep_byte(seed, (uint64_t)(r * cgs + g) * 8, thresh);
-          bits[r * cgs + g] = (uint8_t)kb;
+          if (GEN) {
+            kb = keep_byte(seed, (uint64_t)(r * cgs + g) * 8, thresh);
+            bits[r * cgs + g] = (uint8_t)kb;
+          } else {
+            kb = bits[r * cgs + g];      // precomputed by the mask bank
+          }
         }
         Pack8<Tout> q;
         const Pack8<Tin> cq = sc[g];
@@ -704,13 +708,13 @@ int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void
   return LS2_DISPATCH_IO(tin, tout, "bdr_layernorm_fwd", [&] {
     return LS2_DISPATCH_STAT(tstat, [&] {
       using C = typename CompOf<Tin>::type;
-      auto go = [&](auto iters, auto drop) {
+      auto go = [&](auto iters, auto drop, auto genc) {
         constexpr int I = decltype(iters)::value;
-        constexpr bool D = decltype(drop)::value;
+        constexpr bool D = decltype(drop)::value, G = decltype(genc)::value;
         const size_t psm = 3 * (size_t)cols * sizeof(Tin);
-        const int grid = resident_grid((const void*)ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D>,
+        const int grid = resident_grid((const void*)ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D, G>,
                                        kLnWarps * 32, psm, ceil_div(rows, kLnWarps));
-        ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D><<<grid, kLnWarps * 32, psm, st>>>(
+        ln_fwd_bdr_warp<Tin, Tout, Tstat, I, D, G><<<grid, kLnWarps * 32, psm, st>>>(
             (const Tin*)x, (const Tin*)bias, (const Tin*)res, (Tout*)yres, keep_bits,
             (const Tin*)w, (const Tin*)b, (Tout*)u, (Tstat*)mu, (Tstat*)sigma, rows, cols, eps,
             seed, seed_ptr, thresh, (C)dscale);
@@ -722,8 +726,11 @@ int ls2_bdr_layernorm_fwd(const void* x, const void* bias, const void* res, void
       using T_ = std::true_type;
       using F_ = std::false_type;
       const int it = ln_iters(cols);
-      if (use_drop) return it == 1 ? go(I1{}, T_{}) : it == 2 ? go(I2{}, T_{}) : go(I4{}, T_{});
-      return it == 1 ? go(I1{}, F_{}) : it == 2 ? go(I2{}, F_{}) : go(I4{}, F_{});
+      if (use_drop == 2)      // read the keep bits (mask bank)
+        return it == 1 ? go(I1{}, T_{}, F_{}) : it == 2 ? go(I2{}, T_{}, F_{}) : go(I4{}, T_{}, F_{});
+      if (use_drop)
+        return it == 1 ? go(I1{}, T_{}, T_{}) : it == 2 ? go(I2{}, T_{}, T_{}) : go(I4{}, T_{}, T_{});
+      return it == 1 ? go(I1{}, F_{}, T_{}) : it == 2 ? go(I2{}, F_{}, T_{}) : go(I4{}, F_{}, T_{});
     });
   });
 }

@@ -27,7 +27,7 @@ from .data import make_task
 from .dist import DataParallel
 from .errors import DataError
 from .memplan import PlannedArena, RecordingArena, TensorTag, classify, estimate_capacity
-from .model import Batch, Transformer, _ViewSink, validate_batch
+from .model import Batch, MaskBank, SeedTable, Transformer, _ViewSink, validate_batch
 from .trainer import OptimConfig, Workspace, _state, workspace_pack
 
 EVAL_STEP_BASE = 1 << 30
@@ -142,6 +142,13 @@ class TrainingEngine:
         # by default: measured 1% slower at T-base, because the one-wave fused
         # kernels cannot co-reside with a concurrent GEMM's CTAs
         self.use_lane = os.environ.get("LS2_WGRAD_LANE", "0") == "1"
+        # every forward dropout site of a step drawn by one launch (model.MaskBank)
+        self.masks = MaskBank(self.device) if os.environ.get("LS2_MASK_BANK", "1") != "0" else None
+        # next step's site seeds: the bank draws step t+1's bits beside step t's Adam
+        self._seeds_next = SeedTable(self.device)
+        # off by default: measured slower at T-base (Adam's bit-exact IEEE div/sqrt
+        # keep its SMs' ALUs busy, so the draw does not hide beside it)
+        self._early_masks = os.environ.get("LS2_EARLY_MASKS", "0") == "1"
         self.last_out3 = None
 
     # -- arena setup (F/engine.py:89-103) ----------------------------------------------
@@ -158,12 +165,17 @@ class TrainingEngine:
         self.model.forward_backward(self.pviews, batch,
                                     p_drop=self.cfg.train.p_drop if compute_grads else 0.0,
                                     alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
-                                    step=0, arena=rec, sink=sink, compute_grads=compute_grads)
+                                    step=0, arena=rec, sink=sink, compute_grads=compute_grads,
+                                    masks=self.masks)
         return rec.finish()
 
     def setup_arena(self) -> int:
         """Dry-run every bucket shape, size the arena once (bytes), register plans."""
         recorded = {}
+        if self.masks is not None:
+            shapes = list(self.task.possible_shapes())
+            mt = max(b * l for b, l in shapes)
+            self.masks.configure(mt, mt)
         for b, l in self.task.possible_shapes():
             batch = self._dummy_batch(b, l)
             recorded[("train", b, l)] = self._record_shape(batch, True)
@@ -193,10 +205,22 @@ class TrainingEngine:
             io = self._io[(b, l)] = _StaticIO(b, l, self.device)
         return io
 
+    def _stage_next_seeds(self, step: int):
+        """Host: the site seeds of step+1 into the next-step table's staging buffer."""
+        t = self.cfg.train
+        self.model.register_seeds(self._seeds_next, t.seed, step + 1, t.p_drop)
+        self._seeds_next.write_host(sync=False)
+
     def _fwd_bwd(self, io: _StaticIO, key, step: int, upload: bool = True):
         t = self.cfg.train
         if upload:
             io.upload()
+            if self.masks is not None and t.p_drop > 0.0:
+                if not torch.cuda.is_current_stream_capturing():
+                    self._stage_next_seeds(step)
+                nx = self._seeds_next
+                n = len(nx.values)
+                nx.dev[:n].copy_(nx.host[:n], non_blocking=True)
         self.arena.begin(key)
         sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
         if self.dp.active:
@@ -209,7 +233,7 @@ class TrainingEngine:
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
             arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
-            upload_seeds=upload)
+            upload_seeds=upload, masks=self.masks)
         self.arena.end()
         return out.out3, sink
 
@@ -274,6 +298,28 @@ class TrainingEngine:
             _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr() + 2 * start, stop - start,
                       self._nonfinite.data_ptr(), cs.cuda_stream)
 
+    def _draw_next_masks(self, uploaded: bool):
+        """Beside the optimizer pass (HBM-bound, half the SM slots), draw the next
+        step's dropout bits on the side stream and stamp them; returns the event
+        the step's end must wait on.  The device-resident benchmark graph keeps
+        its seeds, so it redraws the same step (same work)."""
+        bank = self.masks
+        if bank is None or bank.desc is None or not self._early_masks or \
+                self.cfg.train.p_drop <= 0.0:
+            return None
+        tbl = self._seeds_next if uploaded else self.model.seed_table(self.device)
+        side = _lib.context().side_stream
+        main = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            bank.generate(tbl.dev)
+            bank.stamp.copy_(tbl.step_slot())
+        done = torch.cuda.Event()
+        done.record(side)
+        return done
+
     def _finish_deferred(self, sink, out3, nonfinite_ptr, entries=None):
         """One launch finishing every deferred bias / LayerNorm gradient (partials
         left by their producers) straight into the fp16 workspace."""
@@ -313,6 +359,7 @@ class TrainingEngine:
                       float(1.0 / t.act_grad_scale), self._nonfinite.data_ptr(), st)
             self._finish_deferred(sink, out3, self._nonfinite.data_ptr())
         loss_ptr = out3.data_ptr()
+        joined = self._draw_next_masks(host_copy)
         if self.optim.algorithm == "adam":
             _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
                       ws.m32.data_ptr(), ws.v32.data_ptr(), ws.n_elements,
@@ -325,6 +372,8 @@ class TrainingEngine:
                       loss_ptr, st)
         _lib.call("ls2_step_commit", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
                   loss_ptr, self._flag.data_ptr(), st)
+        if joined is not None:
+            torch.cuda.current_stream().wait_event(joined)
         self._dev_out[0:3].copy_(out3)
         self._dev_out[3].copy_(self._flag[0])
         self._dev_out[4].copy_(self._nonfinite[0])
@@ -352,11 +401,14 @@ class TrainingEngine:
         torch.cuda.synchronize()
 
     def refresh_seeds(self, step: int):
-        """Write this step's per-site dropout seeds into the pinned staging buffer."""
+        """Write this step's per-site dropout seeds (and the next step's, for the
+        mask bank) into the pinned staging buffers."""
         t = self.cfg.train
         seeds = self.model.seed_table(self.device)
         self.model.register_seeds(seeds, t.seed, step, t.p_drop)
         seeds.write_host()
+        if self.masks is not None and t.p_drop > 0.0:
+            self._stage_next_seeds(step)
 
     def train_step(self, step: int, trace=None) -> StepMetrics:
         t0 = time.perf_counter()

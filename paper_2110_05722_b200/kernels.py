@@ -314,9 +314,11 @@ def check_tokens(tokens, vocab: int, max_len: int | None = None):
 
 
 def embedding_forward(emb, pos, tokens, cfg: EmbeddingConfig, p_drop: float, seed: int,
-                      out=None, keep_out=None, bits_out=None, validate: bool = True):
+                      out=None, keep_out=None, bits_out=None, validate: bool = True,
+                      mask: DropoutMask | None = None):
     """y[b,i,:] = keep * (s * emb[tokens[b,i],:] + pos[i,:]) / (1 - p).
 
+    mask: reuse an existing mask's bits instead of drawing them (injected masks).
     Returns ([B, L, d], DropoutMask)."""
     tk = check_tokens(tokens, cfg.vocab, cfg.max_len) if validate else tokens
     b, l = tk.shape
@@ -326,13 +328,18 @@ def embedding_forward(emb, pos, tokens, cfg: EmbeddingConfig, p_drop: float, see
     y, orig = _out(out, (b, l, d), tout, e.device)
     use, thresh, ds = _drop_args(p_drop)
     n = b * l * d
-    bits = bits_out if bits_out is not None else (_new_bits(n, e.device) if use else None)
+    gen = 1
+    if mask is not None and use:
+        bits, gen = mask.bitmask(), 0
+    else:
+        bits = bits_out if bits_out is not None else (_new_bits(n, e.device) if use else None)
     _lib.call("ls2_embedding_fwd", e.data_ptr(), p.data_ptr(), tk.data_ptr(), y.data_ptr(),
-              _lib.ptr(bits), None, b, l, d, cfg.vocab, float(cfg.scale), use, 1,
+              _lib.ptr(bits), None, b, l, d, cfg.vocab, float(cfg.scale), use, gen,
               *_seed_args(seed), thresh, ds, _lib.dtype_code(tin), _lib.dtype_code(tout),
               _lib.stream_handle())
     y = _finish(y, orig)
-    mask = DropoutMask(p=p_drop, bits=bits, shape=(b, l, d), dense_dtype=tout)
+    if mask is None or not use:
+        mask = DropoutMask(p=p_drop, bits=bits, shape=(b, l, d), dense_dtype=tout)
     if keep_out is not None:
         _fill_keep(keep_out, mask)
         mask.keep = keep_out

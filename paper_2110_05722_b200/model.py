@@ -611,6 +611,23 @@ class SeedTable:
         self.index.clear()
         self.values.clear()
 
+    def set_step(self, step: int):
+        """Slot 0 holds the step number (the mask bank's stamp compares with it)."""
+        self.slot_value("__step__", step)
+
+    def step_slot(self):
+        return self.slot_value("__step__", None)
+
+    def slot_value(self, name: str, value):
+        key = (name,)
+        i = self.index.get(key)
+        if i is None:
+            i = self.index[key] = len(self.values)
+            self.values.append(0 if value is None else value)
+        elif value is not None:
+            self.values[i] = value
+        return self.dev[i:i + 1]
+
     def slot(self, base: int, *tags: int):
         key = (base,) + tags
         i = self.index.get(key)
@@ -655,6 +672,103 @@ def _site_seed(seed, site: int, k: int):
     return derive_seed(seed, site, k)
 
 
+class MaskBank:
+    """Keep bits of every forward dropout site of a step, drawn by ONE launch.
+
+    The reference draws each site's mask inside its op (F/kernels.py:155-166,
+    splitmix64 per element).  Drawing all of a step's sites with one
+    ALU-dense ls2_dropout_bits_multi launch turns the memory-bound fused
+    forward kernels (bias+ReLU+dropout, bias+dropout+residual(+LayerNorm),
+    embedding) into pure streams that read 1 bit per element; the bits are
+    identical.  Keep bit i of a site depends only on (site seed, i), so each
+    site owns a fixed region sized for the largest batch shape and any shape
+    reads a prefix: one layout for every bucket.
+
+    The draw runs at the start of the step.  Optionally (LS2_EARLY_MASKS=1) the
+    engine draws step t+1's bits beside step t's Adam and stamps them with t+1;
+    step t+1 then finds stamp == its step and its in-step draw exits at once
+    (any other order — first step, a skipped step number — draws in-step).  Sites are keyed
+    by their seed slot in the step's SeedTable; the backward pass reads the
+    same bits again.  The buffer lives outside the activation arena.
+    """
+
+    def __init__(self, device):
+        self.device = device
+        self.buf = None
+        self.desc = None
+        self.nsites = 0
+        self.words = 0
+        self.sites: dict = {}
+        self.max_tokens = None            # (src, tgt) tokens of the largest batch shape
+        self.stamp = torch.full((1,), -1, dtype=torch.int64, device=device)
+        self.thresh = 0
+        self.active = False
+
+    def configure(self, max_src_tokens: int, max_tgt_tokens: int):
+        self.max_tokens = (int(max_src_tokens), int(max_tgt_tokens))
+
+    def prepare(self, sites_fn, src_tokens: int, tgt_tokens: int, thresh: int):
+        """Lay the sites out once (sites_fn(src_tokens, tgt_tokens) -> [(slot, n)])."""
+        if self.max_tokens is None:
+            self.max_tokens = (src_tokens, tgt_tokens)
+        if src_tokens > self.max_tokens[0] or tgt_tokens > self.max_tokens[1]:
+            raise ShapeMismatch("batch larger than the mask bank's configured maximum")
+        if self.desc is None:
+            rows, woff, offs = [], 0, {}
+            for slot, n in sites_fn(*self.max_tokens):
+                rows.append([slot, n, woff, 0])
+                offs[slot] = 4 * woff
+                woff += ((n + 31) // 32 + 3) // 4 * 4        # 16-byte aligned sites
+            self.desc = torch.tensor(rows, dtype=torch.int64, device=self.device)
+            self.nsites, self.words, self.sites = len(rows), woff, offs
+            self.buf = torch.zeros(4 * woff, dtype=torch.uint8, device=self.device)
+        self.thresh = thresh
+
+    def generate(self, seeds_dev: torch.Tensor, stamp=None, want=None):
+        """Draw every site with the seeds in seeds_dev (skipped on the device
+        when *stamp == *want)."""
+        _lib.call("ls2_dropout_bits_multi", self.desc.data_ptr(), self.nsites, self.words,
+                  self.buf.data_ptr(), seeds_dev.data_ptr(), self.thresh, _lib.ptr(stamp),
+                  _lib.ptr(want), _lib.stream_handle())
+
+    def bits(self, seed, n: int):
+        """Bank view for the site whose seed is the table slot `seed`, else None."""
+        if not self.active or not isinstance(seed, torch.Tensor):
+            return None
+        off = self.sites.get(seed.storage_offset())
+        return None if off is None else self.buf[off:off + _nbits(n)]
+
+    def owns(self, t) -> bool:
+        if self.buf is None:
+            return False
+        p = t.data_ptr()
+        return self.buf.data_ptr() <= p < self.buf.data_ptr() + self.buf.numel()
+
+
+_MASKS: MaskBank | None = None       # the bank of the forward_backward in flight
+
+
+def _bank_bits(seed, n: int):
+    return _MASKS.bits(seed, n) if _MASKS is not None else None
+
+
+class _BankArena:
+    """Arena facade: bank views are not arena blocks, their frees are no-ops."""
+
+    def __init__(self, arena, bank: MaskBank):
+        self._arena, self._bank = arena, bank
+
+    def alloc(self, shape, dtype):
+        return self._arena.alloc(shape, dtype)
+
+    def free(self, t):
+        if not self._bank.owns(t):
+            self._arena.free(t)
+
+    def __getattr__(self, name):
+        return getattr(self._arena, name)
+
+
 def _stat_dtype(dt):
     return torch.float64 if dt == torch.float64 else torch.float32
 
@@ -687,7 +801,8 @@ def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p
     r, dt = b * l, proj.dtype
     sdt = _stat_dtype(dt)
     y = arena.alloc((b, l, d), dt)
-    keep = arena.alloc((_nbits(r * d),), torch.uint8)
+    banked = _bank_bits(seed, r * d) if p_drop > 0.0 else None
+    keep = banked if banked is not None else arena.alloc((_nbits(r * d),), torch.uint8)
     mu, sg = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
     u = arena.alloc((b, l, d), dt)
     bb, lw, lb = _as_dt(bias, dt), _as_dt(ln_w, dt), _as_dt(ln_b, dt)
@@ -696,9 +811,15 @@ def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p
         sv, sp = K._seed_args(seed)
         _lib.call("ls2_bdr_layernorm_fwd", proj.data_ptr(), bb.data_ptr(), res.data_ptr(),
                   y.data_ptr(), keep.data_ptr(), lw.data_ptr(), lb.data_ptr(), u.data_ptr(),
-                  mu.data_ptr(), sg.data_ptr(), r, d, float(eps), use, sv, sp, thresh, ds,
+                  mu.data_ptr(), sg.data_ptr(), r, d, float(eps),
+                  2 if (use and banked is not None) else use, sv, sp, thresh, ds,
                   _lib.dtype_code(dt), _lib.dtype_code(dt), _lib.dtype_code(sdt),
                   _lib.stream_handle())
+    elif banked is not None:
+        K.bias_dropout_residual(proj, bb, res, p_drop, seed, out=y,
+                                mask=DropoutMask(p=p_drop, bits=keep, shape=(b, l, d)))
+        K.layernorm_forward(y, lw, lb, eps, out=u, mu_out=mu, sigma_out=sg,
+                            check_degenerate=False)
     else:
         K.bias_dropout_residual(proj, bb, res, p_drop, seed, out=y, bits_out=keep)
         K.layernorm_forward(y, lw, lb, eps, out=u, mu_out=mu, sigma_out=sg,
@@ -752,18 +873,25 @@ def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p):
     a1 = arena.alloc((b, l, dff), dt)
     _linear(u.view(r, d), w.w1, None, a1.view(r, dff))
     z = arena.alloc((b, l, dff), dt)
-    keep_r = arena.alloc((_nbits(r * dff),), torch.uint8)
+    s_relu = _site_seed(seed, site, k_relu)
+    banked = _bank_bits(s_relu, r * dff) if p_drop > 0.0 else None
+    keep_r = banked if banked is not None else arena.alloc((_nbits(r * dff),), torch.uint8)
     relum = arena.alloc((_nbits(r * dff),), torch.uint8)
-    K.bias_relu_dropout(a1, _as_dt(w.b1, dt), p_drop, _site_seed(seed, site, k_relu), out=z,
-                        bits_out=keep_r, relu_bits_out=relum)
+    K.bias_relu_dropout(a1, _as_dt(w.b1, dt), p_drop, s_relu, out=z, bits_out=keep_r,
+                        relu_bits_out=relum,
+                        mask=None if banked is None else
+                        DropoutMask(p=p_drop, bits=keep_r, shape=(b, l, dff)))
     arena.free(a1)
     stash.push(p + "keepr", keep_r); stash.push(p + "relum", relum); stash.push(p + "z", z)
     f = arena.alloc((b, l, d), dt)
     _linear(z.view(r, dff), w.w2, None, f.view(r, d))
     y2 = arena.alloc((b, l, d), dt)
-    keep_t = arena.alloc((_nbits(r * d),), torch.uint8)
-    K.bias_dropout_residual(f, _as_dt(w.b2, dt), y_in, p_drop, _site_seed(seed, site, k_tail),
-                            out=y2, bits_out=keep_t)
+    s_tail = _site_seed(seed, site, k_tail)
+    banked = _bank_bits(s_tail, r * d) if p_drop > 0.0 else None
+    keep_t = banked if banked is not None else arena.alloc((_nbits(r * d),), torch.uint8)
+    K.bias_dropout_residual(f, _as_dt(w.b2, dt), y_in, p_drop, s_tail, out=y2, bits_out=keep_t,
+                            mask=None if banked is None else
+                            DropoutMask(p=p_drop, bits=keep_t, shape=(b, l, d)))
     arena.free(f)
     stash.push(p + "keept", keep_t)
     return y2
@@ -1156,6 +1284,7 @@ class Transformer:
         (F/model.py:868-898 seed derivations: (seed,step,0..3), then site, k)."""
         cfg = self.cfg
         seeds.reset()
+        seeds.set_step(step)
         s_src = seeds.slot(derive_seed(seed, step, 0))
         enc_seed = _LayerSeed(seeds, derive_seed(seed, step, 1))
         s_tgt = seeds.slot(derive_seed(seed, step, 2))
@@ -1172,11 +1301,49 @@ class Transformer:
     def forward_backward(self, params, batch: Batch, *, p_drop=0.0, alpha=0.0, seed=0, step=0,
                          arena=None, sink: GradSink | None = None, compute_grads=True,
                          grad_scale=1.0, trace=None, strategy=None, capture: dict | None = None,
-                         validate: bool = True, upload_seeds: bool = True) -> ModelOutput:
+                         validate: bool = True, upload_seeds: bool = True,
+                         masks: MaskBank | None = None) -> ModelOutput:
         """Run one batch end to end; gradients go into `sink`.
 
         grad_scale multiplies the criterion gradient.  compute_grads=False is a
-        pure forward (evaluation).  capture receives "logq" (debug hook)."""
+        pure forward (evaluation).  capture receives "logq" (debug hook).
+        masks: a MaskBank drawing every forward dropout site in one launch."""
+        global _MASKS
+        if masks is None:
+            return self._forward_backward(params, batch, p_drop=p_drop, alpha=alpha, seed=seed,
+                                          step=step, arena=arena, sink=sink,
+                                          compute_grads=compute_grads, grad_scale=grad_scale,
+                                          trace=trace, strategy=strategy, capture=capture,
+                                          validate=validate, upload_seeds=upload_seeds)
+        _MASKS = masks
+        try:
+            return self._forward_backward(params, batch, p_drop=p_drop, alpha=alpha, seed=seed,
+                                          step=step, arena=arena, sink=sink,
+                                          compute_grads=compute_grads, grad_scale=grad_scale,
+                                          trace=trace, strategy=strategy, capture=capture,
+                                          validate=validate, upload_seeds=upload_seeds)
+        finally:
+            masks.active = False
+            _MASKS = None
+
+    def _mask_sites(self, s_src, enc_seed, s_tgt, dec_seed, ts: int, tt: int):
+        """(seed slot, elements) of every forward dropout site, in consumption
+        order, for ts source and tt target tokens."""
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        slot = lambda t: t.storage_offset()      # noqa: E731
+        sites = [(slot(s_src), ts * d)]
+        for i in range(self.cfg.n_enc):
+            sites += [(slot(enc_seed.site(i, 0)), ts * d), (slot(enc_seed.site(i, 1)), ts * f),
+                      (slot(enc_seed.site(i, 2)), ts * d)]
+        sites.append((slot(s_tgt), tt * d))
+        for i in range(self.cfg.n_dec):
+            sites += [(slot(dec_seed.site(i, 0)), tt * d), (slot(dec_seed.site(i, 1)), tt * d),
+                      (slot(dec_seed.site(i, 2)), tt * f), (slot(dec_seed.site(i, 3)), tt * d)]
+        return sites
+
+    def _forward_backward(self, params, batch: Batch, *, p_drop, alpha, seed, step, arena, sink,
+                          compute_grads, grad_scale, trace, strategy, capture, validate,
+                          upload_seeds) -> ModelOutput:
         cfg = self.cfg
         ctx = _lib.context()
         arena = arena or NullArena(ctx.device)
@@ -1209,12 +1376,26 @@ class Transformer:
         s_src, enc_seed, s_tgt, dec_seed = self.register_seeds(seeds, seed, step, p_drop)
         if p_drop > 0.0 and upload_seeds:
             seeds.upload()
+        bank = _MASKS
+        if bank is not None and p_drop > 0.0 and dt != torch.float64:
+            # every forward dropout site of the step in one launch (a no-op on the
+            # device when the bits were drawn beside the previous step's Adam)
+            bank.prepare(lambda ts, tt: self._mask_sites(s_src, enc_seed, s_tgt, dec_seed, ts, tt),
+                         b * ls, b * lt, K._drop_args(p_drop)[1])
+            bank.generate(seeds.dev, stamp=bank.stamp, want=seeds.step_slot())
+            bank.active = True
+            arena = _BankArena(arena, bank)
 
         # --- forward: encoder ---
         h = arena.alloc((b, ls, d), dt)
-        keep_src = arena.alloc((_nbits(b * ls * d),), torch.uint8)
+        keep_src = _bank_bits(s_src, b * ls * d) if p_drop > 0.0 else None
+        banked = keep_src is not None
+        if not banked:
+            keep_src = arena.alloc((_nbits(b * ls * d),), torch.uint8)
         K.embedding_forward(tok_emb, pos, src, emb_cfg, p_drop, s_src, out=h, bits_out=keep_src,
-                            validate=False)
+                            validate=False,
+                            mask=DropoutMask(p=p_drop, bits=keep_src, shape=(b, ls, d)) if banked
+                            else None)
         stash.push("src_keep", keep_src)
         enc_w = [EncoderLayerWeights.from_params(params, f"enc{i}.") for i in range(cfg.n_enc)]
         for i in range(cfg.n_enc):
@@ -1234,9 +1415,14 @@ class Transformer:
 
         # --- forward: decoder ---
         g = arena.alloc((b, lt, d), dt)
-        keep_tgt = arena.alloc((_nbits(b * lt * d),), torch.uint8)
+        keep_tgt = _bank_bits(s_tgt, b * lt * d) if p_drop > 0.0 else None
+        banked = keep_tgt is not None
+        if not banked:
+            keep_tgt = arena.alloc((_nbits(b * lt * d),), torch.uint8)
         K.embedding_forward(tok_emb, pos, tgt_in, emb_cfg, p_drop, s_tgt, out=g,
-                            bits_out=keep_tgt, validate=False)
+                            bits_out=keep_tgt, validate=False,
+                            mask=DropoutMask(p=p_drop, bits=keep_tgt, shape=(b, lt, d)) if banked
+                            else None)
         stash.push("tgt_keep", keep_tgt)
         dec_w = [DecoderLayerWeights.from_params(params, f"dec{i}.") for i in range(cfg.n_dec)]
         for i in range(cfg.n_dec):

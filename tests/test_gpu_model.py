@@ -313,3 +313,31 @@ def test_dp_exchange_tbase_graph_step():
         assert abs(a.loss - b.loss) <= 1e-3 * abs(a.loss)
     p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
     assert np.abs(p1 - p2).max() <= 2e-3
+
+
+def _run_steps(steps, graphs=True):
+    run = RunConfig()
+    run.train.p_drop = 0.1
+    run.train.cuda_graphs = graphs
+    eng = TrainingEngine(run)
+    eng.setup_arena()
+    return eng, [eng.train_step(s) for s in steps]
+
+
+@pytest.mark.parametrize("graphs,early", [(True, "1"), (False, "1"), (True, "0")])
+def test_mask_bank_step_equals_inline_masks(monkeypatch, graphs, early):
+    """Engine with the mask bank (every site drawn by one launch, step t+1's bits
+    drawn beside step t's Adam) vs inline drawing: same masks, so the same
+    losses; parameters equal up to embedding atomics.  The step sequence has
+    gaps, so both the early draw and the in-step fallback are exercised."""
+    steps = [0, 1, 2, 5, 6, 7, 9]
+    monkeypatch.setenv("LS2_MASK_BANK", "0")
+    e1, m1 = _run_steps(steps, graphs)
+    monkeypatch.setenv("LS2_MASK_BANK", "1")
+    monkeypatch.setenv("LS2_EARLY_MASKS", early)
+    e2, m2 = _run_steps(steps, graphs)
+    assert e1.masks is None and e2.masks is not None and e2.masks.buf is not None
+    for a, b in zip(m1, m2):
+        assert abs(a.loss - b.loss) <= 1e-5 * max(1.0, abs(a.loss)), (a.step, a.loss, b.loss)
+    p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
+    assert np.abs(p1 - p2).max() <= 2e-3

@@ -427,3 +427,62 @@ def test_gemm_known_and_errors():
     assert np.array_equal(H(c), [[19.0, 22.0], [43.0, 50.0]])
     with pytest.raises(ShapeMismatch):
         K.gemm(C(np.zeros((2, 3))), C(np.zeros((4, 2))))
+
+
+# --- mask bank: every site of a step in one launch ------------------------------------
+
+def test_dropout_bits_multi_matches_reference_rng():
+    """ls2_dropout_bits_multi == the reference's per-site masks, bit for bit
+    (ragged site sizes, sites packed at 16-byte offsets, zero padding)."""
+    from paper_2110_05722_b200 import _lib
+    sizes = [4096 * 512, 1000, 33, 4096 * 2048 + 7, 1, 64 * 64 * 512]
+    seeds = [(1 << 63) + 12345, 7, 99, 2 ** 64 - 1, 0, 424242]
+    p = 0.1
+    thr = K._drop_args(p)[1]
+    rows, woff = [], 0
+    for i, n in enumerate(sizes):
+        rows.append([i, n, woff, 0])
+        woff += ((n + 31) // 32 + 3) // 4 * 4
+    desc = torch.tensor(rows, dtype=torch.int64, device="cuda")
+    sd = torch.tensor([s - (1 << 64) if s >= (1 << 63) else s for s in seeds], dtype=torch.int64,
+                      device="cuda")
+    buf = torch.full((4 * woff,), 0xAB, dtype=torch.uint8, device="cuda")
+    _lib.call("ls2_dropout_bits_multi", desc.data_ptr(), len(sizes), woff, buf.data_ptr(),
+              sd.data_ptr(), thr, None, None, _lib.stream_handle())
+    got = H(buf)
+    for (slot, n, w0, _), s in zip(rows, seeds):
+        keep = O.dropout_keep((n,), p, s) if n <= 200_000 else None
+        bits = got[4 * w0:4 * w0 + (n + 7) // 8]
+        dense = np.unpackbits(bits, bitorder="little")[:n]
+        if keep is not None:
+            assert np.array_equal(dense, keep.astype(np.uint8)), (slot, n)
+        else:   # large sites: against the single-site device kernel (itself pinned to golden)
+            ref = torch.empty((n + 7) // 8, dtype=torch.uint8, device="cuda")
+            _lib.call("ls2_dropout_bits", ref.data_ptr(), n, s, None, thr, _lib.stream_handle())
+            assert np.array_equal(bits, H(ref)), (slot, n)
+        pad = np.unpackbits(got[4 * w0:4 * w0 + 4 * (((n + 31) // 32 + 3) // 4 * 4)],
+                            bitorder="little")[n:]
+        assert not pad.any()
+
+
+def test_bdr_layernorm_read_bits_equals_draw():
+    from paper_2110_05722_b200 import _lib
+    rng = np.random.default_rng(3)
+    r, d = 4096, 512
+    x, res = (C(rng.normal(size=(r, d)).astype(np.float16)) for _ in range(2))
+    bias, w, b = (C(rng.normal(size=d).astype(np.float16)) for _ in range(3))
+    outs = []
+    for mode in (1, 2):
+        y, u = torch.empty_like(x), torch.empty_like(x)
+        mu, sg = (torch.empty(r, dtype=torch.float32, device="cuda") for _ in range(2))
+        bits = torch.empty(r * d // 8, dtype=torch.uint8, device="cuda")
+        if mode == 2:
+            _lib.call("ls2_dropout_bits", bits.data_ptr(), r * d, 77, None,
+                      K._drop_args(0.1)[1], _lib.stream_handle())
+        _lib.call("ls2_bdr_layernorm_fwd", x.data_ptr(), bias.data_ptr(), res.data_ptr(),
+                  y.data_ptr(), bits.data_ptr(), w.data_ptr(), b.data_ptr(), u.data_ptr(),
+                  mu.data_ptr(), sg.data_ptr(), r, d, 1e-5, mode, 77, None, K._drop_args(0.1)[1],
+                  1 / 0.9, _lib.F16, _lib.F16, _lib.F32, _lib.stream_handle())
+        outs.append((H(y), H(u), H(mu), H(sg), H(bits)))
+    for a, b2 in zip(*outs):
+        assert np.array_equal(a, b2)

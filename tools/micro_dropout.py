@@ -65,6 +65,21 @@ def main():
         thr = K._drop_args(0.1)[1]
         out[f"maskgen_{name}"] = graph_time(lambda: _lib.call(
             "ls2_dropout_bits", bits.data_ptr(), n, 5, None, thr, _lib.stream_handle()))
+    # the whole T-base step's forward sites in one launch (mask bank)
+    sizes = [N * 512] + [N * 512, N * 2048, N * 512] * 6 + [N * 512] + \
+        [N * 512, N * 512, N * 2048, N * 512] * 6
+    rows, woff = [], 0
+    for i, n in enumerate(sizes):
+        rows.append([i, n, woff, 0])
+        woff += ((n + 31) // 32 + 3) // 4 * 4
+    desc = torch.tensor(rows, dtype=torch.int64, device=dev)
+    seeds = torch.arange(len(sizes), dtype=torch.int64, device=dev) * 7919
+    buf = torch.empty(4 * woff, dtype=torch.uint8, device=dev)
+    thr = K._drop_args(0.1)[1]
+    out["maskbank_tbase_step"] = graph_time(lambda: _lib.call(
+        "ls2_dropout_bits_multi", desc.data_ptr(), len(sizes), woff, buf.data_ptr(),
+        seeds.data_ptr(), thr, None, None, _lib.stream_handle()), reps=10)
+    out["maskbank_elements"] = float(sum(sizes))
     print(json.dumps({k: round(v, 2) for k, v in out.items()}, indent=1))
 
 
