@@ -237,10 +237,7 @@ int ls2_adam(uint16_t* p16, const uint16_t* g16, float* m, float* v, int64_t n, 
   if (n <= 0) return LS2_OK;
   if (t_host <= 0 && !applied) return fail(LS2_ERR_SHAPE, "adam: need t_host or applied counter");
   const bool vec = aligned16(p16) && aligned16(g16) && aligned16(m) && aligned16(v);
-  // half the SM's thread slots: enough bytes in flight to saturate HBM, and the
-  // other half stays free for the next step's mask-bank draw running beside it
-  const int grid = std::min(stream_grid(vec ? ceil_div(n, 8) : n), kNumSMs * 4);
-  adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+  adam_kernel<<<stream_grid(vec ? ceil_div(n, 8) : n), 256, 0, as_stream(stream)>>>(
       p16, g16, m, v, n, hyper, bc_table, bc_len, t_host, applied, nonfinite, loss, vec);
   return check_launch("adam");
 }
