@@ -37,6 +37,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Transformer-base train tokens/sec @1/2/4/8 B200; kernel HBM GB/s vs peak"
 B, L, V = 64, 64, 32000
+# BASELINE.json configs: [1] Transformer-base (the headline, default) and
+# [2] Transformer-big (d1024 h16 f4096, 64 x 128 = 8192 tokens/GPU) via --model tbig
+MODELS = {"tbase": (64, 64, "Transformer-base 6e6d, d512 h8 f2048 V32000"),
+          "tbig": (64, 128, "Transformer-big 6e6d, d1024 h16 f4096 V32000")}
 
 
 def _peaks():
@@ -223,10 +227,14 @@ def run_ours(args):
     from paper_2110_05722_b200.dist import DataParallel, init_from_env
     from paper_2110_05722_b200.engine import TrainingEngine
 
+    from paper_2110_05722_b200.config import transformer_big
+    global B, L
+    B, L, desc = MODELS[args.model]
     rank, world, local = init_from_env()
     torch.cuda.set_device(local)
     dp = DataParallel(force=os.environ.get("LS2_DP_FORCE") == "1")
-    run = RunConfig(model=transformer_base(V, 256),
+    mcfg = transformer_base(V, 256) if args.model == "tbase" else transformer_big(V, 256)
+    run = RunConfig(model=mcfg,
                     train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L,
                                       seed=1234 + 0 * rank, loss_scale=1.0))
     task = FixedShapeTask(B, L, V, seed=17 + rank)
@@ -298,9 +306,9 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "fp16", "data": "synthetic (uniform tokens, 64x64 per GPU)",
-                "config": {"workload": "Transformer-base 6e6d, d512 h8 f2048 V32000, "
-                                       "4096 target tok/GPU, p_drop 0.1, alpha 0.1, Adam",
+                "dtype": "fp16", "data": f"synthetic (uniform tokens, {B}x{L} per GPU)",
+                "config": {"workload": f"{desc}, {B * L} target tok/GPU, p_drop 0.1, "
+                                       "alpha 0.1, Adam",
                            "global_batch": world * B * L, "seq_len": L,
                            "parallelism": f"dp{world}",
                            "exchange": ("bucketed fp16 NCCL all-reduce overlapped with backward, "
@@ -316,7 +324,7 @@ def run_ours(args):
                              "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic, "launch_ms": adam_ms},
                 }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.model == "tbase":
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
@@ -332,6 +340,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--model", default="tbase", choices=sorted(MODELS))
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

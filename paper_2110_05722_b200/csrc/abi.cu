@@ -36,6 +36,56 @@ __global__ void dropout_bits_kernel(uint8_t* bits, int64_t n, uint64_t seed, con
   }
 }
 
+// 32 keep bits with the integer work split across the FMA-heavy pipe (64-bit
+// products, the last shift done as mul.hi by 2) and the ALU pipe (shifts, xors,
+// the compare): each pipe takes one warp instruction every other cycle, so
+// balancing them is what sets the draw rate (ncu: fmaheavy and alu both busy).  The compare is a carry chain: z3hi + ~Thi carries
+// out iff z3hi > Thi, and addc shifts that carry into the word MSB-first; ties
+// (z3hi == Thi, probability 2^-32 per draw) are caught by a running max of the
+// sums and the word is then redrawn with the exact 64-bit form.
+__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+__device__ __noinline__ uint32_t keep_word_exact(uint64_t seed, uint64_t first, uint64_t thresh) {
+  return keep_bits_n<32>(seed, first, thresh);
+}
+
+__device__ __forceinline__ uint32_t keep_word_fast(uint64_t seed, uint64_t first, uint64_t thresh) {
+  constexpr uint32_t kAlo = (uint32_t)kMixA, kAhi = (uint32_t)(kMixA >> 32);
+  constexpr uint32_t kBlo = (uint32_t)kMixB, kBhi = (uint32_t)(kMixB >> 32);
+  const uint64_t T = thresh << 11;
+  const uint32_t nThi = ~(uint32_t)(T >> 32);
+  uint64_t x = seed + (first + 31) * kPhi;        // MSB-first: element first+31 .. first
+  uint32_t b = 0, tie = 0;
+#pragma unroll
+  for (int e = 31; e >= 0; --e) {
+    const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32);
+    // y1 = x ^ (x >> 30)   (ALU: funnel shift + xors)
+    const uint32_t y1lo = xlo ^ __funnelshift_r(xlo, xhi, 30);
+    const uint32_t y1hi = xhi ^ (xhi >> 30);
+    // z1 = y1 * A
+    const uint64_t p = (uint64_t)y1lo * kAlo;
+    const uint32_t z1lo = (uint32_t)p;
+    const uint32_t z1hi = (uint32_t)(p >> 32) + y1lo * kAhi + y1hi * kAlo;
+    // y2 = z1 ^ (z1 >> 27)  (ALU)
+    const uint32_t y2lo = z1lo ^ __funnelshift_r(z1lo, z1hi, 27);
+    const uint32_t y2hi = z1hi ^ (z1hi >> 27);
+    // high word of z2 = y2 * B, then z3 = z2 ^ (z2 >> 31)
+    const uint32_t z2hi = __umulhi(y2lo, kBlo) + y2lo * kBhi + y2hi * kBlo;
+    const uint32_t z3hi = z2hi ^ mulhi_u32(z2hi, 2u);
+    uint32_t sum;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %1, %1;"
+        : "=r"(sum), "+r"(b) : "r"(z3hi), "r"(nThi));
+    tie = max(tie, sum);                            // sum == ~0 <=> z3hi == Thi
+    x -= kPhi;
+  }
+  if (__builtin_expect(tie == 0xFFFFFFFFu, 0)) return keep_word_exact(seed, first, thresh);
+  return b;
+}
+
 // Every dropout site of a step in one launch (the mask bank).  desc rows
 // {seed slot, elements, first 32-bit word} (int64), sorted by first word;
 // site s fills words [first_s, first_s + ceil(n_s/32)) of `words` with the
@@ -61,7 +111,7 @@ __global__ void __launch_bounds__(256) dropout_bits_multi_kernel(
        w += (int64_t)gridDim.x * blockDim.x) {
     while (w >= s_first[site + 1]) ++site;           // w only grows: sites in order
     const int64_t e0 = (w - s_first[site]) * 32;
-    uint32_t b = keep_bits_n<32>(s_seed[site], (uint64_t)e0, thresh);
+    uint32_t b = keep_word_fast(s_seed[site], (uint64_t)e0, thresh);
     const int64_t valid = s_n[site] - e0;
     if (valid < 32) b &= valid <= 0 ? 0u : ((1u << valid) - 1u);
     words[w] = b;

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--json", default=None)
     ap.add_argument("--top", type=int, default=45)
+    ap.add_argument("--model", default="tbase", choices=["tbase", "tbig"])
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -27,8 +28,10 @@ def main():
     from paper_2110_05722_b200.data import FixedShapeTask
     from paper_2110_05722_b200.engine import TrainingEngine
 
-    B, L, V = 64, 64, 32000
-    run = RunConfig(model=transformer_base(V, 256),
+    from paper_2110_05722_b200.config import transformer_big
+    B, L, V = (64, 64, 32000) if a.model == "tbase" else (64, 128, 32000)
+    run = RunConfig(model=transformer_base(V, 256) if a.model == "tbase" else
+                    transformer_big(V, 256),
                     train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L))
     eng = TrainingEngine(run, task=FixedShapeTask(B, L, V, seed=17))
     eng.setup_arena()

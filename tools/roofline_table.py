@@ -12,12 +12,17 @@ import argparse
 import json
 import re
 
-N, D, F, V, B, L, H = 4096, 512, 2048, 32000, 64, 64, 8
-P = 60_655_616          # Transformer-base parameters (learned positions, max_len 256)
-BHL2 = B * H * L * L
+SIZES = {   # tokens, d, ffn, vocab, batch, len, heads, parameters (learned positions, max_len 256)
+    "tbase": (4096, 512, 2048, 32000, 64, 64, 8, 60_655_616),
+    "tbig": (8192, 1024, 4096, 32000, 64, 128, 16, 209_391_616),
+}
 
-# (regex on the kernel name, description, algorithmic bytes per launch)
-ALGO = [
+
+def algo_table(model: str):
+    N, D, F, V, B, L, H, P = SIZES[model]
+    BHL2 = B * H * L * L
+    # (regex on the kernel name, description, algorithmic bytes per launch)
+    return [
     (r"bdr_fwd_vec", "bias+dropout+residual fwd", 3 * N * D * 2 + N * D // 8),
     (r"bdr_bwd_vec", "bias+dropout+residual bwd (+dbias partials)", 2 * N * D * 2 + N * D // 8),
     (r"brd_fwd_vec", "bias+ReLU+dropout fwd", 2 * N * F * 2 + 2 * N * F // 8),
@@ -37,7 +42,10 @@ ALGO = [
     (r"emb_fwd_vec", "embedding fwd (gather, scale, pos, dropout)", 8 * N + 3 * N * D * 2 + N * D // 8),
     (r"emb_bwd_scatter", "embedding bwd scatter (fp32 RMW)", N * D * 2 + 2 * N * D * 4 + N * D // 8),
     (r"emb_bwd_pos", "positional-table grad", N * D * 2 + N * D // 8),
-]
+    (r"dropout_bits_multi", "mask bank: every forward dropout site (ALU-bound draw)",
+     (6 * (2 * N * D + N * F) + 6 * (3 * N * D + N * F) + 2 * N * D) // 8),
+    (r"finish_narrow", "deferred bias/LN column sums -> fp16 workspace", None),
+    ]
 
 
 def main():
@@ -45,7 +53,9 @@ def main():
     ap.add_argument("json")
     ap.add_argument("--peak", type=float, default=6449.4)
     ap.add_argument("--md", default=None)
+    ap.add_argument("--model", default="tbase", choices=sorted(SIZES))
     a = ap.parse_args()
+    ALGO = algo_table(a.model)
     d = json.load(open(a.json))
     lines = ["| kernel | what | launches/step | µs/launch (in situ) | algorithmic MB/launch | "
              "achieved GB/s | frac of HBM peak |", "|---|---|---|---|---|---|---|"]
@@ -53,7 +63,7 @@ def main():
     for k in d["kernels"]:
         name = k["name"]
         for pat, what, nbytes in ALGO:
-            if re.search(pat, name):
+            if re.search(pat, name) and nbytes is not None:
                 n = max(k["launches_per_step"], 1)
                 us = k["us_per_step"] / n
                 gbs = nbytes / (us * 1e-6) / 1e9
