@@ -146,8 +146,7 @@ class TrainingEngine:
         self.masks = MaskBank(self.device) if os.environ.get("LS2_MASK_BANK", "1") != "0" else None
         # next step's site seeds: the bank draws step t+1's bits beside step t's Adam
         self._seeds_next = SeedTable(self.device)
-        # off by default: measured slower at T-base (Adam's bit-exact IEEE div/sqrt
-        # keep its SMs' ALUs busy, so the draw does not hide beside it)
+        # LS2_EARLY_MASKS=1: draw the next step's bits layer by layer during backward
         self._early_masks = os.environ.get("LS2_EARLY_MASKS", "0") == "1"
         self.last_out3 = None
 
@@ -223,6 +222,11 @@ class TrainingEngine:
                 nx.dev[:n].copy_(nx.host[:n], non_blocking=True)
         self.arena.begin(key)
         sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
+        self._bank_done = None
+        if self.masks is not None and self._early_masks and t.p_drop > 0.0:
+            # the next step's dropout bits, layer by layer as backward releases them
+            self._bank_table = self._seeds_next if upload else self.model.seed_table(self.device)
+            sink.on_layer_done = self._bank_layer_done
         if self.dp.active:
             # buckets are narrowed / all-reduced on the comm stream while the
             # backward pass is still running (dist.py)
@@ -298,27 +302,36 @@ class TrainingEngine:
             _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr() + 2 * start, stop - start,
                       self._nonfinite.data_ptr(), cs.cuda_stream)
 
-    def _draw_next_masks(self, uploaded: bool):
-        """Beside the optimizer pass (HBM-bound, half the SM slots), draw the next
-        step's dropout bits on the side stream and stamp them; returns the event
-        the step's end must wait on.  The device-resident benchmark graph keeps
-        its seeds, so it redraws the same step (same work)."""
+    _BANK_GROUPS = {"cross_kv.": "tgt"}
+
+    def _bank_layer_done(self, prefixes):
+        """Backward released these layers' dropout bits: redraw them for the next
+        step on the low-priority side stream, overlapping the rest of backward."""
         bank = self.masks
-        if bank is None or bank.desc is None or not self._early_masks or \
-                self.cfg.train.p_drop <= 0.0:
-            return None
-        tbl = self._seeds_next if uploaded else self.model.seed_table(self.device)
+        if bank.desc is None:
+            return
+        if prefixes is None:
+            groups = ["src"]
+        else:
+            groups = []
+            for p in prefixes:
+                g = self._BANK_GROUPS.get(p, p.rstrip("."))
+                if g in bank.groups:
+                    groups.append(g)
+        if not groups:
+            return
         side = _lib.context().side_stream
-        main = torch.cuda.current_stream()
         ev = torch.cuda.Event()
-        ev.record(main)
+        ev.record(torch.cuda.current_stream())
         side.wait_event(ev)
         with torch.cuda.stream(side):
-            bank.generate(tbl.dev)
-            bank.stamp.copy_(tbl.step_slot())
-        done = torch.cuda.Event()
-        done.record(side)
-        return done
+            for g in groups:
+                bank.generate_group(g, self._bank_table.dev)
+            if prefixes is None:
+                bank.stamp.copy_(self._bank_table.step_slot())
+        if prefixes is None:
+            self._bank_done = torch.cuda.Event()
+            self._bank_done.record(side)
 
     def _finish_deferred(self, sink, out3, nonfinite_ptr, entries=None):
         """One launch finishing every deferred bias / LayerNorm gradient (partials
@@ -359,7 +372,7 @@ class TrainingEngine:
                       float(1.0 / t.act_grad_scale), self._nonfinite.data_ptr(), st)
             self._finish_deferred(sink, out3, self._nonfinite.data_ptr())
         loss_ptr = out3.data_ptr()
-        joined = self._draw_next_masks(host_copy)
+        joined = getattr(self, "_bank_done", None)
         if self.optim.algorithm == "adam":
             _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
                       ws.m32.data_ptr(), ws.v32.data_ptr(), ws.n_elements,

@@ -353,11 +353,15 @@ class _ViewSink(GradSink):
         self.arena = None
         self.lane = None                  # _Lane for weight-gradient GEMMs (engine path)
         self.on_ready = None              # engine hook: gradients of these names are final
+        self.on_layer_done = None         # engine hook: raw ready() prefixes
         self.totals = None                # (loss, count, correct) once the criterion ran
 
     def ready(self, prefixes):
         """Backward has finished every parameter whose name starts with one of
-        `prefixes` (None: all remaining) — the data-parallel exchange may start."""
+        `prefixes` (None: all remaining) — the data-parallel exchange may start,
+        and that layer's dropout bits are dead (mask bank)."""
+        if self.on_layer_done is not None:
+            self.on_layer_done(prefixes)
         if self.on_ready is not None:
             names = None if prefixes is None else \
                 [n for n in self.store if any(n.startswith(p) for p in prefixes)]
@@ -714,15 +718,30 @@ class MaskBank:
         if src_tokens > self.max_tokens[0] or tgt_tokens > self.max_tokens[1]:
             raise ShapeMismatch("batch larger than the mask bank's configured maximum")
         if self.desc is None:
-            rows, woff, offs = [], 0, {}
-            for slot, n in sites_fn(*self.max_tokens):
+            rows, woff, offs, spans = [], 0, {}, {}
+            for slot, n, grp in sites_fn(*self.max_tokens):
                 rows.append([slot, n, woff, 0])
                 offs[slot] = 4 * woff
+                spans.setdefault(grp, []).append(len(rows) - 1)
                 woff += ((n + 31) // 32 + 3) // 4 * 4        # 16-byte aligned sites
             self.desc = torch.tensor(rows, dtype=torch.int64, device=self.device)
             self.nsites, self.words, self.sites = len(rows), woff, offs
             self.buf = torch.zeros(4 * woff, dtype=torch.uint8, device=self.device)
+            # per-layer groups (contiguous in the layout): drawn one by one as the
+            # backward pass releases them (engine, LS2_EARLY_MASKS=1)
+            self.groups = {}
+            for grp, idx in spans.items():
+                w0 = rows[idx[0]][2]
+                w1 = rows[idx[-1]][2] + ((rows[idx[-1]][1] + 31) // 32 + 3) // 4 * 4
+                sub = [[rows[i][0], rows[i][1], rows[i][2] - w0, 0] for i in idx]
+                self.groups[grp] = (torch.tensor(sub, dtype=torch.int64, device=self.device),
+                                    len(sub), w1 - w0, 4 * w0)
         self.thresh = thresh
+
+    def generate_group(self, grp: str, seeds_dev: torch.Tensor):
+        desc, ns, words, off = self.groups[grp]
+        _lib.call("ls2_dropout_bits_multi", desc.data_ptr(), ns, words, self.buf.data_ptr() + off,
+                  seeds_dev.data_ptr(), self.thresh, None, None, _lib.stream_handle())
 
     def generate(self, seeds_dev: torch.Tensor, stamp=None, want=None):
         """Draw every site with the seeds in seeds_dev (skipped on the device
@@ -1331,14 +1350,16 @@ class Transformer:
         order, for ts source and tt target tokens."""
         d, f = self.cfg.d_model, self.cfg.d_ff
         slot = lambda t: t.storage_offset()      # noqa: E731
-        sites = [(slot(s_src), ts * d)]
+        sites = [(slot(s_src), ts * d, "src")]
         for i in range(self.cfg.n_enc):
-            sites += [(slot(enc_seed.site(i, 0)), ts * d), (slot(enc_seed.site(i, 1)), ts * f),
-                      (slot(enc_seed.site(i, 2)), ts * d)]
-        sites.append((slot(s_tgt), tt * d))
+            g = f"enc{i}"
+            sites += [(slot(enc_seed.site(i, 0)), ts * d, g), (slot(enc_seed.site(i, 1)), ts * f, g),
+                      (slot(enc_seed.site(i, 2)), ts * d, g)]
+        sites.append((slot(s_tgt), tt * d, "tgt"))
         for i in range(self.cfg.n_dec):
-            sites += [(slot(dec_seed.site(i, 0)), tt * d), (slot(dec_seed.site(i, 1)), tt * d),
-                      (slot(dec_seed.site(i, 2)), tt * f), (slot(dec_seed.site(i, 3)), tt * d)]
+            g = f"dec{i}"
+            sites += [(slot(dec_seed.site(i, 0)), tt * d, g), (slot(dec_seed.site(i, 1)), tt * d, g),
+                      (slot(dec_seed.site(i, 2)), tt * f, g), (slot(dec_seed.site(i, 3)), tt * d, g)]
         return sites
 
     def _forward_backward(self, params, batch: Batch, *, p_drop, alpha, seed, step, arena, sink,
