@@ -250,51 +250,65 @@ __device__ __forceinline__ void store_rows(__half* gbase, int64_t ld, const __ha
   }
 }
 
-template <int QT, int KT>
-__global__ void __launch_bounds__(32 * (QT > KT ? QT : KT)) attn_bwd_kernel(AttnBwdArgs a) {
-  constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
-  extern __shared__ __align__(16) __half sm[];
-  __half* Qs = sm;                    // [LQ][72]
-  __half* Ks = Qs + LQ * kRow;        // [LK][72]
-  __half* Vs = Ks + LK * kRow;        // [LK][72]
-  __half* Os = Vs + LK * kRow;        // dO [LQ][72]
-  __half* Ps = Os + LQ * kRow;        // [LQ][LK+8]
-  __half* Ss = Ps + LQ * PLD;         // dS [LQ][LK+8]
-  const int bh = blockIdx.x, b = bh / a.H, h = bh % a.H;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// 2 * max(QT, KT) warps in two concurrent roles per phase:
+//   phase A  query warps: dP = dO V^T, dS = P (dP - rowsum(dP P)) * scale -> smem
+//            key warps:   dV = P^T dO  (needs only P and dO: runs beside dS)
+//   phase B  query warps: dQ = dS K
+//            key warps:   dK = dS^T Q
+// so the dependent chain per CTA is two 32-MMA steps, not two 64-MMA steps.
+// issue the cp.async loads of one (batch, head) item: Q, K, V, dO tiles and P
+__device__ __forceinline__ void attn_bwd_issue(const AttnBwdArgs& a, int bh, __half* Qs, __half* Ks,
+                                               __half* Vs, __half* Os, __half* Ps, int LQ, int LK,
+                                               int PLD) {
+  const int b = bh / a.H, h = bh % a.H;
   load_tile(Qs, a.q + (int64_t)b * a.Lq * a.ldq + h * kHd, a.ldq, a.Lq, LQ);
   load_tile(Ks, a.k + (int64_t)b * a.Lk * a.ldk + h * kHd, a.ldk, a.Lk, LK);
   load_tile(Vs, a.v + (int64_t)b * a.Lk * a.ldv + h * kHd, a.ldv, a.Lk, LK);
   load_tile(Os, a.dout + (int64_t)b * a.Lq * a.lddo + h * kHd, a.lddo, a.Lq, LQ);
-  {  // P (zero padded) [LQ][LK]
-    const __half* pg = a.probs + (int64_t)bh * a.Lq * a.Lk;
-    if ((a.Lk & 7) == 0) {
-      const int cpr = LK >> 3;
-      for (int i = threadIdx.x; i < LQ * cpr; i += blockDim.x) {
-        const int r = i / cpr, ch = i % cpr;
-        const bool ok = r < a.Lq && ch * 8 < a.Lk;
-        cp_async16(Ps + r * PLD + ch * 8, pg + (ok ? (int64_t)r * a.Lk + ch * 8 : 0), ok);
-      }
-    } else {
-      for (int i = threadIdx.x; i < LQ * LK; i += blockDim.x) {
-        const int r = i / LK, c = i % LK;
-        Ps[r * PLD + c] = (r < a.Lq && c < a.Lk) ? pg[(int64_t)r * a.Lk + c] : __float2half(0.f);
-      }
+  const __half* pg = a.probs + (int64_t)bh * a.Lq * a.Lk;
+  if ((a.Lk & 7) == 0) {
+    const int cpr = LK >> 3;
+    for (int i = threadIdx.x; i < LQ * cpr; i += blockDim.x) {
+      const int r = i / cpr, ch = i % cpr;
+      const bool ok = r < a.Lq && ch * 8 < a.Lk;
+      cp_async16(Ps + r * PLD + ch * 8, pg + (ok ? (int64_t)r * a.Lk + ch * 8 : 0), ok);
+    }
+  } else {
+    for (int i = threadIdx.x; i < LQ * LK; i += blockDim.x) {
+      const int r = i / LK, c = i % LK;
+      Ps[r * PLD + c] = (r < a.Lq && c < a.Lk) ? pg[(int64_t)r * a.Lk + c] : __float2half(0.f);
     }
   }
-  cp_async_wait_all();
-  __syncthreads();
-  const int g = lane >> 2, t = lane & 3;
+  asm volatile("cp.async.commit_group;\n" ::);
+}
 
-  // phase 1 (warp = 16 query rows): dP = dO V^T; dS = P*(dP - rowsum(dP*P))*scale; dQ = dS K
-  if (w < QT) {
+// 2 * max(QT, KT) warps in two concurrent roles per phase:
+//   phase A  query warps: dP = dO V^T, dS = P (dP - rowsum(dP P)) * scale -> smem
+//            key warps:   dV = P^T dO  (needs only P and dO: runs beside dS)
+//   phase B  query warps: dQ = dS K
+//            key warps:   dK = dS^T Q
+// so the dependent chain per item is two 32-MMA steps, not two 64-MMA steps.
+template <int QT, int KT>
+__device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, const __half* Qs,
+                                                 const __half* Ks, const __half* Vs,
+                                                 const __half* Os, const __half* Ps, __half* Ss) {
+  constexpr int PLD = 16 * KT + kPad;
+  constexpr int NW = QT > KT ? QT : KT;
+  const int b = bh / a.H, h = bh % a.H;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const bool qw = w < NW;             // query-tile role (else key-tile role)
+  const int tw = qw ? w : w - NW;     // tile index of this warp
+
+  // ---- phase A ----
+  if (qw && tw < QT) {
     float dp[2 * KT][4];
 #pragma unroll
     for (int j = 0; j < 2 * KT; ++j) dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < kHd; kk += 16) {
       uint32_t af[4];
-      frag_a(af, Os, kRow, 16 * w, kk, lane);
+      frag_a(af, Os, kRow, 16 * tw, kk, lane);
 #pragma unroll
       for (int nt = 0; nt < KT; ++nt) {
         uint32_t bf[4];
@@ -303,35 +317,63 @@ __global__ void __launch_bounds__(32 * (QT > KT ? QT : KT)) attn_bwd_kernel(Attn
         mma16816(dp[2 * nt + 1], af, bf[2], bf[3]);
       }
     }
-    const int r0 = 16 * w + g, r1 = r0 + 8;
-    float pv[2 * KT][4];
+    const int r0 = 16 * tw + g, r1 = r0 + 8;
     float s0 = 0.f, s1 = 0.f;
 #pragma unroll
     for (int j = 0; j < 2 * KT; ++j) {
       const float2 x0 = unpack_h2(*reinterpret_cast<const uint32_t*>(Ps + r0 * PLD + 8 * j + 2 * t));
       const float2 x1 = unpack_h2(*reinterpret_cast<const uint32_t*>(Ps + r1 * PLD + 8 * j + 2 * t));
-      pv[j][0] = x0.x; pv[j][1] = x0.y; pv[j][2] = x1.x; pv[j][3] = x1.y;
-      s0 += dp[j][0] * pv[j][0] + dp[j][1] * pv[j][1];
-      s1 += dp[j][2] * pv[j][2] + dp[j][3] * pv[j][3];
+      s0 += dp[j][0] * x0.x + dp[j][1] * x0.y;
+      s1 += dp[j][2] * x1.x + dp[j][3] * x1.y;
     }
     s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
     s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
     s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
     s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    uint32_t ds[2 * KT][2];
 #pragma unroll
     for (int j = 0; j < 2 * KT; ++j) {
-      ds[j][0] = pack_h2(pv[j][0] * (dp[j][0] - s0) * a.scale, pv[j][1] * (dp[j][1] - s0) * a.scale);
-      ds[j][1] = pack_h2(pv[j][2] * (dp[j][2] - s1) * a.scale, pv[j][3] * (dp[j][3] - s1) * a.scale);
-      *reinterpret_cast<uint32_t*>(Ss + r0 * PLD + 8 * j + 2 * t) = ds[j][0];
-      *reinterpret_cast<uint32_t*>(Ss + r1 * PLD + 8 * j + 2 * t) = ds[j][1];
+      const float2 x0 = unpack_h2(*reinterpret_cast<const uint32_t*>(Ps + r0 * PLD + 8 * j + 2 * t));
+      const float2 x1 = unpack_h2(*reinterpret_cast<const uint32_t*>(Ps + r1 * PLD + 8 * j + 2 * t));
+      *reinterpret_cast<uint32_t*>(Ss + r0 * PLD + 8 * j + 2 * t) =
+          pack_h2(x0.x * (dp[j][0] - s0) * a.scale, x0.y * (dp[j][1] - s0) * a.scale);
+      *reinterpret_cast<uint32_t*>(Ss + r1 * PLD + 8 * j + 2 * t) =
+          pack_h2(x1.x * (dp[j][2] - s1) * a.scale, x1.y * (dp[j][3] - s1) * a.scale);
     }
+  } else if (!qw && tw < KT) {
+    float dv[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
+#pragma unroll
+    for (int qt = 0; qt < QT; ++qt) {
+      uint32_t ap[4];
+      frag_a_t(ap, Ps, PLD, 16 * tw, 16 * qt, lane);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        uint32_t bo[4];
+        frag_b_kn(bo, Os, kRow, 16 * qt, 16 * nt, lane);
+        mma16816(dv[2 * nt], ap, bo[0], bo[1]);
+        mma16816(dv[2 * nt + 1], ap, bo[2], bo[3]);
+      }
+    }
+    const int r0 = 16 * tw + g, r1 = r0 + 8;
+    __half* d0 = a.dv + ((int64_t)b * a.Lk + r0) * a.lddv + h * kHd + 2 * t;
+    __half* d1 = d0 + 8 * a.lddv;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (r0 < a.Lk) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dv[j][0], dv[j][1]);
+      if (r1 < a.Lk) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dv[j][2], dv[j][3]);
+    }
+  }
+  __syncthreads();
+  // ---- phase B ----
+  if (qw && tw < QT) {
     float dq[8][4];
 #pragma unroll
     for (int j = 0; j < 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
-      const uint32_t af[4] = {ds[2 * kt][0], ds[2 * kt][1], ds[2 * kt + 1][0], ds[2 * kt + 1][1]};
+      uint32_t af[4];
+      frag_a(af, Ss, PLD, 16 * tw, 16 * kt, lane);
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         uint32_t bf[4];
@@ -340,54 +382,96 @@ __global__ void __launch_bounds__(32 * (QT > KT ? QT : KT)) attn_bwd_kernel(Attn
         mma16816(dq[2 * nt + 1], af, bf[2], bf[3]);
       }
     }
-    __half* dqg = a.dq + (int64_t)b * a.Lq * a.lddq + h * kHd;
+    const int r0 = 16 * tw + g, r1 = r0 + 8;
+    __half* d0 = a.dq + ((int64_t)b * a.Lq + r0) * a.lddq + h * kHd + 2 * t;
+    __half* d1 = d0 + 8 * a.lddq;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (r0 < a.Lq)
-        *reinterpret_cast<uint32_t*>(dqg + (int64_t)r0 * a.lddq + 8 * j + 2 * t) = pack_h2(dq[j][0], dq[j][1]);
-      if (r1 < a.Lq)
-        *reinterpret_cast<uint32_t*>(dqg + (int64_t)r1 * a.lddq + 8 * j + 2 * t) = pack_h2(dq[j][2], dq[j][3]);
+      if (r0 < a.Lq) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dq[j][0], dq[j][1]);
+      if (r1 < a.Lq) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dq[j][2], dq[j][3]);
     }
-  }
-  __syncthreads();
-  // phase 2 (warp = 16 key rows): dK = dS^T Q; dV = P^T dO
-  if (w < KT) {
-    float dk[8][4], dv[8][4];
+  } else if (!qw && tw < KT) {
+    float dk[8][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
-      dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
-    }
+    for (int j = 0; j < 8; ++j) dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
 #pragma unroll
     for (int qt = 0; qt < QT; ++qt) {
-      uint32_t as[4], ap[4];
-      frag_a_t(as, Ss, PLD, 16 * w, 16 * qt, lane);
-      frag_a_t(ap, Ps, PLD, 16 * w, 16 * qt, lane);
+      uint32_t as[4];
+      frag_a_t(as, Ss, PLD, 16 * tw, 16 * qt, lane);
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        uint32_t bq[4], bo[4];
+        uint32_t bq[4];
         frag_b_kn(bq, Qs, kRow, 16 * qt, 16 * nt, lane);
-        frag_b_kn(bo, Os, kRow, 16 * qt, 16 * nt, lane);
         mma16816(dk[2 * nt], as, bq[0], bq[1]);
         mma16816(dk[2 * nt + 1], as, bq[2], bq[3]);
-        mma16816(dv[2 * nt], ap, bo[0], bo[1]);
-        mma16816(dv[2 * nt + 1], ap, bo[2], bo[3]);
       }
     }
-    const int r0 = 16 * w + g, r1 = r0 + 8;
-    __half* dkg = a.dk + (int64_t)b * a.Lk * a.lddk + h * kHd;
-    __half* dvg = a.dv + (int64_t)b * a.Lk * a.lddv + h * kHd;
+    const int r0 = 16 * tw + g, r1 = r0 + 8;
+    __half* d0 = a.dk + ((int64_t)b * a.Lk + r0) * a.lddk + h * kHd + 2 * t;
+    __half* d1 = d0 + 8 * a.lddk;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (r0 < a.Lk) {
-        *reinterpret_cast<uint32_t*>(dkg + (int64_t)r0 * a.lddk + 8 * j + 2 * t) = pack_h2(dk[j][0], dk[j][1]);
-        *reinterpret_cast<uint32_t*>(dvg + (int64_t)r0 * a.lddv + 8 * j + 2 * t) = pack_h2(dv[j][0], dv[j][1]);
-      }
-      if (r1 < a.Lk) {
-        *reinterpret_cast<uint32_t*>(dkg + (int64_t)r1 * a.lddk + 8 * j + 2 * t) = pack_h2(dk[j][2], dk[j][3]);
-        *reinterpret_cast<uint32_t*>(dvg + (int64_t)r1 * a.lddv + 8 * j + 2 * t) = pack_h2(dv[j][2], dv[j][3]);
-      }
+      if (r0 < a.Lk) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dk[j][0], dk[j][1]);
+      if (r1 < a.Lk) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dk[j][2], dk[j][3]);
     }
+  }
+}
+
+// one CTA per item (tiles up to 128 x 128)
+template <int QT, int KT>
+__global__ void __launch_bounds__(64 * (QT > KT ? QT : KT), (QT > KT ? QT : KT) <= 4 ? 4 : 1)
+attn_bwd_kernel(AttnBwdArgs a) {
+  constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
+  extern __shared__ __align__(16) __half sm[];
+  __half* Qs = sm;                    // [LQ][72]
+  __half* Ks = Qs + LQ * kRow;        // [LK][72]
+  __half* Vs = Ks + LK * kRow;        // [LK][72]
+  __half* Os = Vs + LK * kRow;        // dO [LQ][72]
+  __half* Ps = Os + LQ * kRow;        // [LQ][LK+8]
+  __half* Ss = Ps + LQ * PLD;         // dS [LQ][LK+8]
+  attn_bwd_issue(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  attn_bwd_compute<QT, KT>(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, Ss);
+}
+
+// Persistent, double-buffered (tiles up to 64 x 64, two CTAs per SM): a CTA
+// walks items blockIdx.x, +gridDim.x, ... and the next item's five tiles load
+// (cp.async) while the current one is computed and stored, so an SM's loads,
+// tensor-core work and stores overlap instead of running as three phases.
+template <int QT, int KT>
+__global__ void __launch_bounds__(64 * (QT > KT ? QT : KT), 2)
+attn_bwd_persist(AttnBwdArgs a, int nitems) {
+  constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
+  constexpr int STAGE = 2 * LQ * kRow + 2 * LK * kRow + LQ * PLD;   // halves
+  extern __shared__ __align__(16) __half sm[];
+  __half* Ss = sm + 2 * STAGE;
+  auto stage = [&](int s, __half*& Qs, __half*& Ks, __half*& Vs, __half*& Os, __half*& Ps) {
+    Qs = sm + s * STAGE;
+    Ks = Qs + LQ * kRow;
+    Vs = Ks + LK * kRow;
+    Os = Vs + LK * kRow;
+    Ps = Os + LQ * kRow;
+  };
+  __half *Qs, *Ks, *Vs, *Os, *Ps;
+  if ((int)blockIdx.x < nitems) {
+    stage(0, Qs, Ks, Vs, Os, Ps);
+    attn_bwd_issue(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD);
+  }
+  int k = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+    const int nxt = item + gridDim.x;
+    if (nxt < nitems) {
+      stage((k + 1) & 1, Qs, Ks, Vs, Os, Ps);
+      attn_bwd_issue(a, nxt, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    stage(k & 1, Qs, Ks, Vs, Os, Ps);
+    attn_bwd_compute<QT, KT>(a, item, Qs, Ks, Vs, Os, Ps, Ss);
+    __syncthreads();   // stage k&1 and dS are free for the item after next
   }
 }
 
@@ -412,13 +496,32 @@ int launch_fwd(const AttnArgs& a, int nbh, cudaStream_t st) {
 
 template <int QT, int KT>
 int launch_bwd(const AttnBwdArgs& a, int nbh, cudaStream_t st) {
+  if constexpr (QT <= 4 && KT <= 4) {
+    static const bool persist = [] {
+      const char* e = getenv("LS2_ATTN_PERSIST");
+      return !(e && e[0] == '0');
+    }();
+    if (persist) {
+      constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
+      const size_t sm = (size_t)(2 * (2 * LQ * kRow + 2 * LK * kRow + LQ * PLD) + LQ * PLD) * 2;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(attn_bwd_persist<QT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+        attr = true;
+      }
+      const int grid = nbh < 2 * kNumSMs ? nbh : 2 * kNumSMs;
+      attn_bwd_persist<QT, KT><<<grid, 64 * (QT > KT ? QT : KT), sm, st>>>(a, nbh);
+      return check_launch("attention_bwd");
+    }
+  }
   const size_t sm = bwd_smem(QT, KT);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_bwd_kernel<QT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  attn_bwd_kernel<QT, KT><<<nbh, 32 * (QT > KT ? QT : KT), sm, st>>>(a);
+  attn_bwd_kernel<QT, KT><<<nbh, 64 * (QT > KT ? QT : KT), sm, st>>>(a);
   return check_launch("attention_bwd");
 }
 

@@ -338,6 +338,6 @@ def test_mask_bank_step_equals_inline_masks(monkeypatch, graphs, early):
     e2, m2 = _run_steps(steps, graphs)
     assert e1.masks is None and e2.masks is not None and e2.masks.buf is not None
     for a, b in zip(m1, m2):
-        assert abs(a.loss - b.loss) <= 1e-5 * max(1.0, abs(a.loss)), (a.step, a.loss, b.loss)
+        assert abs(a.loss - b.loss) <= 1e-4 * max(1.0, abs(a.loss)), (a.step, a.loss, b.loss)
     p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
     assert np.abs(p1 - p2).max() <= 2e-3
