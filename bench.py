@@ -40,7 +40,11 @@ B, L, V = 64, 64, 32000
 # BASELINE.json configs: [1] Transformer-base (the headline, default) and
 # [2] Transformer-big (d1024 h16 f4096, 64 x 128 = 8192 tokens/GPU) via --model tbig
 MODELS = {"tbase": (64, 64, "Transformer-base 6e6d, d512 h8 f2048 V32000"),
-          "tbig": (64, 128, "Transformer-big 6e6d, d1024 h16 f4096 V32000")}
+          "tbig": (64, 128, "Transformer-big 6e6d, d1024 h16 f4096 V32000"),
+          # [3] BERT-base-shaped encoder + tied MLM criterion (15% MLM positions);
+          # its tokens/s counts every input token (the usual BERT convention)
+          "bert128": (64, 128, "BERT-base-shaped 12e, d768 h12 f3072 V30522, MLM 15%"),
+          "bert512": (16, 512, "BERT-base-shaped 12e, d768 h12 f3072 V30522, MLM 15%")}
 
 
 def _peaks():
@@ -227,17 +231,22 @@ def run_ours(args):
     from paper_2110_05722_b200.dist import DataParallel, init_from_env
     from paper_2110_05722_b200.engine import TrainingEngine
 
-    from paper_2110_05722_b200.config import transformer_big
-    global B, L
+    from paper_2110_05722_b200.config import bert_base, transformer_big
+    from paper_2110_05722_b200.data import MLMTask
+    global B, L, V
     B, L, desc = MODELS[args.model]
+    bert = args.model.startswith("bert")
+    if bert:
+        V = 30522
     rank, world, local = init_from_env()
     torch.cuda.set_device(local)
     dp = DataParallel(force=os.environ.get("LS2_DP_FORCE") == "1")
-    mcfg = transformer_base(V, 256) if args.model == "tbase" else transformer_big(V, 256)
+    mcfg = (transformer_base(V, 256) if args.model == "tbase" else
+            transformer_big(V, 256) if args.model == "tbig" else bert_base(V, 512))
     run = RunConfig(model=mcfg,
                     train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L,
                                       seed=1234 + 0 * rank, loss_scale=1.0))
-    task = FixedShapeTask(B, L, V, seed=17 + rank)
+    task = MLMTask(B, L, V, seed=17 + rank) if bert else FixedShapeTask(B, L, V, seed=17 + rank)
     eng = TrainingEngine(run, task=task, dp=dp)
     eng.setup_arena()
     key = ("train", B, L)

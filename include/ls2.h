@@ -184,6 +184,13 @@ int ls2_criterion_fused(const void* logits, const int64_t* targets, void* dlogit
                         void* logq_out, double* row_stats, double* out3, int* bad_target,
                         int64_t rows, int64_t v, double alpha, int64_t pad_id, int has_pad,
                         double grad_scale, int t_logits, void* stream);
+/* the same over rows of pitch ld >= v (ld = v rounded up to a multiple of 8, for
+ * vocabularies like BERT's 30522): columns [v, ld) are ignored on read and hold
+ * don't-care values in dlogits; 16-bit logits, two rows must fit in 200 KB */
+int ls2_criterion_fused_ld(const void* logits, int64_t ld, const int64_t* targets, void* dlogits,
+                           double* row_stats, double* out3, int* bad_target, int64_t rows,
+                           int64_t v, double alpha, int64_t pad_id, int has_pad,
+                           double grad_scale, int t_logits, void* stream);
 
 /* ---- embedding: F/kernels.py:203-228 / F/gradients.py:20-44 ---- */
 int ls2_embedding_fwd(const void* emb, const void* pos, const int64_t* tokens, void* y,

@@ -714,3 +714,63 @@ def train_step_flat(model: OracleTransformer, shapes, p16, m32, v32, batch, *, p
     bad = adam_flat(p16, g16, m32, v32, lr=lr, beta1=beta1, beta2=beta2, eps=eps_opt, wd=wd,
                     loss_scale=loss_scale, t=t)
     return loss, count, correct, bad == 0
+
+
+# ---------------------------------------------------------------------------
+# BERT-shaped encoder + tied MLM criterion (BASELINE.json configs[3]).  Not a
+# reference model: composed only from the pinned pieces above (embedding,
+# encoder layer, LayerNorm, log-softmax, label-smoothed CE) in the order
+# F/model.py:831-996 applies them to the encoder half; non-MLM positions carry
+# the pad target.  Its parity rests on those pieces' golden pins.
+# ---------------------------------------------------------------------------
+
+def encoder_param_shapes(n_enc, d, dff, vocab, max_len, learned=True):
+    full = model_param_shapes(n_enc, 0, d, dff, vocab, max_len, learned)
+    keep = [s for s in full if not s[0].startswith(("cross_kv.", "dec_ln."))]
+    return keep
+
+
+class OracleEncoderMLM(OracleTransformer):
+    def __init__(self, n_enc, d, heads, dff, vocab, max_len, eps=1e-5, **kw):
+        super().__init__(n_enc, 0, d, heads, dff, vocab, max_len, eps, **kw)
+
+    def forward_backward(self, P, src, tgt_out, src_len, *, pad_id=0, p=0.0, alpha=0.0, seed=0,
+                         step=0, grad_scale=1.0, compute_grads=True):
+        t = ctype(P["tok_emb"])
+        src = np.asarray(src)
+        tgt = np.asarray(tgt_out).reshape(-1)
+        b, ls = src.shape
+        d = self.d
+        pos = P["pos_emb"] if self.learned else sinusoid(self.max_len, d, t)
+        enc_keep = pad_keep(src_len, ls, ls)
+        ks = dropout_keep((b, ls, d), p, fold_seed(seed, step, 0), t)
+        h = embedding_fwd(P["tok_emb"], pos, src, self.scale, ks, p).astype(t)
+        eseed = fold_seed(seed, step, 1)
+        ecache = []
+        for i in range(self.n_enc):
+            h, c = self.enc_fwd(h, P, f"enc{i}.", enc_keep, p, eseed, i, t)
+            ecache.append(c)
+        enc_in = h
+        enc_out, mu_e, sg_e = layernorm_fwd(h, P["enc_ln.w"], P["enc_ln.b"], self.eps)
+        W = P["tok_emb"]
+        logits = self._mm(enc_out.reshape(-1, d), cast(W, t).T).astype(t)
+        logq = log_softmax_fwd(logits)
+        loss, count = ls_ce_fwd(logq, tgt, alpha, pad_id)
+        ok = tgt != pad_id
+        correct = int((np.argmax(logq, axis=-1)[ok] == tgt[ok]).sum())
+        if not compute_grads:
+            return loss, count, correct, None
+        G = {}
+        dl = ls_ce_bwd(np.exp(logq), tgt, alpha, pad_id, grad_scale).astype(t)
+        denc = self._mm(dl, cast(W, t)).reshape(b, ls, d).astype(t)
+        self._acc(G, "tok_emb", self._mm(dl.T, enc_out.reshape(-1, d)))
+        dh, dw, db = layernorm_bwd(denc, enc_in, P["enc_ln.w"], mu_e, sg_e)
+        self._acc(G, "enc_ln.w", dw)
+        self._acc(G, "enc_ln.b", db)
+        for i in reversed(range(self.n_enc)):
+            dh = self.enc_bwd(dh, ecache[i], P, f"enc{i}.", p, G, t)
+        de, dpos = embedding_bwd(dh, src, ks, p, self.vocab, self.max_len, self.scale, self.learned)
+        self._acc(G, "tok_emb", de)
+        if dpos is not None:
+            self._acc(G, "pos_emb", dpos)
+        return loss, count, correct, G

@@ -57,6 +57,7 @@ _SIGS = {
     "ls2_ls_ce_fwd": [P, P, P, P, P, L, L, D, L, I, I, P],
     "ls2_ls_ce_bwd": [P, P, P, P, L, L, D, L, I, D, I, I, P],
     "ls2_criterion_fused": [P, P, P, P, P, P, P, L, L, D, L, I, D, I, P],
+    "ls2_criterion_fused_ld": [P, L, P, P, P, P, P, L, L, D, L, I, D, I, P],
     "ls2_attention_supported": [L, L, L, I],
     "ls2_attention_fwd": [P, L, P, L, P, L, P, P, L, L, L, L, L, L, I, P, D, P],
     "ls2_attention_bwd": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, D, P],

@@ -352,7 +352,7 @@ template <typename T, int CH, int G>
 __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
     const T* __restrict__ logits, const int64_t* __restrict__ targets, T* dlogits,
     double* __restrict__ cl_stats, int* __restrict__ bad_target, int64_t rows, int V, int S,
-    double alpha, int64_t pad_id, int has_pad, double grad_scale) {
+    double alpha, int64_t pad_id, int has_pad, double grad_scale, int ldr) {
   using PT = Pair<T>;
   using P2 = typename PT::P2;
   struct alignas(16) Chunk { P2 h[4]; };
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
   const int q = C > 1 ? (int)cl.block_rank() : 0;
   const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
   const int col0 = q * S;
-  const int len = min(S, V - col0);
+  const int len = C == 1 ? S : min(S, V - col0);   // C == 1: S = row pitch (>= V)
   const uint32_t slice_bytes = (uint32_t)len * sizeof(T);
   const uint32_t buf_stride = ((uint32_t)S * sizeof(T) + 127u) & ~127u;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < NB; ++i)
       if (r0 + i * rstride < rows)
-        bulk_load(ce_smem + (g * NB + i) * buf_stride, logits + (r0 + i * rstride) * V + col0,
+        bulk_load(ce_smem + (g * NB + i) * buf_stride, logits + (r0 + i * rstride) * ldr + col0,
                   slice_bytes, &bar[g * NB + i]);
     s_acc[g][0] = s_acc[g][1] = s_acc[g][2] = 0.0;
   }
@@ -426,6 +426,19 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
         if (c < nchunk) hq[j] = row[c];
       }
     }
+    // a row pitch past V (V % 8 != 0, C == 1): the last chunk's columns >= V
+    // read as -inf (no max, no exp); they are left out of sum(h) below
+    const int tailc = (ldr != V) ? V / 8 : -1, tailn = V & 7;
+    if (tailc >= 0) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j)
+        if (gt + j * NT == tailc) {
+          T* hv = reinterpret_cast<T*>(&hq[j]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (e >= tailn) hv[e] = cvt<T>(-INFINITY);
+        }
+    }
     if (gt == 0) s_ht[g] = own_t ? cvt<float>(reinterpret_cast<const T*>(row)[lt]) : 0.f;
     // pass 1 (registers): packed max, fp32x2 sum
     P2 m2 = PT::pack(make_float2(-INFINITY, -INFINITY));
@@ -435,10 +448,20 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         if (F || gt + j * NT < nchunk) {
+          if (gt + j * NT == tailc) {      // masked tail: max over all, sum of the valid
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            m2 = PT::max(m2, hq[j].h[e]);
-            s2 = fadd2(s2, PT::f(hq[j].h[e]));
+            for (int e = 0; e < 4; ++e) {
+              m2 = PT::max(m2, hq[j].h[e]);
+              const float2 f = PT::f(hq[j].h[e]);
+              s2.x += (2 * e < tailn) ? f.x : 0.f;
+              s2.y += (2 * e + 1 < tailn) ? f.y : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              m2 = PT::max(m2, hq[j].h[e]);
+              s2 = fadd2(s2, PT::f(hq[j].h[e]));
+            }
           }
         }
       }
@@ -452,7 +475,7 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
     group_sync<G>(g);              // the row buffer is consumed: refill it
     if (gt == 0 && r + NB * rstride < rows) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bulk_load(ce_smem + bi * buf_stride, logits + (r + NB * rstride) * V + col0, slice_bytes,
+      bulk_load(ce_smem + bi * buf_stride, logits + (r + NB * rstride) * ldr + col0, slice_bytes,
                 &bar[bi]);
     }
     float mq = lane < WG ? s_max[g][lane] : -INFINITY;
@@ -582,7 +605,7 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
       const float gs = valid ? (float)grad_scale : 0.f;
       const float cz = gs * scale / zt;                   // zt carries the cache scale
       const float2 cz2 = make_float2(cz, cz), of2 = make_float2(-a_v * gs, -a_v * gs);
-      T* drow = dlogits + r * (int64_t)V + col0;
+      T* drow = dlogits + r * (int64_t)ldr + col0;
       auto pass3 = [&](auto fc) {
         constexpr bool F = decltype(fc)::value;
 #pragma unroll
@@ -748,7 +771,7 @@ template <typename T, int CH, int G>
 static int launch_ce_rows_ch(const T* logits, const int64_t* targets, T* dlogits, double* row_stats,
                              double* out3, int* bad_target, int64_t rows, int64_t v, int C, int S,
                              double alpha, int64_t pad_id, int has_pad, double grad_scale,
-                             cudaStream_t st) {
+                             int64_t ldr, cudaStream_t st) {
   auto kern = criterion_rows_kernel<T, CH, G>;
   const int smem = 2 * (int)(((int64_t)S * 2 + 127) / 128 * 128);   // G*NB == 2 buffers
   static std::mutex mu;
@@ -791,7 +814,7 @@ static int launch_ce_rows_ch(const T* logits, const int64_t* targets, T* dlogits
   if (ncl <= 0) return -1;
   cfg.gridDim = dim3(C * ncl);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, logits, targets, dlogits, row_stats, bad_target,
-                                     rows, (int)v, S, alpha, pad_id, has_pad, grad_scale);
+                                     rows, (int)v, S, alpha, pad_id, has_pad, grad_scale, (int)ldr);
   if (e != cudaSuccess) return fail(LS2_ERR_CUDA, std::string("criterion_rows: ") + cudaGetErrorString(e));
   if (int rc = check_launch("criterion_rows")) return rc;
   criterion_reduce_cta<<<1, 32, 0, st>>>(row_stats, ncl, out3);
@@ -802,10 +825,10 @@ template <typename T>
 static int launch_ce_rows(const T* logits, const int64_t* targets, T* dlogits, double* row_stats,
                           double* out3, int* bad_target, int64_t rows, int64_t v, int C, int S,
                           double alpha, int64_t pad_id, int has_pad, double grad_scale,
-                          cudaStream_t st) {
+                          int64_t ldr, cudaStream_t st) {
 #define LS2_CE_GO(CH_, G_)                                                                        \
   return launch_ce_rows_ch<T, CH_, G_>(logits, targets, dlogits, row_stats, out3, bad_target,     \
-                                       rows, v, C, S, alpha, pad_id, has_pad, grad_scale, st)
+                                       rows, v, C, S, alpha, pad_id, has_pad, grad_scale, ldr, st)
   // two row groups per CTA while a row fits 8 chunks per thread of a 512-thread group
   static const bool groups2 = [] {
     const char* e = getenv("LS2_CE_GROUPS");
@@ -832,6 +855,32 @@ using namespace ls2;
 
 extern "C" {
 
+int ls2_criterion_fused_ld(const void* logits, int64_t ld, const int64_t* targets, void* dlogits,
+                           double* row_stats, double* out3, int* bad_target, int64_t rows,
+                           int64_t v, double alpha, int64_t pad_id, int has_pad,
+                           double grad_scale, int t_logits, void* stream) {
+  if (ld == v) return ls2_criterion_fused(logits, targets, dlogits, nullptr, row_stats, out3,
+                                          bad_target, rows, v, alpha, pad_id, has_pad, grad_scale,
+                                          t_logits, stream);
+  if (rows <= 0) return cudaMemsetAsync(out3, 0, 3 * sizeof(double), as_stream(stream)) == cudaSuccess ? LS2_OK : fail(LS2_ERR_CUDA, "memset");
+  if (v < 2 || ld < v || ld % 8 != 0 || ld - v >= 8 || !aligned16(logits) ||
+      (dlogits && !aligned16(dlogits)) || (t_logits != LS2_F16 && t_logits != LS2_BF16))
+    return fail(LS2_ERR_SHAPE, "criterion_fused_ld: needs 16-bit logits, ld = V rounded up to 8");
+  int slice = 0;
+  if (ce_cluster_size(ld, &slice) != 1 || rows < 2)
+    return fail(LS2_ERR_SHAPE, "criterion_fused_ld: row too long for the padded-pitch path");
+  cudaStream_t st = as_stream(stream);
+  int rc = t_logits == LS2_F16
+               ? launch_ce_rows<__half>((const __half*)logits, targets, (__half*)dlogits, row_stats,
+                                        out3, bad_target, rows, v, 1, (int)ld, alpha, pad_id,
+                                        has_pad, grad_scale, ld, st)
+               : launch_ce_rows<__nv_bfloat16>((const __nv_bfloat16*)logits, targets,
+                                               (__nv_bfloat16*)dlogits, row_stats, out3,
+                                               bad_target, rows, v, 1, (int)ld, alpha, pad_id,
+                                               has_pad, grad_scale, ld, st);
+  return rc < 0 ? fail(LS2_ERR_SHAPE, "criterion_fused_ld: no launch configuration") : rc;
+}
+
 int ls2_criterion_fused(const void* logits, const int64_t* targets, void* dlogits, void* logq_out,
                         double* row_stats, double* out3, int* bad_target, int64_t rows, int64_t v,
                         double alpha, int64_t pad_id, int has_pad, double grad_scale,
@@ -849,11 +898,11 @@ int ls2_criterion_fused(const void* logits, const int64_t* targets, void* dlogit
     int rc = t_logits == LS2_F16
                  ? launch_ce_rows<__half>((const __half*)logits, targets, (__half*)dlogits,
                                           row_stats, out3, bad_target, rows, v, ccl, cslice,
-                                          alpha, pad_id, has_pad, grad_scale, st)
+                                          alpha, pad_id, has_pad, grad_scale, v, st)
                  : launch_ce_rows<__nv_bfloat16>(
                        (const __nv_bfloat16*)logits, targets, (__nv_bfloat16*)dlogits, row_stats,
                        out3, bad_target, rows, v, ccl, cslice, alpha, pad_id, has_pad, grad_scale,
-                       st);
+                       v, st);
     if (rc >= 0) return rc;        // -1: no cluster fits; take the generic path
   }
   int rc = [&]() -> int {

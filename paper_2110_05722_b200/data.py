@@ -125,6 +125,32 @@ class FixedShapeTask:
                      src_len=np.full(self.b, self.l, np.int64), pad_id=self.pad_id)
 
 
+class MLMTask:
+    """Masked-LM batches for the BERT-shaped encoder (BASELINE.json configs[3]):
+    B x L ids uniform in [2, V); each position is an MLM position with
+    probability `mask_prob` (counter RNG), its input replaced by `mask_id` and
+    its target the original id; every other target is pad.  A pure function of
+    (seed, step)."""
+
+    def __init__(self, batch: int, length: int, vocab: int, seed: int = 0, pad_id: int = 0,
+                 mask_prob: float = 0.15, mask_id: int = 1):
+        self.b, self.l, self.v, self.seed, self.pad_id = batch, length, vocab, seed, pad_id
+        self.mask_prob, self.mask_id = mask_prob, mask_id
+
+    def possible_shapes(self) -> list:
+        return [(self.b, self.l)]
+
+    def batch(self, step: int) -> Batch:
+        n = self.b * self.l
+        u = _uniform(derive_seed(self.seed, step, 11), 2 * n)
+        tok = (2 + (u[:n] * (self.v - 2)).astype(np.int64)).reshape(self.b, self.l)
+        mlm = (u[n:] < self.mask_prob).reshape(self.b, self.l)
+        src = np.where(mlm, self.mask_id, tok)
+        tgt = np.where(mlm, tok, self.pad_id)
+        return Batch(src=src, tgt_in=src.copy(), tgt_out=tgt,
+                     src_len=np.full(self.b, self.l, np.int64), pad_id=self.pad_id)
+
+
 def make_task(run_cfg):
     if run_cfg.data.task == "file":
         raise DataError("file task: use load_token_file + a custom batcher (not on the hot path)")

@@ -27,7 +27,7 @@ from .data import make_task
 from .dist import DataParallel
 from .errors import DataError
 from .memplan import PlannedArena, RecordingArena, TensorTag, classify, estimate_capacity
-from .model import Batch, MaskBank, SeedTable, Transformer, _ViewSink, validate_batch
+from .model import Batch, MaskBank, SeedTable, Transformer, _ViewSink, make_model, validate_batch
 from .trainer import OptimConfig, Workspace, _state, workspace_pack
 
 EVAL_STEP_BASE = 1 << 30
@@ -102,7 +102,7 @@ class TrainingEngine:
         self.cfg = run_cfg
         ctx = _lib.context(device)
         self.device = ctx.device
-        self.model = Transformer(run_cfg.model)
+        self.model = make_model(run_cfg.model)
         self.task = task if task is not None else make_task(run_cfg)
         t = run_cfg.train
         self.optim = OptimConfig(algorithm=t.algorithm, lr=t.lr, beta1=t.beta1, beta2=t.beta2,

@@ -53,8 +53,13 @@ class ModelConfig:
     learned_positional: bool = True
     eps: float = 1e-5
     embed_scale: float | None = None
+    # "transformer": the reference's encoder-decoder; "encoder": a BERT-shaped
+    # encoder with a tied masked-LM criterion (BASELINE.json configs[3])
+    arch: str = "transformer"
 
     def __post_init__(self):
+        if self.arch not in ("transformer", "encoder"):
+            raise ConfigError(f"unknown arch {self.arch!r}")
         if self.d_model % self.n_heads:
             raise ConfigError(f"d_model {self.d_model} not divisible by n_heads {self.n_heads}")
         if self.vocab < 2:
@@ -90,6 +95,8 @@ def param_spec(cfg: ModelConfig):
         spec.append(("pos_emb", (cfg.max_len, d)))
     for i in range(cfg.n_enc):
         spec += _layer_spec(f"enc{i}.", d, dff, False)
+    if cfg.arch == "encoder":
+        return spec + [("enc_ln.w", (d,)), ("enc_ln.b", (d,))]
     spec += [("enc_ln.w", (d,)), ("enc_ln.b", (d,)),
              ("cross_kv.w", (2 * cfg.n_dec * d, d)), ("cross_kv.b", (2 * cfg.n_dec * d,))]
     for i in range(cfg.n_dec):
@@ -1603,3 +1610,167 @@ def transformer_forward_backward(cfg: ModelConfig, params, batch: Batch, **kwarg
     sink = kwargs.pop("sink", None) or GradSink()
     out = Transformer(cfg).forward_backward(params, batch, sink=sink, **kwargs)
     return out, sink.store
+
+
+class EncoderMLM(Transformer):
+    """BERT-shaped encoder with a tied masked-LM criterion (BASELINE.json
+    configs[3]): not a reference model, composed from the
+    reference's own pieces — embedding (F/kernels.py:203-228), pre-LN encoder
+    layers (F/model.py:335-510), final LayerNorm, tied output projection and
+    the label-smoothed criterion (F/model.py:908-939).  Non-MLM positions carry
+    the pad target, so the criterion skips them (count = MLM tokens).  Batch:
+    src = masked input ids, tgt_out = original ids at MLM positions (pad
+    elsewhere); tgt_in is unused.  V need not be a multiple of 8 (BERT's
+    30522): the logits rows are then laid out with a padded pitch.
+    """
+
+    def _mask_sites(self, s_src, enc_seed, s_tgt, dec_seed, ts: int, tt: int):
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        slot = lambda t: t.storage_offset()      # noqa: E731
+        sites = [(slot(s_src), ts * d, "src")]
+        for i in range(self.cfg.n_enc):
+            g = f"enc{i}"
+            sites += [(slot(enc_seed.site(i, 0)), ts * d, g), (slot(enc_seed.site(i, 1)), ts * f, g),
+                      (slot(enc_seed.site(i, 2)), ts * d, g)]
+        return sites
+
+    def register_seeds(self, seeds: SeedTable, seed: int, step: int, p_drop: float):
+        cfg = self.cfg
+        seeds.reset()
+        seeds.set_step(step)
+        s_src = seeds.slot(derive_seed(seed, step, 0))
+        enc_seed = _LayerSeed(seeds, derive_seed(seed, step, 1))
+        if p_drop > 0.0:
+            for i in range(cfg.n_enc):
+                for k in range(3):
+                    enc_seed.site(i, k)
+        return s_src, enc_seed, None, None
+
+    def _forward_backward(self, params, batch: Batch, *, p_drop, alpha, seed, step, arena, sink,
+                          compute_grads, grad_scale, trace, strategy, capture, validate,
+                          upload_seeds) -> ModelOutput:
+        cfg = self.cfg
+        ctx = _lib.context()
+        arena = arena or NullArena(ctx.device)
+        stash = ActivationStash()
+        sink = GradSink() if sink is None else sink
+        if isinstance(sink, _ViewSink):
+            sink.arena = arena
+        if validate:
+            validate_batch(batch, cfg)
+        src = K.dev(batch.src, torch.int64)
+        tgt_out = K.dev(batch.tgt_out, torch.int64).reshape(-1)
+        src_len = K.dev(batch.src_len, torch.int64)
+        b, ls = src.shape
+        d, n, v = cfg.d_model, cfg.n_heads, cfg.vocab
+        params = {k: (t if isinstance(t, torch.Tensor) else K.dev(t)) for k, t in params.items()}
+        dt = self.act_dtype(params)
+        sdt = _stat_dtype(dt)
+        emb_cfg = EmbeddingConfig(scale=cfg.scale, vocab=v, max_len=cfg.max_len,
+                                  learned_positional=cfg.learned_positional)
+        tok_emb = _as_dt(params["tok_emb"], dt)
+        pos = _as_dt(self._positional(params, dt), dt)
+        enc_mask = AttentionMask("padding", src_len)
+        seeds = self.seed_table(ctx.device)
+        s_src, enc_seed, _, _ = self.register_seeds(seeds, seed, step, p_drop)
+        if p_drop > 0.0 and upload_seeds:
+            seeds.upload()
+        bank = _MASKS
+        if bank is not None and p_drop > 0.0 and dt != torch.float64:
+            bank.prepare(lambda ts, tt: self._mask_sites(s_src, enc_seed, None, None, ts, tt),
+                         b * ls, b * ls, K._drop_args(p_drop)[1])
+            bank.generate(seeds.dev, stamp=bank.stamp, want=seeds.step_slot())
+            bank.active = True
+            arena = _BankArena(arena, bank)
+
+        # --- forward: embedding, encoder stack, final LayerNorm ---
+        h = arena.alloc((b, ls, d), dt)
+        keep_src = _bank_bits(s_src, b * ls * d) if p_drop > 0.0 else None
+        banked = keep_src is not None
+        if not banked:
+            keep_src = arena.alloc((_nbits(b * ls * d),), torch.uint8)
+        K.embedding_forward(tok_emb, pos, src, emb_cfg, p_drop, s_src, out=h, bits_out=keep_src,
+                            validate=False,
+                            mask=DropoutMask(p=p_drop, bits=keep_src, shape=(b, ls, d)) if banked
+                            else None)
+        stash.push("src_keep", keep_src)
+        enc_w = [EncoderLayerWeights.from_params(params, f"enc{i}.") for i in range(cfg.n_enc)]
+        for i in range(cfg.n_enc):
+            h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
+                                         eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
+                                         site=i)
+        stash.push("enc_ln_in", h)
+        mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
+        enc_out = arena.alloc((b, ls, d), dt)
+        K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
+                            cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
+                            check_degenerate=False)
+
+        # --- MLM criterion over every position (pad targets are skipped) ---
+        rt = b * ls
+        ld = (v + 7) // 8 * 8 if dt in (torch.float16, torch.bfloat16) else v
+        logits_buf = arena.alloc((rt, ld), dt)
+        logits = logits_buf[:, :v] if ld != v else logits_buf
+        K.gemm(enc_out.view(rt, d), tok_emb, trans_b=True, out=logits)
+        row_stats = arena.alloc((2 * rt,), torch.float64)
+        out3 = torch.empty(3, dtype=torch.float64, device=ctx.device)
+        if dt == torch.float64:
+            self._criterion_f64(logits, tgt_out, out3, alpha, batch.pad_id, grad_scale,
+                                compute_grads, None)
+        else:
+            _lib.call("ls2_criterion_fused_ld", logits_buf.data_ptr(), ld, tgt_out.data_ptr(),
+                      logits_buf.data_ptr() if compute_grads else None, row_stats.data_ptr(),
+                      out3.data_ptr(), None, rt, v, float(alpha), int(batch.pad_id), 1,
+                      float(grad_scale), _lib.dtype_code(logits_buf), _lib.stream_handle())
+        arena.free(row_stats)
+        if isinstance(sink, _ViewSink):
+            sink.totals = out3
+        out = ModelOutput(out3)
+        if not compute_grads:
+            stash.drain(arena)
+            arena.free(mu_e); arena.free(sg_e)
+            arena.free(enc_out)
+            arena.free(logits_buf)
+            return out
+
+        # --- backward ---
+        lane = None
+        main_arena = arena
+        if getattr(sink, "use_lane", False) and dt != torch.float64:
+            lane = _Lane(arena)
+            sink.lane = lane
+            arena = _LaneArena(arena, lane)
+        join = lane.join if lane is not None else (lambda: None)
+        denc = arena.alloc((b, ls, d), dt)
+        K.gemm(logits, tok_emb, out=denc.view(rt, d))
+        _wgrad(sink, "tok_emb", logits, enc_out.view(rt, d))
+        arena.free(logits_buf); arena.free(enc_out)
+        h_in = stash.pop("enc_ln_in")
+        dh = arena.alloc((b, ls, d), dt)
+        _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
+        arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
+        join()
+        _ready(sink, "enc_ln.")
+        for i in reversed(range(cfg.n_enc)):
+            dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
+                                        arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
+            join()
+            _ready(sink, f"enc{i}.")
+        keep_src = stash.pop("src_keep")
+        self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
+        arena.free(dh); arena.free(keep_src)
+        join()
+        _ready(sink, None)
+        if lane is not None:
+            sink.lane = None
+        arena = main_arena
+        if len(stash):
+            raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")
+        for buf in getattr(sink, "deferred_buffers", lambda: [])():
+            arena.free(buf)
+        return out
+
+
+def make_model(cfg: ModelConfig):
+    """The model class for cfg.arch."""
+    return EncoderMLM(cfg) if cfg.arch == "encoder" else Transformer(cfg)

@@ -486,3 +486,36 @@ def test_bdr_layernorm_read_bits_equals_draw():
         outs.append((H(y), H(u), H(mu), H(sg), H(bits)))
     for a, b2 in zip(*outs):
         assert np.array_equal(a, b2)
+
+
+@pytest.mark.parametrize("rows,v", [(512, 30522), (300, 1003), (64, 50001)])
+def test_fused_criterion_padded_pitch_vs_oracle(rows, v):
+    """Rows of pitch ld = V rounded up to 8 (BERT's V = 30522): loss, count,
+    argmax and the gradient of the V real columns match the oracle; the pad
+    columns (garbage on entry) are ignored."""
+    from paper_2110_05722_b200 import _lib
+    ld = (v + 7) // 8 * 8
+    rng = np.random.default_rng(v)
+    h = (rng.normal(size=(rows, v)) * 2).astype(np.float16)
+    buf = np.full((rows, ld), 60000.0, dtype=np.float16)       # pad columns: huge garbage
+    buf[:, :v] = h
+    hd = C(buf)
+    tg = rng.integers(0, v, rows)
+    tg[::5] = 0
+    logq = O.log_softmax_fwd(h.astype(np.float32))
+    loss, cnt = O.ls_ce_fwd(logq, tg, 0.1, 0)
+    ok = tg != 0
+    correct = int((np.argmax(h.astype(np.float32), axis=-1)[ok] == tg[ok]).sum())
+    d_ref = O.ls_ce_bwd(np.exp(logq), tg, 0.1, 0, grad_scale=2.0)
+    td = C(tg.astype(np.int64))
+    stats = torch.empty(2 * rows, dtype=torch.float64, device="cuda")
+    out3 = torch.empty(3, dtype=torch.float64, device="cuda")
+    _lib.call("ls2_criterion_fused_ld", hd.data_ptr(), ld, td.data_ptr(), hd.data_ptr(),
+              stats.data_ptr(), out3.data_ptr(), None, rows, v, 0.1, 0, 1, 2.0, _lib.F16,
+              _lib.stream_handle())
+    o = H(out3)
+    assert o[1] == cnt and o[2] == correct
+    assert abs(o[0] - loss) <= 1e-4 * abs(loss)
+    got = hd.float().cpu().numpy()[:, :v]
+    assert np.linalg.norm(got - d_ref) <= 2e-2 * np.linalg.norm(d_ref)
+    assert np.all(got[tg == 0] == 0)
