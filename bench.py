@@ -147,8 +147,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    # one sequence per step keeps the default --steps 200 run to about a minute
-    seqs = 1
+    # each step is a bounded sample of the T-base step: as many sequences as keep
+    # the whole --steps/--warmup run near 2.5 minutes (~0.27 s per sequence on
+    # 16 host cores), between 1 and 8 (numpy/OpenBLAS run bigger batches better)
+    seqs = max(1, min(8, int(150.0 / (0.27 * (args.steps + args.warmup)))))
     st = oracle_sample_setup(seqs)
     for s in range(args.warmup):
         oracle_sample_step(st, s)
