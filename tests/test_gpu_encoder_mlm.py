@@ -11,10 +11,11 @@ from oracle import lsport as O
 
 pytestmark = pytest.mark.gpu
 
+from paper_2110_05722_b200 import model as M                 # host-importable (no GPU needed)
+from paper_2110_05722_b200.config import RunConfig, TrainConfig
+from paper_2110_05722_b200.data import MLMTask
+
 if torch.cuda.is_available():
-    from paper_2110_05722_b200 import model as M
-    from paper_2110_05722_b200.config import RunConfig, TrainConfig
-    from paper_2110_05722_b200.data import MLMTask
     from paper_2110_05722_b200.engine import TrainingEngine
 
 
