@@ -167,6 +167,16 @@ int ls2_attention_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, co
                       int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
                       int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
                       double scale, void* stream);
+/* the same, also leaving the projection biases' gradient partials: row b of
+ * csq / csk / csv (f64, row pitch ld*, columns h*64..h*64+63) = column sums over
+ * the sequence of the stored dQ / dK / dV of (b, h); any may be NULL.  Summing
+ * the B rows (fixed order) gives dbias — the engine's deferred finish does it. */
+int ls2_attention_bwd_bias(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                           int64_t ldv, const void* probs, const void* dout, int64_t lddo,
+                           void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                           int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
+                           double scale, double* csq, int64_t ldcsq, double* csk, int64_t ldcsk,
+                           double* csv, int64_t ldcsv, void* stream);
 
 /* ---- label-smoothed CE: F/kernels.py:338-360, F/gradients.py:47-74 ----
  * row_stats (double[rows*2]) receives per-row (loss, correct) partials;

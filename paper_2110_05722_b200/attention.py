@@ -50,7 +50,17 @@ def forward(q, ldq, k, ldk, v, ldv, probs, o, ldo, batch, heads, lq, lk, hd, mas
 
 
 def backward(q, ldq, k, ldk, v, ldv, probs, dout, lddo, dq, lddq, dk, lddk, dv, lddv, batch,
-             heads, lq, lk, hd, scale):
-    _lib.call("ls2_attention_bwd", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(), ldv,
+             heads, lq, lk, hd, scale, colsums=None):
+    """colsums: optional ((buf, col0, ld) or None) x 3 for dQ, dK, dV — f64 rows of
+    per-batch column sums (the projection biases' gradient partials)."""
+    cs = []
+    for c in (colsums or (None, None, None)):
+        if c is None:
+            cs += [None, 0]
+        else:
+            buf, col0, ld = c
+            cs += [buf.data_ptr() + 8 * col0, ld]
+    _lib.call("ls2_attention_bwd_bias", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(), ldv,
               probs.data_ptr(), dout.data_ptr(), lddo, dq.data_ptr(), lddq, dk.data_ptr(), lddk,
-              dv.data_ptr(), lddv, batch, heads, lq, lk, hd, float(scale), _lib.stream_handle())
+              dv.data_ptr(), lddv, batch, heads, lq, lk, hd, float(scale), *cs,
+              _lib.stream_handle())

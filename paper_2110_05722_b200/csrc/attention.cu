@@ -240,7 +240,51 @@ struct AttnBwdArgs {
   int64_t lddq, lddk, lddv;
   int H, Lq, Lk;
   float scale;
+  // optional bias-gradient partials (the projection biases' column sums of the
+  // stored dQ / dK / dV): row b, columns h*64.. of each, f64, one row per batch
+  double *csq, *csk, *csv;
+  int64_t ldcsq, ldcsk, ldcsv;
 };
+
+// column sums of one warp's 16-row tile of a result (the fp16-rounded values
+// the kernel stores; rows >= valid excluded), folded over the 8 row lanes in a
+// fixed order; lanes 0..3 leave columns 8j + 2t, +1 in cs[0..63]
+__device__ __forceinline__ void tile_colsum(const float (&acc)[8][4], int r0, int valid,
+                                            float* cs, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v0 = r0 < valid ? unpack_h2(pack_h2(acc[j][0], acc[j][1])) : make_float2(0.f, 0.f);
+    const float2 v1 = r0 + 8 < valid ? unpack_h2(pack_h2(acc[j][2], acc[j][3])) : make_float2(0.f, 0.f);
+    float sx = v0.x + v1.x, sy = v0.y + v1.y;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    if (g == 0) {
+      cs[8 * j + 2 * t] = sx;
+      cs[8 * j + 2 * t + 1] = sy;
+    }
+  }
+}
+
+// fold the per-warp tile sums in warp order and write the f64 partial rows
+template <int QT, int KT>
+__device__ __forceinline__ void attn_bwd_colsum_store(const AttnBwdArgs& a, int bh, const float* cs) {
+  constexpr int NW = QT > KT ? QT : KT;
+  const int b = bh / a.H, h = bh % a.H;
+  for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) {
+    const int which = i >> 6, c = i & 63;
+    double* dst = which == 0 ? a.csq : which == 1 ? a.csk : a.csv;
+    if (!dst) continue;
+    const int64_t ld = which == 0 ? a.ldcsq : which == 1 ? a.ldcsk : a.ldcsv;
+    const int nw = which == 0 ? QT : KT;
+    float sacc = 0.f;
+    for (int w = 0; w < nw; ++w) sacc += cs[(which * NW + w) * 64 + c];
+    dst[(int64_t)b * ld + h * kHd + c] = (double)sacc;
+  }
+}
 
 __device__ __forceinline__ void store_rows(__half* gbase, int64_t ld, const __half* s, int rows) {
   for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) {
@@ -291,7 +335,8 @@ __device__ __forceinline__ void attn_bwd_issue(const AttnBwdArgs& a, int bh, __h
 template <int QT, int KT>
 __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, const __half* Qs,
                                                  const __half* Ks, const __half* Vs,
-                                                 const __half* Os, const __half* Ps, __half* Ss) {
+                                                 const __half* Os, const __half* Ps, __half* Ss,
+                                                 float* cs) {
   constexpr int PLD = 16 * KT + kPad;
   constexpr int NW = QT > KT ? QT : KT;
   const int b = bh / a.H, h = bh % a.H;
@@ -363,6 +408,7 @@ __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, c
       if (r0 < a.Lk) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dv[j][0], dv[j][1]);
       if (r1 < a.Lk) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dv[j][2], dv[j][3]);
     }
+    if (a.csv) tile_colsum(dv, r0, a.Lk, cs + (2 * NW + tw) * 64, lane);
   }
   __syncthreads();
   // ---- phase B ----
@@ -390,6 +436,7 @@ __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, c
       if (r0 < a.Lq) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dq[j][0], dq[j][1]);
       if (r1 < a.Lq) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dq[j][2], dq[j][3]);
     }
+    if (a.csq) tile_colsum(dq, r0, a.Lq, cs + tw * 64, lane);
   } else if (!qw && tw < KT) {
     float dk[8][4];
 #pragma unroll
@@ -414,6 +461,7 @@ __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, c
       if (r0 < a.Lk) *reinterpret_cast<uint32_t*>(d0 + 8 * j) = pack_h2(dk[j][0], dk[j][1]);
       if (r1 < a.Lk) *reinterpret_cast<uint32_t*>(d1 + 8 * j) = pack_h2(dk[j][2], dk[j][3]);
     }
+    if (a.csk) tile_colsum(dk, r0, a.Lk, cs + (NW + tw) * 64, lane);
   }
 }
 
@@ -429,10 +477,15 @@ attn_bwd_kernel(AttnBwdArgs a) {
   __half* Os = Vs + LK * kRow;        // dO [LQ][72]
   __half* Ps = Os + LQ * kRow;        // [LQ][LK+8]
   __half* Ss = Ps + LQ * PLD;         // dS [LQ][LK+8]
+  float* cs = reinterpret_cast<float*>(Ss + LQ * PLD);   // [3][NW][64] bias-grad tile sums
   attn_bwd_issue(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD);
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  attn_bwd_compute<QT, KT>(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, Ss);
+  attn_bwd_compute<QT, KT>(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, Ss, cs);
+  if (a.csq || a.csk || a.csv) {
+    __syncthreads();
+    attn_bwd_colsum_store<QT, KT>(a, blockIdx.x, cs);
+  }
 }
 
 // Persistent, double-buffered (tiles up to 64 x 64, two CTAs per SM): a CTA
@@ -444,8 +497,11 @@ __global__ void __launch_bounds__(64 * (QT > KT ? QT : KT), 2)
 attn_bwd_persist(AttnBwdArgs a, int nitems) {
   constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
   constexpr int STAGE = 2 * LQ * kRow + 2 * LK * kRow + LQ * PLD;   // halves
+  constexpr int NW = QT > KT ? QT : KT;
   extern __shared__ __align__(16) __half sm[];
   __half* Ss = sm + 2 * STAGE;
+  float* cs0 = reinterpret_cast<float*>(Ss + LQ * PLD);   // [2 parity][3][NW][64]
+  const bool colsum = a.csq || a.csk || a.csv;
   auto stage = [&](int s, __half*& Qs, __half*& Ks, __half*& Vs, __half*& Os, __half*& Ps) {
     Qs = sm + s * STAGE;
     Ks = Qs + LQ * kRow;
@@ -470,8 +526,11 @@ attn_bwd_persist(AttnBwdArgs a, int nitems) {
     }
     __syncthreads();
     stage(k & 1, Qs, Ks, Vs, Os, Ps);
-    attn_bwd_compute<QT, KT>(a, item, Qs, Ks, Vs, Os, Ps, Ss);
+    float* cs = cs0 + (k & 1) * 3 * NW * 64;
+    attn_bwd_compute<QT, KT>(a, item, Qs, Ks, Vs, Os, Ps, Ss, cs);
     __syncthreads();   // stage k&1 and dS are free for the item after next
+    // the tile sums are parity-buffered, so this fold overlaps the next item
+    if (colsum) attn_bwd_colsum_store<QT, KT>(a, item, cs);
   }
 }
 
@@ -479,7 +538,9 @@ inline size_t fwd_smem(int qt, int kt) {
   return (size_t)(16 * qt * kRow + 2 * 16 * kt * kRow + 16 * qt * (16 * kt + kPad)) * 2;
 }
 inline size_t bwd_smem(int qt, int kt) {
-  return (size_t)(2 * 16 * qt * kRow + 2 * 16 * kt * kRow + 2 * 16 * qt * (16 * kt + kPad)) * 2;
+  const int nw = qt > kt ? qt : kt;
+  return (size_t)(2 * 16 * qt * kRow + 2 * 16 * kt * kRow + 2 * 16 * qt * (16 * kt + kPad)) * 2 +
+         (size_t)3 * nw * 64 * 4;
 }
 
 template <int QT, int KT>
@@ -503,7 +564,9 @@ int launch_bwd(const AttnBwdArgs& a, int nbh, cudaStream_t st) {
     }();
     if (persist) {
       constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
-      const size_t sm = (size_t)(2 * (2 * LQ * kRow + 2 * LK * kRow + LQ * PLD) + LQ * PLD) * 2;
+      constexpr int NW = QT > KT ? QT : KT;
+      const size_t sm = (size_t)(2 * (2 * LQ * kRow + 2 * LK * kRow + LQ * PLD) + LQ * PLD) * 2 +
+                        (size_t)2 * 3 * NW * 64 * 4;
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(attn_bwd_persist<QT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -568,11 +631,23 @@ int ls2_attention_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, co
                       int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
                       int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
                       double scale, void* stream) {
+  return ls2_attention_bwd_bias(q, ldq, k, ldk, v, ldv, probs, dout, lddo, dq, lddq, dk, lddk, dv,
+                                lddv, batch, heads, lq, lk, hd, scale, nullptr, 0, nullptr, 0,
+                                nullptr, 0, stream);
+}
+
+int ls2_attention_bwd_bias(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                           int64_t ldv, const void* probs, const void* dout, int64_t lddo,
+                           void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                           int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
+                           double scale, double* csq, int64_t ldcsq, double* csk, int64_t ldcsk,
+                           double* csv, int64_t ldcsv, void* stream) {
   if (!ls2_attention_supported(lq, lk, hd, LS2_F16))
     return fail(LS2_ERR_SHAPE, "attention_bwd: needs fp16, hd == 64, L <= 128");
   AttnBwdArgs a{(const __half*)q, (const __half*)k, (const __half*)v, (const __half*)probs,
                 (const __half*)dout, ldq, ldk, ldv, lddo, (__half*)dq, (__half*)dk, (__half*)dv,
-                lddq, lddk, lddv, (int)heads, (int)lq, (int)lk, (float)scale};
+                lddq, lddk, lddv, (int)heads, (int)lq, (int)lk, (float)scale,
+                csq, csk, csv, ldcsq, ldcsk, ldcsv};
   const int qt = tiles_of((int)lq), kt = tiles_of((int)lk);
   const int nbh = (int)(batch * heads);
   cudaStream_t st = as_stream(stream);

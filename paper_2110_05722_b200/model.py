@@ -260,7 +260,7 @@ def packed_kv_forward(enc_out, pw: PackedCrossWeights, arena=None):
 
 
 def packed_kv_backward(dks, dvs, enc_out, pw: PackedCrossWeights, arena=None, packed=None,
-                       sink=None):
+                       sink=None, bias_done: bool = False):
     """dx = sum_i Wkey_i^T dK_i + Wval_i^T dV_i via one packed GEMM; (dx, dw, db).
 
     Raises IncompleteGradientSet unless every decoder layer contributed.  When
@@ -288,7 +288,8 @@ def packed_kv_backward(dks, dvs, enc_out, pw: PackedCrossWeights, arena=None, pa
     dw = db = None
     if sink is not None:
         _wgrad(sink, "cross_kv.w", dy2, e2)
-        _colsum_grad(sink, "cross_kv.b", dy2)
+        if not bias_done:          # else: left by the attention backward kernels
+            _colsum_grad(sink, "cross_kv.b", dy2)
     else:
         dw = K.gemm(dy2, e2, trans_a=True)
         db = G.column_sum(dy2)
@@ -1041,11 +1042,17 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dpro
     K.gemm(dproj.view(r, d), _as_dt(w.wo, dt), out=dctxm.view(r, d))
     _wgrad(sink, pp + "attn.wo", dproj.view(r, d), ctxm.view(r, d))
     arena.free(dproj); arena.free(ctxm)
+    bias_done = False
     if ATT.fused_ok(dt, l, l, hd, AttentionMask("none")):
         dqkv = arena.alloc((b, l, 3 * d), dt)
+        # the qkv bias gradient leaves the kernel as per-batch column partials
+        part = _defer(sink, [pp + "attn.bqkv"], b, 1, 3 * d)
         ATT.backward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
                      probs, dctxm, d, dqkv[..., :d], 3 * d, dqkv[..., d:2 * d], 3 * d,
-                     dqkv[..., 2 * d:], 3 * d, b, n_heads, l, l, hd, 1.0 / math.sqrt(hd))
+                     dqkv[..., 2 * d:], 3 * d, b, n_heads, l, l, hd, 1.0 / math.sqrt(hd),
+                     colsums=None if part is None else
+                     ((part, 0, 3 * d), (part, d, 3 * d), (part, 2 * d, 3 * d)))
+        bias_done = part is not None
         arena.free(probs); arena.free(dctxm); arena.free(qkv)
     else:
         dctx = _heads(dctxm, n_heads)
@@ -1063,7 +1070,8 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dpro
     du1 = arena.alloc((b, l, d), dt)
     K.gemm(dqkv.view(r, 3 * d), _as_dt(w.wqkv, dt), out=du1.view(r, d))
     _wgrad(sink, pp + "attn.wqkv", dqkv.view(r, 3 * d), u1.view(r, d))
-    _colsum_grad(sink, pp + "attn.bqkv", dqkv.view(r, 3 * d))
+    if not bias_done:
+        _colsum_grad(sink, pp + "attn.bqkv", dqkv.view(r, 3 * d))
     arena.free(dqkv); arena.free(u1)
     dx = arena.alloc((b, l, d), dt)
     _ln_bwd(sink, pp, "ln1", du1, x_in, w.ln1_w, mu1, sg1, dx, dy1)
@@ -1129,11 +1137,14 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
 
 def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStash, sink: GradSink,
                            *, n_heads, p_drop, arena=None, prefix="", param_prefix="",
-                           dkv_out=None):
+                           dkv_out=None, kv_colsum=None):
     """Backward of one decoder layer; returns (dx, dK_i, dV_i).
 
     dkv_out: optional (dK_i, dV_i) destination views (slices of the packed
-    cross-K/V gradient buffer) so packed_kv_backward needs no gather copy."""
+    cross-K/V gradient buffer) so packed_kv_backward needs no gather copy.
+    kv_colsum: optional (partial buffer, K column, V column, row pitch): the
+    fused attention backward leaves this layer's share of the packed cross-K/V
+    bias gradient there."""
     arena = arena or NullArena()
     dy = dy if isinstance(dy, torch.Tensor) else K.dev(dy)
     k_i, v_i = kv
@@ -1153,6 +1164,7 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     K.gemm(dproj_x.view(r, d), _as_dt(w.cross_wo, dt), out=dctxm_x.view(r, d))
     _wgrad(sink, pp + "cross.wo", dproj_x.view(r, d), ctxm_x.view(r, d))
     arena.free(dproj_x); arena.free(ctxm_x)
+    cross_bias_done = False
     if ATT.fused_ok(dt, l, ls, hd, AttentionMask("none")) and k_i.dtype == dt and \
             v_i.dtype == dt and (dkv_out is None or dkv_out[0].dtype == dt):
         dqc = arena.alloc((b, l, d), dt)
@@ -1160,9 +1172,16 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
             dk_i, dv_i = dkv_out
         else:
             dk_i, dv_i = arena.alloc((b, ls, d), dt), arena.alloc((b, ls, d), dt)
+        part_q = _defer(sink, [pp + "cross.bq"], b, 1, d)
+        kvcs = (None, None)
+        if kv_colsum is not None and dkv_out is not None:
+            kbuf, kcol, vcol, kld = kv_colsum
+            kvcs = ((kbuf, kcol, kld), (kbuf, vcol, kld))
         ATT.backward(qc, d, k_i, k_i.stride(1), v_i, v_i.stride(1), probs_x, dctxm_x, d,
                      dqc, d, dk_i, dk_i.stride(1), dv_i, dv_i.stride(1), b, n_heads, l, ls, hd,
-                     1.0 / math.sqrt(hd))
+                     1.0 / math.sqrt(hd),
+                     colsums=(None if part_q is None else (part_q, 0, d), kvcs[0], kvcs[1]))
+        cross_bias_done = part_q is not None
         arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
     else:
         dctx_x = _heads(dctxm_x, n_heads)
@@ -1183,7 +1202,8 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     du2 = arena.alloc((b, l, d), dt)
     K.gemm(dqc.view(r, d), _as_dt(w.cross_wq, dt), out=du2.view(r, d))
     _wgrad(sink, pp + "cross.wq", dqc.view(r, d), u2.view(r, d))
-    _colsum_grad(sink, pp + "cross.bq", dqc.view(r, d))
+    if not cross_bias_done:
+        _colsum_grad(sink, pp + "cross.bq", dqc.view(r, d))
     arena.free(dqc); arena.free(u2)
     y1 = stash.pop(p + "y1")
     keep1 = stash.pop(p + "keep1")
@@ -1526,11 +1546,16 @@ class Transformer:
         nd = cfg.n_dec
         dks: list = [None] * nd
         dvs: list = [None] * nd
+        # the packed cross-K/V bias gradient as per-batch partials left by the
+        # fused attention backward of every decoder layer (its own columns)
+        kvpart = _defer(sink, ["cross_kv.b"], b, 1, 2 * nd * d) \
+            if ATT.fused_ok(dt, lt, ls, d // n, AttentionMask("none")) else None
         for i in reversed(range(nd)):
             dest = (dkv[..., i * d:(i + 1) * d], dkv[..., (nd + i) * d:(nd + i + 1) * d])
             dg, dks[i], dvs[i] = decoder_layer_backward(
                 dg, dec_w[i], kv_pairs[i], stash, sink, n_heads=n, p_drop=p_drop, arena=arena,
-                prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest)
+                prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest,
+                kv_colsum=None if kvpart is None else (kvpart, i * d, (nd + i) * d, 2 * nd * d))
             join()
             _ready(sink, f"dec{i}.")
             emit(("dec_layer_backward_done", i))
@@ -1541,7 +1566,8 @@ class Transformer:
 
         # --- backward: packed cross K/V (only now is the enc grad legal) ---
         enc_out = stash.pop("enc_out")
-        denc, _, _ = packed_kv_backward(dks, dvs, enc_out, pw, arena=arena, packed=dkv, sink=sink)
+        denc, _, _ = packed_kv_backward(dks, dvs, enc_out, pw, arena=arena, packed=dkv, sink=sink,
+                                        bias_done=kvpart is not None)
         emit(("enc_out_grad_emitted",))
         arena.free(dkv)
         arena.free(enc_out)
