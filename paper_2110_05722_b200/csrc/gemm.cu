@@ -130,16 +130,21 @@ namespace ls2 {
 // scratch D so C is left untouched.  Off unless LS2_GEMM_TUNE=1 (the
 // heuristic's first choice is taken otherwise).  Reduction schemes are restricted to fp32
 // workspace reductions (no fp16 split-K partial sums, no in-place atomics).
-static bool tuning_enabled() {
-  // off by default: candidates timed in isolation (hot L2, one kernel at a time)
-  // picked algorithms that were slower inside the real step (3.67 vs 3.60 ms at
-  // T-base on the same box); LS2_GEMM_TUNE=1 turns it on
+// off by default: candidates timed in isolation (hot L2, one kernel at a time)
+// picked algorithms that were slower inside the real step (3.67 vs 3.60 ms at
+// T-base on the same box).  LS2_GEMM_TUNE=1 tunes every GEMM, =w only the
+// weight-gradient ones (fp32 output).
+static int tuning_mode() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("LS2_GEMM_TUNE");
-    on = (e && e[0] == '1') ? 1 : 0;
+    on = !e ? 0 : e[0] == '1' ? 1 : e[0] == 'w' ? 2 : 0;
   }
-  return on == 1;
+  return on;
+}
+static bool tuning_enabled(int tc = -1) {
+  const int m = tuning_mode();
+  return m == 1 || (m == 2 && tc == LS2_F32);
 }
 
 // Candidates are timed as a CUDA graph of kTuneReps back-to-back launches on a
@@ -153,7 +158,7 @@ static void lt_tune(Blas* bl, LtPlan* plan, const cublasLtMatmulHeuristicResult_
   plan->algo = res[0].algo;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
-  if (found <= 1 || !tuning_enabled() || cap != cudaStreamCaptureStatusNone) return;
+  if (found <= 1 || !tuning_enabled(tc) || cap != cudaStreamCaptureStatusNone) return;
   cudaStreamSynchronize(st);
   cudaStream_t ts;
   if (cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); return; }
