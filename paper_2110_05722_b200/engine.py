@@ -148,6 +148,12 @@ class TrainingEngine:
         self._seeds_next = SeedTable(self.device)
         # LS2_EARLY_MASKS=1: draw the next step's bits layer by layer during backward
         self._early_masks = os.environ.get("LS2_EARLY_MASKS", "0") == "1"
+        # host/device overlap: once a step's inputs are on the device (an event
+        # recorded inside the graph), the host stages the next step's batch and
+        # seeds while the device still runs this one (LS2_OVERLAP_HOST=0: off)
+        self._consumed = torch.cuda.Event(external=True)
+        self._overlap_host = os.environ.get("LS2_OVERLAP_HOST", "1") != "0"
+        self._pre = None                   # (step, batch, key, error) staged ahead
         self.last_out3 = None
 
     # -- arena setup (F/engine.py:89-103) ----------------------------------------------
@@ -213,13 +219,21 @@ class TrainingEngine:
     def _fwd_bwd(self, io: _StaticIO, key, step: int, upload: bool = True):
         t = self.cfg.train
         if upload:
+            # every host->device input of the step first: the batch, this step's
+            # site seeds, (the next step's seeds); then mark them consumed so the
+            # host can stage the next step while this one runs (train_step)
             io.upload()
-            if self.masks is not None and t.p_drop > 0.0:
+            if t.p_drop > 0.0:
+                seeds = self.model.seed_table(self.device)
+                self.model.register_seeds(seeds, t.seed, step, t.p_drop)
+                seeds.upload()
+            if self.masks is not None and self._early_masks and t.p_drop > 0.0:
                 if not torch.cuda.is_current_stream_capturing():
                     self._stage_next_seeds(step)
                 nx = self._seeds_next
                 n = len(nx.values)
                 nx.dev[:n].copy_(nx.host[:n], non_blocking=True)
+            self._consumed.record()
         self.arena.begin(key)
         sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
         self._bank_done = None
@@ -237,7 +251,7 @@ class TrainingEngine:
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
             arena=self.arena, sink=sink, grad_scale=float(t.act_grad_scale), validate=False,
-            upload_seeds=upload, masks=self.masks)
+            upload_seeds=False, masks=self.masks)
         self.arena.end()
         return out.out3, sink
 
@@ -420,24 +434,54 @@ class TrainingEngine:
         seeds = self.model.seed_table(self.device)
         self.model.register_seeds(seeds, t.seed, step, t.p_drop)
         seeds.write_host()
-        if self.masks is not None and t.p_drop > 0.0:
+        if self.masks is not None and self._early_masks and t.p_drop > 0.0:
             self._stage_next_seeds(step)
+
+    def _prestage(self, step: int):
+        """Host work of `step` done ahead, while the device runs the previous step:
+        build + validate the batch and stage it and the site seeds into the pinned
+        buffers (the previous step's copies out of them have completed)."""
+        try:
+            batch = self.task.batch(step)
+            validate_batch(batch, self.cfg.model)
+        except Exception as exc:                       # raised by that step's call
+            self._pre = (step, None, None, exc)
+            return
+        b, l = np.asarray(batch.src).shape
+        key = ("train", b, l)
+        if key not in self._graphs:
+            self._pre = None
+            return
+        self._io_for(b, l).stage(batch)
+        self.refresh_seeds(step)
+        self._pre = (step, batch, key, None)
 
     def train_step(self, step: int, trace=None) -> StepMetrics:
         t0 = time.perf_counter()
-        batch = self.task.batch(step)
-        validate_batch(batch, self.cfg.model)
-        b, l = np.asarray(batch.src).shape
-        key = ("train", b, l)
+        pre, self._pre = self._pre, None
+        if pre is not None and pre[0] == step:
+            if pre[3] is not None:
+                raise pre[3]
+            batch, key, staged = pre[1], pre[2], True
+        else:
+            batch = self.task.batch(step)
+            validate_batch(batch, self.cfg.model)
+            key, staged = ("train",) + tuple(np.asarray(batch.src).shape), False
+        b, l = key[1], key[2]
         if self.arena is None or not self.arena.has_plan(key):
             raise DataError(f"no arena plan for batch shape {key}; call setup_arena()")
         io = self._io_for(b, l)
         graphed = self.use_graphs and key in self._graphs
-        io.stage(batch)
         if graphed:
-            self.refresh_seeds(step)
+            if not staged:
+                io.stage(batch)
+                self.refresh_seeds(step)
             self._graphs[key].replay()
+            if self._overlap_host:
+                self._consumed.synchronize()           # inputs are on the device
+                self._prestage(step + 1)
         else:
+            io.stage(batch)
             self._run(io, key, step, graphed=False)
         torch.cuda.current_stream().synchronize()
         loss, count, correct, applied, nonfinite = self._host_out.tolist()
