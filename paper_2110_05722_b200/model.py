@@ -20,6 +20,7 @@ ordering contract).  B200-specific choices, all invisible at the API:
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -774,6 +775,11 @@ class MaskBank:
 
 _MASKS: MaskBank | None = None       # the bank of the forward_backward in flight
 
+# chain fusion across layer boundaries (LS2_CHAIN_FUSE=0: off): a layer's FFN
+# tail (bias+dropout+residual) runs fused with the LayerNorm that consumes its
+# output (the next layer's ln1, or the stack's final LN), forward and backward
+CHAIN_FUSE = os.environ.get("LS2_CHAIN_FUSE", "1") != "0"
+
 
 def _bank_bits(seed, n: int):
     return _MASKS.bits(seed, n) if _MASKS is not None else None
@@ -819,11 +825,10 @@ def _fusable_rows(*ts) -> bool:
     return all(t is None or (t.is_contiguous() and t.data_ptr() % 16 == 0) for t in ts)
 
 
-def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p, keep_tag,
-                 y_tag, ln):
-    """y = bias_dropout_residual(proj, bias, res) and u = LN(y): one fused pass when
-    possible (ls2_bdr_layernorm_fwd), else the two reference-shaped ops.
-    Pushes keep, y, mu, sg, u (in that order) and returns (y, u)."""
+def _tail_ln_core(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena):
+    """y = bias_dropout_residual(proj, bias, res) and u = LN(y) in one fused
+    pass when possible (ls2_bdr_layernorm_fwd), else the two reference-shaped
+    ops; returns (y, keep bits, mu, sigma, u)."""
     b, l, d = proj.shape
     r, dt = b * l, proj.dtype
     sdt = _stat_dtype(dt)
@@ -851,20 +856,33 @@ def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p
         K.bias_dropout_residual(proj, bb, res, p_drop, seed, out=y, bits_out=keep)
         K.layernorm_forward(y, lw, lb, eps, out=u, mu_out=mu, sigma_out=sg,
                             check_degenerate=False)
+    return y, keep, mu, sg, u
+
+
+
+def _tail_ln_fwd(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena, stash, p, keep_tag,
+                 y_tag, ln):
+    """_tail_ln_core + stash: pushes keep, y, mu, sg, u (in that order); returns (y, u)."""
+    y, keep, mu, sg, u = _tail_ln_core(proj, bias, res, p_drop, seed, ln_w, ln_b, eps, arena)
     stash.push(p + keep_tag, keep); stash.push(p + y_tag, y)
     stash.push(p + "mu" + ln, mu); stash.push(p + "sg" + ln, sg); stash.push(p + "u" + ln, u)
     return y, u
 
 
-def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, p):
+def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash, p, pre=None):
+    """pre: (u1, mu1, sg1) = LN1(x) already produced by the previous layer's
+    fused FFN tail (chain fusion), else LN1 runs here."""
     b, l, d = x.shape
     r, dt, hd = b * l, x.dtype, d // n_heads
     sdt = _stat_dtype(dt)
     stash.push(p + "x_in", x)
-    mu1, sg1 = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
-    u1 = arena.alloc((b, l, d), dt)
-    K.layernorm_forward(x, _as_dt(w.ln1_w, dt), _as_dt(w.ln1_b, dt), eps, out=u1, mu_out=mu1,
-                        sigma_out=sg1, check_degenerate=False)
+    if pre is not None:
+        u1, mu1, sg1 = pre
+    else:
+        mu1, sg1 = arena.alloc((r,), sdt), arena.alloc((r,), sdt)
+        u1 = arena.alloc((b, l, d), dt)
+        K.layernorm_forward(x, _as_dt(w.ln1_w, dt), _as_dt(w.ln1_b, dt), eps, out=u1, mu_out=mu1,
+                            sigma_out=sg1, check_degenerate=False)
     stash.push(p + "mu1", mu1); stash.push(p + "sg1", sg1); stash.push(p + "u1", u1)
     qkv = arena.alloc((b, l, 3 * d), dt)
     _linear(u1.view(r, d), w.wqkv, w.bqkv, qkv.view(r, 3 * d))
@@ -892,8 +910,12 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     return y1, u2
 
 
-def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p):
-    """FFN sublayer on the already-normalized input u = LN(y_in)."""
+def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p, next_ln=None):
+    """FFN sublayer on the already-normalized input u = LN(y_in).
+
+    next_ln: (w, b, eps) of the LayerNorm that consumes this layer's output (the
+    next layer's ln1, or the stack's final LN): the FFN tail is then fused with
+    it and (y2, (u, mu, sigma)) is returned instead of y2."""
     b, l, d = y_in.shape
     r, dt = b * l, y_in.dtype
     dff = w.w1.shape[0]
@@ -912,8 +934,14 @@ def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p):
     stash.push(p + "keepr", keep_r); stash.push(p + "relum", relum); stash.push(p + "z", z)
     f = arena.alloc((b, l, d), dt)
     _linear(z.view(r, dff), w.w2, None, f.view(r, d))
-    y2 = arena.alloc((b, l, d), dt)
     s_tail = _site_seed(seed, site, k_tail)
+    if next_ln is not None:
+        nw, nb, neps = next_ln
+        y2, keep_t, mu, sg, un = _tail_ln_core(f, w.b2, y_in, p_drop, s_tail, nw, nb, neps, arena)
+        arena.free(f)
+        stash.push(p + "keept", keep_t)
+        return y2, (un, mu, sg)
+    y2 = arena.alloc((b, l, d), dt)
     banked = _bank_bits(s_tail, r * d) if p_drop > 0.0 else None
     keep_t = banked if banked is not None else arena.alloc((_nbits(r * d),), torch.uint8)
     K.bias_dropout_residual(f, _as_dt(w.b2, dt), y_in, p_drop, s_tail, out=y2, bits_out=keep_t,
@@ -930,10 +958,19 @@ def encoder_layer_forward(x, w: EncoderLayerWeights, mask, p_drop, seed, *, n_he
     arena = arena or NullArena()
     stash = stash if stash is not None else ActivationStash()
     x = x if isinstance(x, torch.Tensor) else K.dev(x)
-    y1, u2 = _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash,
-                                 prefix)
-    y2 = _ffn_fwd(y1, u2, w, p_drop, seed, site, 1, 2, arena, stash, prefix)
+    y2, _ = _enc_fwd_chain(x, w, mask, p_drop, seed, n_heads, eps, arena, stash, prefix, site)
     return y2, stash
+
+
+def _enc_fwd_chain(x, w, mask, p_drop, seed, n_heads, eps, arena, stash, prefix, site, pre=None,
+                   next_ln=None):
+    """Encoder layer inside a stack: pre = this layer's LN1 from the previous
+    layer's fused tail; next_ln = the LN after this layer (fused into its FFN
+    tail).  Returns (y, LN-of-y triple or None)."""
+    y1, u2 = _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, stash,
+                                 prefix, pre=pre)
+    out = _ffn_fwd(y1, u2, w, p_drop, seed, site, 1, 2, arena, stash, prefix, next_ln=next_ln)
+    return out if next_ln is not None else (out, None)
 
 
 def _ln_bwd_tail(sink, pp, ln, du, y_in, w_ln, mu, sg, dyo, dres, keep, p_drop, bias_name,
@@ -974,14 +1011,16 @@ def _ln_bwd_tail(sink, pp, ln, du, y_in, w_ln, mu, sg, dyo, dres, keep, p_drop, 
     return True
 
 
-def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag, tail=None):
+def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag, tail=None, df_in=None):
     """FFN sublayer backward.  tail=(bias_name, keep_tag): also run the preceding
     attention tail's bias+dropout+residual backward in the LayerNorm pass and
-    return (dyo, dproj); otherwise return (dyo, None)."""
+    return (dyo, dproj); otherwise return (dyo, None).  df_in: the FFN tail's
+    bias+dropout backward already done (fused into the next LayerNorm's
+    backward, chain fusion): its dx, with the ffn.b2 gradient already taken."""
     b, l, d = dy.shape
     r, dt = b * l, dy.dtype
     dff = w.w1.shape[0]
-    keep_t = stash.pop(p + "keept")
+    keep_t = stash.pop(p + "keept") if df_in is None else None
     z = stash.pop(p + "z")
     relum = stash.pop(p + "relum")
     keep_r = stash.pop(p + "keepr")
@@ -989,9 +1028,12 @@ def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag, tail=None):
     sg = stash.pop(p + "sg" + ln)
     mu = stash.pop(p + "mu" + ln)
     y_in = stash.pop(p + y_in_tag)
-    df = arena.alloc((b, l, d), dt)
-    _bdr_bwd(sink, pp + "ffn.b2", dy, keep_t, p_drop, df)
-    arena.free(keep_t)
+    if df_in is None:
+        df = arena.alloc((b, l, d), dt)
+        _bdr_bwd(sink, pp + "ffn.b2", dy, keep_t, p_drop, df)
+        arena.free(keep_t)
+    else:
+        df = df_in
     dz = arena.alloc((b, l, dff), dt)
     K.gemm(df.view(r, d), _as_dt(w.w2, dt), out=dz.view(r, dff))
     _wgrad(sink, pp + "ffn.w2", df.view(r, d), z.view(r, dff))
@@ -1020,9 +1062,13 @@ def _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, ln, y_in_tag, tail=None):
     return dyo, dproj
 
 
-def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dproj=None):
+def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dproj=None,
+                        tail_prev=None):
     """Self-attention sublayer backward.  dproj: the attention-tail gradient when
-    the caller already produced it (fused into the LayerNorm backward)."""
+    the caller already produced it (fused into the LayerNorm backward).
+    tail_prev: (prefix, param prefix) of the layer below: its FFN tail's
+    bias+dropout backward is fused into this LN1 backward, and (dx, df_prev) is
+    returned instead of dx."""
     b, l, d = dy1.shape
     r, dt, hd = b * l, dy1.dtype, d // n_heads
     if dproj is None:
@@ -1074,21 +1120,46 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dpro
         _colsum_grad(sink, pp + "attn.bqkv", dqkv.view(r, 3 * d))
     arena.free(dqkv); arena.free(u1)
     dx = arena.alloc((b, l, d), dt)
-    _ln_bwd(sink, pp, "ln1", du1, x_in, w.ln1_w, mu1, sg1, dx, dy1)
+    if tail_prev is None:
+        _ln_bwd(sink, pp, "ln1", du1, x_in, w.ln1_w, mu1, sg1, dx, dy1)
+        arena.free(du1); arena.free(mu1); arena.free(sg1); arena.free(x_in)
+        arena.free(dy1)
+        return dx
+    df_prev = _ln_bwd_chain(sink, pp, "ln1", du1, x_in, w.ln1_w, mu1, sg1, dx, dy1, stash,
+                            tail_prev, p_drop, arena)
     arena.free(du1); arena.free(mu1); arena.free(sg1); arena.free(x_in)
     arena.free(dy1)
-    return dx
+    return dx, df_prev
+
+
+def _ln_bwd_chain(sink, pp, ln, du, x_in, w_ln, mu, sg, dx, dres, stash, tail_prev, p_drop, arena):
+    """LayerNorm backward fused with the FFN-tail bias+dropout backward of the
+    layer below (tail_prev = its (prefix, param prefix)): writes dx and returns
+    that layer's df (its ffn.b2 gradient taken here)."""
+    prev_p, prev_pp = tail_prev
+    keep_prev = stash.pop(prev_p + "keept")
+    b, l, d = dx.shape
+    df_prev = arena.alloc((b, l, d), dx.dtype)
+    if not _ln_bwd_tail(sink, pp, ln, du, x_in, w_ln, mu, sg, dx, dres, keep_prev, p_drop,
+                        prev_pp + "ffn.b2", df_prev):
+        _ln_bwd(sink, pp, ln, du, x_in, w_ln, mu, sg, dx, dres)
+        _bdr_bwd(sink, prev_pp + "ffn.b2", dx, keep_prev, p_drop, df_prev)
+    arena.free(keep_prev)
+    return df_prev
 
 
 def encoder_layer_backward(dy, w: EncoderLayerWeights, stash: ActivationStash, sink: GradSink, *,
-                           n_heads, p_drop, arena=None, prefix="", param_prefix=""):
-    """Backward of one encoder layer. Takes ownership of dy, returns dx."""
+                           n_heads, p_drop, arena=None, prefix="", param_prefix="", df_in=None,
+                           tail_prev=None):
+    """Backward of one encoder layer. Takes ownership of dy, returns dx
+    ((dx, df_prev) with tail_prev; df_in / tail_prev: chain fusion, see
+    _ffn_bwd / _self_attention_bwd)."""
     arena = arena or NullArena()
     dy = dy if isinstance(dy, torch.Tensor) else K.dev(dy)
     dy1, dproj = _ffn_bwd(dy, w, stash, sink, p_drop, arena, prefix, param_prefix, "2", "y1",
-                          tail=(param_prefix + "attn.bo", "keep1"))
+                          tail=(param_prefix + "attn.bo", "keep1"), df_in=df_in)
     return _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, prefix, param_prefix,
-                               dproj=dproj)
+                               dproj=dproj, tail_prev=tail_prev)
 
 
 # ---------------------------------------------------------------------------
@@ -1097,8 +1168,11 @@ def encoder_layer_backward(dy, w: EncoderLayerWeights, stash: ActivationStash, s
 
 def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, p_drop, seed, *,
                           n_heads, eps=1e-5, arena=None, stash=None, prefix="", site=0,
-                          strategy=None):
-    """One pre-LN decoder layer consuming precomputed (K_i, V_i)."""
+                          strategy=None, pre=None, next_ln=None):
+    """One pre-LN decoder layer consuming precomputed (K_i, V_i).
+
+    pre / next_ln: chain fusion inside a stack (see _enc_fwd_chain); with
+    next_ln the return value is (y, stash, LN-of-y triple)."""
     arena = arena or NullArena()
     stash = stash if stash is not None else ActivationStash()
     x = x if isinstance(x, torch.Tensor) else K.dev(x)
@@ -1108,7 +1182,7 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     ls = k_i.shape[1]
     p = prefix
     y1, u2 = _self_attention_fwd(x, w, self_mask, p_drop, seed, site, n_heads, eps, arena, stash,
-                                 p)
+                                 p, pre=pre)
     qc = arena.alloc((b, l, d), dt)
     _linear(u2.view(r, d), w.cross_wq, w.cross_bq, qc.view(r, d))
     stash.push(p + "qc", qc)
@@ -1131,13 +1205,16 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     y2, u3 = _tail_ln_fwd(proj_x, w.cross_bo, y1, p_drop, _site_seed(seed, site, 1), w.ln3_w,
                           w.ln3_b, eps, arena, stash, p, "keep2", "y2", "3")
     arena.free(proj_x)
+    if next_ln is not None:
+        y3, tri = _ffn_fwd(y2, u3, w, p_drop, seed, site, 2, 3, arena, stash, p, next_ln=next_ln)
+        return y3, stash, tri
     y3 = _ffn_fwd(y2, u3, w, p_drop, seed, site, 2, 3, arena, stash, p)
     return y3, stash
 
 
 def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStash, sink: GradSink,
                            *, n_heads, p_drop, arena=None, prefix="", param_prefix="",
-                           dkv_out=None, kv_colsum=None):
+                           dkv_out=None, kv_colsum=None, df_in=None, tail_prev=None):
     """Backward of one decoder layer; returns (dx, dK_i, dV_i).
 
     dkv_out: optional (dK_i, dV_i) destination views (slices of the packed
@@ -1153,7 +1230,7 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     ls = k_i.shape[1]
     p, pp = prefix, param_prefix
     dy2, dproj_x = _ffn_bwd(dy, w, stash, sink, p_drop, arena, p, pp, "3", "y2",
-                            tail=(pp + "cross.bo", "keep2"))
+                            tail=(pp + "cross.bo", "keep2"), df_in=df_in)
     ctxm_x = stash.pop(p + "ctxm_x")
     probs_x = stash.pop(p + "probs_x")
     qc = stash.pop(p + "qc")
@@ -1216,6 +1293,10 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
     arena.free(keep1)
     arena.free(du2); arena.free(mu2); arena.free(sg2); arena.free(y1)
     arena.free(dy2)
+    if tail_prev is not None:
+        dx, df_prev = _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp,
+                                          dproj=dproj, tail_prev=tail_prev)
+        return dx, dk_i, dv_i, df_prev
     dx = _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dproj=dproj)
     return dx, dk_i, dv_i
 
@@ -1446,16 +1527,27 @@ class Transformer:
                             else None)
         stash.push("src_keep", keep_src)
         enc_w = [EncoderLayerWeights.from_params(params, f"enc{i}.") for i in range(cfg.n_enc)]
+        chain = CHAIN_FUSE and cfg.n_enc > 0
+        pre = None
         for i in range(cfg.n_enc):
-            h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
-                                         eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
-                                         site=i)
+            if chain:
+                nxt = (enc_w[i + 1].ln1_w, enc_w[i + 1].ln1_b) if i + 1 < cfg.n_enc else \
+                    (params["enc_ln.w"], params["enc_ln.b"])
+                h, pre = _enc_fwd_chain(h, enc_w[i], enc_mask, p_drop, enc_seed, n, cfg.eps, arena,
+                                        stash, f"enc{i}.", i, pre=pre, next_ln=(*nxt, cfg.eps))
+            else:
+                h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
+                                             eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
+                                             site=i)
         stash.push("enc_ln_in", h)
-        mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
-        enc_out = arena.alloc((b, ls, d), dt)
-        K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
-                            cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
-                            check_degenerate=False)
+        if chain:
+            enc_out, mu_e, sg_e = pre
+        else:
+            mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
+            enc_out = arena.alloc((b, ls, d), dt)
+            K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
+                                cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
+                                check_degenerate=False)
         stash.push("enc_ln_mu", mu_e); stash.push("enc_ln_sg", sg_e)
         stash.push("enc_out", enc_out)
         pw = self.packed_weights(params)
@@ -1473,16 +1565,29 @@ class Transformer:
                             else None)
         stash.push("tgt_keep", keep_tgt)
         dec_w = [DecoderLayerWeights.from_params(params, f"dec{i}.") for i in range(cfg.n_dec)]
+        dchain = CHAIN_FUSE and cfg.n_dec > 0
+        pre = None
         for i in range(cfg.n_dec):
-            g, _ = decoder_layer_forward(g, dec_w[i], kv_pairs[i], dec_mask, cross_mask, p_drop,
-                                         dec_seed, n_heads=n, eps=cfg.eps, arena=arena,
-                                         stash=stash, prefix=f"dec{i}.", site=i)
+            if dchain:
+                nxt = (dec_w[i + 1].ln1_w, dec_w[i + 1].ln1_b) if i + 1 < cfg.n_dec else \
+                    (params["dec_ln.w"], params["dec_ln.b"])
+                g, _, pre = decoder_layer_forward(g, dec_w[i], kv_pairs[i], dec_mask, cross_mask,
+                                                  p_drop, dec_seed, n_heads=n, eps=cfg.eps,
+                                                  arena=arena, stash=stash, prefix=f"dec{i}.",
+                                                  site=i, pre=pre, next_ln=(*nxt, cfg.eps))
+            else:
+                g, _ = decoder_layer_forward(g, dec_w[i], kv_pairs[i], dec_mask, cross_mask,
+                                             p_drop, dec_seed, n_heads=n, eps=cfg.eps, arena=arena,
+                                             stash=stash, prefix=f"dec{i}.", site=i)
         stash.push("dec_ln_in", g)
-        mu_d, sg_d = arena.alloc((b * lt,), sdt), arena.alloc((b * lt,), sdt)
-        dec_out = arena.alloc((b, lt, d), dt)
-        K.layernorm_forward(g, _as_dt(params["dec_ln.w"], dt), _as_dt(params["dec_ln.b"], dt),
-                            cfg.eps, out=dec_out, mu_out=mu_d, sigma_out=sg_d,
-                            check_degenerate=False)
+        if dchain:
+            dec_out, mu_d, sg_d = pre
+        else:
+            mu_d, sg_d = arena.alloc((b * lt,), sdt), arena.alloc((b * lt,), sdt)
+            dec_out = arena.alloc((b, lt, d), dt)
+            K.layernorm_forward(g, _as_dt(params["dec_ln.w"], dt), _as_dt(params["dec_ln.b"], dt),
+                                cfg.eps, out=dec_out, mu_out=mu_d, sigma_out=sg_d,
+                                check_degenerate=False)
         stash.push("dec_ln_mu", mu_d); stash.push("dec_ln_sg", sg_d)
         stash.push("dec_out", dec_out)
 
@@ -1537,13 +1642,18 @@ class Transformer:
         sg_d = stash.pop("dec_ln_sg"); mu_d = stash.pop("dec_ln_mu")
         g_in = stash.pop("dec_ln_in")
         dg = arena.alloc((b, lt, d), dt)
-        _ln_bwd(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg, None)
+        nd = cfg.n_dec
+        df = None
+        if dchain:     # fused with the last decoder layer's FFN-tail backward
+            df = _ln_bwd_chain(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg,
+                               None, stash, (f"dec{nd - 1}.", f"dec{nd - 1}."), p_drop, arena)
+        else:
+            _ln_bwd(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg, None)
         arena.free(ddec); arena.free(mu_d); arena.free(sg_d); arena.free(g_in)
         _ready(sink, "dec_ln.", "out_proj.")
 
         # --- backward: decoder stack; dK_i/dV_i land in one packed buffer ---
         dkv = arena.alloc((b, ls, 2 * cfg.n_dec * d), dt)
-        nd = cfg.n_dec
         dks: list = [None] * nd
         dvs: list = [None] * nd
         # the packed cross-K/V bias gradient as per-batch partials left by the
@@ -1552,10 +1662,16 @@ class Transformer:
             if ATT.fused_ok(dt, lt, ls, d // n, AttentionMask("none")) else None
         for i in reversed(range(nd)):
             dest = (dkv[..., i * d:(i + 1) * d], dkv[..., (nd + i) * d:(nd + i + 1) * d])
-            dg, dks[i], dvs[i] = decoder_layer_backward(
+            tp = (f"dec{i - 1}.", f"dec{i - 1}.") if (dchain and i > 0) else None
+            res = decoder_layer_backward(
                 dg, dec_w[i], kv_pairs[i], stash, sink, n_heads=n, p_drop=p_drop, arena=arena,
                 prefix=f"dec{i}.", param_prefix=f"dec{i}.", dkv_out=dest,
-                kv_colsum=None if kvpart is None else (kvpart, i * d, (nd + i) * d, 2 * nd * d))
+                kv_colsum=None if kvpart is None else (kvpart, i * d, (nd + i) * d, 2 * nd * d),
+                df_in=df, tail_prev=tp)
+            if tp is not None:
+                dg, dks[i], dvs[i], df = res
+            else:
+                (dg, dks[i], dvs[i]), df = res, None
             join()
             _ready(sink, f"dec{i}.")
             emit(("dec_layer_backward_done", i))
@@ -1574,13 +1690,22 @@ class Transformer:
         sg_e = stash.pop("enc_ln_sg"); mu_e = stash.pop("enc_ln_mu")
         h_in = stash.pop("enc_ln_in")
         dh = arena.alloc((b, ls, d), dt)
-        _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
+        df = None
+        if chain:      # fused with the last encoder layer's FFN-tail backward
+            ne = cfg.n_enc
+            df = _ln_bwd_chain(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh,
+                               None, stash, (f"enc{ne - 1}.", f"enc{ne - 1}."), p_drop, arena)
+        else:
+            _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
         arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
         join()
         _ready(sink, "cross_kv.", "enc_ln.")
         for i in reversed(range(cfg.n_enc)):
-            dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
-                                        arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
+            tp = (f"enc{i - 1}.", f"enc{i - 1}.") if (chain and i > 0) else None
+            res = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
+                                         arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.",
+                                         df_in=df, tail_prev=tp)
+            dh, df = res if tp is not None else (res, None)
             join()
             _ready(sink, f"enc{i}.")
         keep_src = stash.pop("src_keep")
@@ -1721,16 +1846,27 @@ class EncoderMLM(Transformer):
                             else None)
         stash.push("src_keep", keep_src)
         enc_w = [EncoderLayerWeights.from_params(params, f"enc{i}.") for i in range(cfg.n_enc)]
+        chain = CHAIN_FUSE and cfg.n_enc > 0
+        pre = None
         for i in range(cfg.n_enc):
-            h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
-                                         eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
-                                         site=i)
+            if chain:
+                nxt = (enc_w[i + 1].ln1_w, enc_w[i + 1].ln1_b) if i + 1 < cfg.n_enc else \
+                    (params["enc_ln.w"], params["enc_ln.b"])
+                h, pre = _enc_fwd_chain(h, enc_w[i], enc_mask, p_drop, enc_seed, n, cfg.eps, arena,
+                                        stash, f"enc{i}.", i, pre=pre, next_ln=(*nxt, cfg.eps))
+            else:
+                h, _ = encoder_layer_forward(h, enc_w[i], enc_mask, p_drop, enc_seed, n_heads=n,
+                                             eps=cfg.eps, arena=arena, stash=stash, prefix=f"enc{i}.",
+                                             site=i)
         stash.push("enc_ln_in", h)
-        mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
-        enc_out = arena.alloc((b, ls, d), dt)
-        K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
-                            cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
-                            check_degenerate=False)
+        if chain:
+            enc_out, mu_e, sg_e = pre
+        else:
+            mu_e, sg_e = arena.alloc((b * ls,), sdt), arena.alloc((b * ls,), sdt)
+            enc_out = arena.alloc((b, ls, d), dt)
+            K.layernorm_forward(h, _as_dt(params["enc_ln.w"], dt), _as_dt(params["enc_ln.b"], dt),
+                                cfg.eps, out=enc_out, mu_out=mu_e, sigma_out=sg_e,
+                                check_degenerate=False)
 
         # --- MLM criterion over every position (pad targets are skipped) ---
         rt = b * ls
@@ -1773,13 +1909,22 @@ class EncoderMLM(Transformer):
         arena.free(logits_buf); arena.free(enc_out)
         h_in = stash.pop("enc_ln_in")
         dh = arena.alloc((b, ls, d), dt)
-        _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
+        df = None
+        if chain:      # fused with the last encoder layer's FFN-tail backward
+            ne = cfg.n_enc
+            df = _ln_bwd_chain(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh,
+                               None, stash, (f"enc{ne - 1}.", f"enc{ne - 1}."), p_drop, arena)
+        else:
+            _ln_bwd(sink, "", "enc_ln", denc, h_in, params["enc_ln.w"], mu_e, sg_e, dh, None)
         arena.free(denc); arena.free(mu_e); arena.free(sg_e); arena.free(h_in)
         join()
         _ready(sink, "enc_ln.")
         for i in reversed(range(cfg.n_enc)):
-            dh = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
-                                        arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.")
+            tp = (f"enc{i - 1}.", f"enc{i - 1}.") if (chain and i > 0) else None
+            res = encoder_layer_backward(dh, enc_w[i], stash, sink, n_heads=n, p_drop=p_drop,
+                                         arena=arena, prefix=f"enc{i}.", param_prefix=f"enc{i}.",
+                                         df_in=df, tail_prev=tp)
+            dh, df = res if tp is not None else (res, None)
             join()
             _ready(sink, f"enc{i}.")
         keep_src = stash.pop("src_keep")
