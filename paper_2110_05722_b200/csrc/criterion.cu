@@ -367,10 +367,14 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
   __shared__ int s_first[G][WG];
   __shared__ float s_ht[G];
   __shared__ double s_acc[G][3];     // per group: (loss, correct, count) in row order
-  // cluster exchange slots [row parity][source rank], pushed by the source CTA
-  __shared__ float x_max[2][kMaxC], x_z[2][kMaxC], x_ht[2][kMaxC];
-  __shared__ double x_sh[2][kMaxC];
-  __shared__ int x_first[2][kMaxC];
+  // cluster exchange slots [group][row parity][source rank], pushed by the
+  // source CTA's group; xbar[group][parity] counts the C pushes (DSMEM mbarrier
+  // arrivals with cluster-scope release), so each row group syncs with the
+  // same group of the other CTAs only, and the two groups stay out of phase
+  __shared__ float x_max[G][2][kMaxC], x_z[G][2][kMaxC], x_ht[G][2][kMaxC];
+  __shared__ double x_sh[G][2][kMaxC];
+  __shared__ int x_first[G][2][kMaxC];
+  __shared__ uint64_t xbar[G][2];
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
   const int q = C > 1 ? (int)cl.block_rank() : 0;
@@ -387,6 +391,10 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
   const int64_t r0 = cid + (int64_t)g * ncl;
   if (gt == 0) {
     for (int i = 0; i < NB; ++i) mbar_init(&bar[g * NB + i], 1);
+    if (C > 1) {
+      mbar_init(&xbar[g][0], C);
+      mbar_init(&xbar[g][1], C);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < NB; ++i)
       if (r0 + i * rstride < rows)
@@ -394,7 +402,8 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
                   slice_bytes, &bar[g * NB + i]);
     s_acc[g][0] = s_acc[g][1] = s_acc[g][2] = 0.0;
   }
-  __syncthreads();
+  if (C > 1) cl.sync();   // every CTA's barriers initialised before any remote arrive
+  else __syncthreads();
   const float l2e = 1.4426950408889634f;
   const float a_v = (float)(alpha / (double)V);
   const float one_m_a = (float)(1.0 - alpha);
@@ -553,9 +562,9 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
       }
     } else {
       if (gw == 0) {
-        float zz = s_z[0][lane];
-        double ss = s_sh[0][lane];
-        int ff = s_first[0][lane];
+        float zz = lane < WG ? s_z[g][lane] : 0.f;
+        double ss = lane < WG ? s_sh[g][lane] : 0.0;
+        int ff = lane < WG ? s_first[g][lane] : INT32_MAX;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           zz += __shfl_xor_sync(0xffffffffu, zz, o);
@@ -563,26 +572,39 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
           ff = min(ff, __shfl_xor_sync(0xffffffffu, ff, o));
         }
         if (lane < C) {
-          *cl.map_shared_rank(&x_max[xb][q], lane) = mq;
-          *cl.map_shared_rank(&x_z[xb][q], lane) = zz;
-          *cl.map_shared_rank(&x_sh[xb][q], lane) = ss;
-          *cl.map_shared_rank(&x_first[xb][q], lane) = ff;
-          *cl.map_shared_rank(&x_ht[xb][q], lane) = s_ht[0];
+          *cl.map_shared_rank(&x_max[g][xb][q], lane) = mq;
+          *cl.map_shared_rank(&x_z[g][xb][q], lane) = zz;
+          *cl.map_shared_rank(&x_sh[g][xb][q], lane) = ss;
+          *cl.map_shared_rank(&x_first[g][xb][q], lane) = ff;
+          *cl.map_shared_rank(&x_ht[g][xb][q], lane) = s_ht[g];
+          // release the pushes to CTA `lane`: arrive on its barrier for this group/parity
+          uint32_t rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                       : "=r"(rb) : "r"(smem_u32(&xbar[g][xb])), "r"((uint32_t)lane));
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb)
+                       : "memory");
         }
       }
-      cl.sync();                                           // the one exchange per row
-      const float mp = lane < C ? x_max[xb][lane] : -INFINITY;
+      {   // the one exchange per row: all C pushes of this group have landed here
+        const uint32_t lb = smem_u32(&xbar[g][xb]);
+        const uint32_t par = (uint32_t)((k >> 1) & 1);
+        asm volatile(
+            "{\n .reg .pred p;\n XW_%=:\n"
+            " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra XW_%=;\n}" ::"r"(lb), "r"(par) : "memory");
+      }
+      const float mp = lane < C ? x_max[g][xb][lane] : -INFINITY;
       M = mp;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      zt = lane < C ? x_z[xb][lane] * exp2f((mp - M) * l2e) : 0.f;
+      zt = lane < C ? x_z[g][xb][lane] * exp2f((mp - M) * l2e) : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) zt += __shfl_xor_sync(0xffffffffu, zt, o);
       scale = exp2f((mq - M) * l2e);
       if (q == 0 && gw == 0) {
-        int ft = (lane < C && mp == M) ? x_first[xb][lane] : INT32_MAX;
-        double sht = lane < C ? x_sh[xb][lane] : 0.0;
-        float ht = lane < C ? x_ht[xb][lane] : 0.f;
+        int ft = (lane < C && mp == M) ? x_first[g][xb][lane] : INT32_MAX;
+        double sht = lane < C ? x_sh[g][xb][lane] : 0.0;
+        float ht = lane < C ? x_ht[g][xb][lane] : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           ft = min(ft, __shfl_xor_sync(0xffffffffu, ft, o));
@@ -592,11 +614,11 @@ __global__ void __launch_bounds__(kCeTmaThreads, 1) criterion_rows_kernel(
         if (lane == 0) {
           const double lse = (double)M + log((double)zt) - (double)PT::kLog2Scale * 0.6931471805599453;
           if (valid && tgt_ok) {
-            s_acc[0][0] += -(1.0 - alpha) * ((double)ht - lse) -
+            s_acc[g][0] += -(1.0 - alpha) * ((double)ht - lse) -
                            (alpha / (double)V) * (sht - (double)V * lse);
-            s_acc[0][1] += (ft == tgt) ? 1.0 : 0.0;
+            s_acc[g][1] += (ft == tgt) ? 1.0 : 0.0;
           }
-          s_acc[0][2] += valid ? 1.0 : 0.0;
+          s_acc[g][2] += valid ? 1.0 : 0.0;
         }
       }
     }
@@ -835,7 +857,7 @@ static int launch_ce_rows(const T* logits, const int64_t* targets, T* dlogits, d
     return !(e && e[0] == '1');
   }();
   const int need2 = (int)ceil_div((int64_t)S / 8, (int64_t)(kCeTmaThreads / 2));
-  if (C == 1 && groups2 && need2 <= 8) {
+  if (groups2 && need2 <= 8) {
     if (need2 <= 1) LS2_CE_GO(1, 2);
     if (need2 <= 2) LS2_CE_GO(2, 2);
     if (need2 <= 4) LS2_CE_GO(4, 2);
