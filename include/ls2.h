@@ -261,6 +261,13 @@ int ls2_gemm(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
  * (ptrs_ready=1: the caller guarantees ptr_scratch already holds this call's
  *  A/B/C pointer arrays, e.g. cached per static arena address) */
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2);
+/* weight-gradient GEMM on tcgen05/TMEM/TMA (hand-written, gemm_tc.cu): C[m x n] (f32,
+ * row-major) = A^T B (+ C when beta), A [k x m] and B [k x n] fp16 row-major; a cluster
+ * of S CTAs splits K and reduces through DSMEM (deterministic).  ls2_wgrad_tc_split
+ * returns S, or 0 when the shape is not covered (m, n multiples of 128, one wave). */
+int ls2_wgrad_tc_split(int64_t m, int64_t n, int64_t k);
+int ls2_wgrad_tc(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                 int64_t m, int64_t n, int64_t k, int beta, void* stream);
 /* plain GEMM on cuBLASLt with an optional fused bias epilogue (C += bias[n] per row);
  * LS2_ERR_CUBLAS if no Lt algorithm supports the combination (caller falls back) */
 int ls2_gemm_lt(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,

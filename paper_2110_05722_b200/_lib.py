@@ -78,6 +78,8 @@ _SIGS = {
     "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, I, P],
     "ls2_gemm_lt": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, P],
     "ls2_gemm_scratch_bytes": [L, L],
+    "ls2_wgrad_tc_split": [L, L, L],
+    "ls2_wgrad_tc": [P, L, P, L, P, L, L, L, L, I, P],
     "ls2_comm_load": [ctypes.c_char_p],
     "ls2_comm_version": [P],
     "ls2_comm_unique_id": [P],
@@ -88,7 +90,7 @@ _SIGS = {
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,
              "ls2_colsum_ws_bytes": L, "ls2_layernorm_bwd_ws_bytes": L,
              "ls2_attention_supported": ctypes.c_int, "ls2_colsum_nblk": ctypes.c_int,
-             "ls2_layernorm_bwd_nblk": ctypes.c_int,
+             "ls2_layernorm_bwd_nblk": ctypes.c_int, "ls2_wgrad_tc_split": ctypes.c_int,
              "ls2_gemm_scratch_bytes": L}
 
 _lib = None

@@ -138,13 +138,13 @@ static int tuning_mode() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("LS2_GEMM_TUNE");
-    on = !e ? 0 : e[0] == '1' ? 1 : e[0] == 'w' ? 2 : 0;
+    on = !e ? 0 : e[0] == '1' ? 1 : e[0] == 'w' ? 2 : e[0] == 'd' ? 3 : 0;
   }
   return on;
 }
 static bool tuning_enabled(int tc = -1) {
   const int m = tuning_mode();
-  return m == 1 || (m == 2 && tc == LS2_F32);
+  return m == 1 || (m == 2 && tc == LS2_F32) || (m == 3 && tc != LS2_F32);
 }
 
 // Candidates are timed as a CUDA graph of kTuneReps back-to-back launches on a

@@ -519,3 +519,31 @@ def test_fused_criterion_padded_pitch_vs_oracle(rows, v):
     got = hd.float().cpu().numpy()[:, :v]
     assert np.linalg.norm(got - d_ref) <= 2e-2 * np.linalg.norm(d_ref)
     assert np.all(got[tg == 0] == 0)
+
+
+# --- tcgen05 weight-gradient GEMM ----------------------------------------------------
+
+@pytest.mark.parametrize("m,n,k,beta", [(512, 512, 4096, 0), (512, 512, 4096, 1),
+                                        (1536, 512, 4096, 0), (2048, 512, 4096, 1),
+                                        (512, 2048, 4096, 0), (256, 384, 1024, 0)])
+def test_wgrad_tc_vs_torch(m, n, k, beta):
+    """C = A^T B (+C) on tcgen05/TMEM (split-K over a cluster, DSMEM reduction)
+    against torch's fp32 product of the same fp16 operands: 1e-5 relative."""
+    from paper_2110_05722_b200 import _lib
+    if not _lib.load_library().ls2_wgrad_tc_split(m, n, k):
+        pytest.skip("shape not covered")
+    torch.manual_seed(m + n + k)
+    a = (torch.randn(k, m, device="cuda") * 0.5).half()
+    b = (torch.randn(k, n, device="cuda") * 0.5).half()
+    c0 = torch.randn(m, n, device="cuda")
+    c = c0.clone()
+    _lib.call("ls2_wgrad_tc", a.data_ptr(), m, b.data_ptr(), n, c.data_ptr(), n, m, n, k, beta,
+              _lib.stream_handle())
+    want = a.float().t() @ b.float() + (c0 if beta else 0)
+    err = (c - want).abs().max().item() / want.abs().max().item()
+    assert err <= 1e-5, err
+    # deterministic: same bits twice
+    c2 = c0.clone()
+    _lib.call("ls2_wgrad_tc", a.data_ptr(), m, b.data_ptr(), n, c2.data_ptr(), n, m, n, k, beta,
+              _lib.stream_handle())
+    assert torch.equal(c, c2)
