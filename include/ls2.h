@@ -236,7 +236,7 @@ int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_s
                      void* stream);
 int ls2_count_nonfinite_f16(const uint16_t* g16, int64_t n, int* nonfinite, void* stream);
 /* deferred column-sum finishes fused with the narrow: desc rows {dst, cols, part, nblk,
- * stride, k} (int64), chunks {desc index, first column} (int32, one CTA per 32 columns);
+ * stride, k} (int64), chunks {desc index, first column} (int32, one CTA per 64 columns);
  * g16[dst + c] = RNE(f32(sum_g partial[part + g*stride + k*cols + c]) * scale) */
 int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chunks,
                       const double* partial_base, uint16_t* g16, double loss_scale,

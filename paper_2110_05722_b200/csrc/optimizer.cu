@@ -167,40 +167,62 @@ __global__ void scale_narrow_kernel(const float* __restrict__ acc, uint16_t* __r
 // all in fixed order, scales like scale_narrow and writes the fp16 gradients.
 // desc row: {dst (element offset in the workspace), cols, part (double offset),
 //            nblk, stride (doubles per block), k}
-__global__ void __launch_bounds__(1024) finish_narrow_kernel(
+// One CTA (8 warps) per 64 columns of one deferred tensor: lane l owns columns
+// c0 + 2l, +1 (16-byte loads), warp w sums partial rows w, w+8, ... with four
+// loads in flight, and the 8 warp sums are folded in warp order (deterministic).
+constexpr int kFinishCols = 64;
+__global__ void __launch_bounds__(256) finish_narrow_kernel(
     const int64_t* __restrict__ desc, const int32_t* __restrict__ chunks,
     const double* __restrict__ part_base, uint16_t* __restrict__ g16, double loss_scale,
     const double* out3, int64_t count_host, float post, int* nonfinite) {
-  __shared__ double red[32][33];
+  __shared__ double red[8][kFinishCols + 1];
   const int di = chunks[2 * blockIdx.x], c0 = chunks[2 * blockIdx.x + 1];
   const int64_t* d = desc + 6 * di;
   const int64_t dst = d[0], cols = d[1], part = d[2], stride = d[4], k = d[5];
   const int nblk = (int)d[3];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = c0 + lane;
+  const int64_t c = c0 + 2 * lane;
   const double* p = part_base + part + k * cols + c;
-  double s0 = 0, s1 = 0;
-  if (c < cols) {
+  double sx = 0, sy = 0;
+  if (c + 1 < cols && (cols & 1) == 0) {
+    double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
     int g = w;
-    for (; g + 32 < nblk; g += 64) {
-      s0 += p[(int64_t)g * stride];
-      s1 += p[(int64_t)(g + 32) * stride];
+    for (; g + 24 < nblk; g += 32) {
+      const double2 v0 = *reinterpret_cast<const double2*>(p + (int64_t)g * stride);
+      const double2 v1 = *reinterpret_cast<const double2*>(p + (int64_t)(g + 8) * stride);
+      const double2 v2 = *reinterpret_cast<const double2*>(p + (int64_t)(g + 16) * stride);
+      const double2 v3 = *reinterpret_cast<const double2*>(p + (int64_t)(g + 24) * stride);
+      a0.x += v0.x; a0.y += v0.y; a1.x += v1.x; a1.y += v1.y;
+      a2.x += v2.x; a2.y += v2.y; a3.x += v3.x; a3.y += v3.y;
     }
-    for (; g < nblk; g += 32) s0 += p[(int64_t)g * stride];
+    for (; g < nblk; g += 8) {
+      const double2 v = *reinterpret_cast<const double2*>(p + (int64_t)g * stride);
+      a0.x += v.x; a0.y += v.y;
+    }
+    sx = (a0.x + a1.x) + (a2.x + a3.x);
+    sy = (a0.y + a1.y) + (a2.y + a3.y);
+  } else {
+    for (int g = w; g < nblk; g += 8) {
+      if (c < cols) sx += p[(int64_t)g * stride];
+      if (c + 1 < cols) sy += p[(int64_t)g * stride + 1];
+    }
   }
-  red[w][lane] = s0 + s1;
+  red[w][2 * lane] = sx;
+  red[w][2 * lane + 1] = sy;
   __syncthreads();
-  if (w == 0) {
+  if (w < 2) {
+    const int cc = lane + 32 * w;
+    const int64_t col = c0 + cc;
     int bad = 0;
-    if (c < cols) {
-      double s = 0;
+    if (col < cols) {
+      double t = 0;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) s += red[q][lane];
+      for (int q = 0; q < 8; ++q) t += red[q][cc];
       double cnt = count_host >= 0 ? (double)count_host : out3[1];
       if (cnt < 1.0) cnt = 1.0;
       const float sc = __fmul_rn((float)(loss_scale / cnt), post);
-      const uint16_t h = f2h(__fmul_rn((float)s, sc));
-      g16[dst + c] = h;
+      const uint16_t h = f2h(__fmul_rn((float)t, sc));
+      g16[dst + col] = h;
       bad = h_nonfinite(h);
     }
     if (nonfinite) {
@@ -273,7 +295,7 @@ int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chun
                       void* stream) {
   if (n_chunks <= 0) return LS2_OK;
   if (count_host < 0 && !out3) return fail(LS2_ERR_SHAPE, "finish_narrow: no token count");
-  finish_narrow_kernel<<<(unsigned)n_chunks, 1024, 0, as_stream(stream)>>>(
+  finish_narrow_kernel<<<(unsigned)n_chunks, 256, 0, as_stream(stream)>>>(
       desc, chunks, partial_base, g16, loss_scale, out3, count_host, post, nonfinite);
   return check_launch("finish_narrow");
 }

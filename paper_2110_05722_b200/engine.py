@@ -360,7 +360,7 @@ class TrainingEngine:
             for i, (n, ptr, nb, st, k, c) in enumerate(key):
                 off, _ = self.ws.resolve(n)
                 desc.append([off, c, ptr // 8, nb, st, k])
-                chunks += [(i, c0) for c0 in range(0, c, 32)]
+                chunks += [(i, c0) for c0 in range(0, c, 64)]
             tab = (torch.tensor(desc, dtype=torch.int64, device=self.device),
                    torch.tensor(chunks, dtype=torch.int32, device=self.device), len(chunks))
             self._finish_tables[key] = tab
