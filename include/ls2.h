@@ -229,6 +229,10 @@ int ls2_sgd(uint16_t* p16, const uint16_t* g16, float* vel, int64_t n, const flo
 /* applied += (nonfinite==0 && loss finite)  — one thread */
 int ls2_step_commit(int64_t* applied, const int* nonfinite, const double* loss,
                     int* applied_flag, void* stream);
+/* step_commit and the step report {loss sum, tokens, correct, applied, non-finite}
+ * (f64 x 5, the train-step D2H source) in one launch; totals = (loss, count, correct) */
+int ls2_step_report(int64_t* applied, const int* nonfinite, const double* totals, double* report,
+                    void* stream);
 /* g16 = RNE(acc32 * f32(loss_scale / max(count,1)) * post), count = out3[1] (device) or
  * count_host (>=0); nonfinite += #non-finite g16 (NULL to skip) */
 int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_scale,

@@ -68,6 +68,7 @@ _SIGS = {
     "ls2_adam": [P, P, P, P, L, P, P, L, L, P, P, P, P],
     "ls2_sgd": [P, P, P, L, P, P, P, P],
     "ls2_step_commit": [P, P, P, P, P],
+    "ls2_step_report": [P, P, P, P, P],
     "ls2_scale_narrow": [P, P, L, D, P, L, Fl, P, P],
     "ls2_count_nonfinite_f16": [P, L, P, P],
     "ls2_finish_narrow": [P, P, L, P, P, D, P, L, Fl, P, P],

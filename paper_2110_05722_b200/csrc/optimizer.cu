@@ -113,6 +113,19 @@ __global__ void step_commit_kernel(int64_t* applied, const int* nonfinite, const
   if (applied_flag) *applied_flag = ok ? 1 : 0;
 }
 
+// step_commit plus the step's 5-number report {loss sum, tokens, correct,
+// applied, non-finite count} in one launch (the D2H source of train_step)
+__global__ void step_report_kernel(int64_t* applied, const int* nonfinite, const double* totals,
+                                   double* report) {
+  const bool ok = !skip_step(nonfinite, totals);
+  if (ok) *applied += 1;
+  report[0] = totals[0];
+  report[1] = totals[1];
+  report[2] = totals[2];
+  report[3] = ok ? 1.0 : 0.0;
+  report[4] = (double)*nonfinite;
+}
+
 __device__ __forceinline__ int warp_count(int c) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -276,6 +289,12 @@ int ls2_step_commit(int64_t* applied, const int* nonfinite, const double* loss, 
                     void* stream) {
   step_commit_kernel<<<1, 1, 0, as_stream(stream)>>>(applied, nonfinite, loss, applied_flag);
   return check_launch("step_commit");
+}
+
+int ls2_step_report(int64_t* applied, const int* nonfinite, const double* totals, double* report,
+                    void* stream) {
+  step_report_kernel<<<1, 1, 0, as_stream(stream)>>>(applied, nonfinite, totals, report);
+  return check_launch("step_report");
 }
 
 int ls2_scale_narrow(const float* acc32, uint16_t* g16, int64_t n, double loss_scale,

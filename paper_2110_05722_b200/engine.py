@@ -397,13 +397,10 @@ class TrainingEngine:
             _lib.call("ls2_sgd", ws.params16.data_ptr(), ws.grads16.data_ptr(), ws.m32.data_ptr(),
                       ws.n_elements, self._opt.hyper.data_ptr(), self._nonfinite.data_ptr(),
                       loss_ptr, st)
-        _lib.call("ls2_step_commit", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
-                  loss_ptr, self._flag.data_ptr(), st)
+        _lib.call("ls2_step_report", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
+                  loss_ptr, self._dev_out.data_ptr(), st)
         if joined is not None:
             torch.cuda.current_stream().wait_event(joined)
-        self._dev_out[0:3].copy_(out3)
-        self._dev_out[3].copy_(self._flag[0])
-        self._dev_out[4].copy_(self._nonfinite[0])
         if host_copy:
             self._host_out.copy_(self._dev_out, non_blocking=True)
 
