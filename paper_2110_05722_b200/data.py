@@ -151,9 +151,96 @@ class MLMTask:
                      src_len=np.full(self.b, self.l, np.int64), pad_id=self.pad_id)
 
 
+class FileTask:
+    """Copy objective over the sequences of a token file (F/data.py:105-155):
+    sequences truncated to max_len, ordered by length (stable), grouped greedily
+    so a group padded to its bucketed length stays within batch_tokens; the
+    batches are precomputed and step s takes batch s mod count."""
+
+    def __init__(self, run_cfg):
+        m, t, d = run_cfg.model, run_cfg.train, run_cfg.data
+        self.pad_id = d.pad_id
+        self.bos = bos_id(d.pad_id, m.vocab)
+        seqs = [s[:m.max_len] for s in load_token_file(d.path, m.vocab) if s]
+        if not seqs:
+            raise DataError(f"no usable sequences in {d.path}")
+        self.batches = self._group(seqs, t.batch_tokens, m.max_len)
+
+    def _group(self, seqs, batch_tokens: int, max_len: int) -> list:
+        out, cur, longest = [], [], 0
+        for i in sorted(range(len(seqs)), key=lambda j: len(seqs[j])):
+            s = seqs[i]
+            lb = bucket_len(max(longest, len(s)), max_len)
+            if cur and lb * (len(cur) + 1) > batch_tokens:
+                out.append(self._pack(cur, max_len))
+                cur, longest = [], 0
+            cur.append(s)
+            longest = max(longest, len(s))
+        if cur:
+            out.append(self._pack(cur, max_len))
+        return out
+
+    def _pack(self, group, max_len: int) -> Batch:
+        lb = bucket_len(max(len(s) for s in group), max_len)
+        b = len(group)
+        src = np.full((b, lb), self.pad_id, dtype=np.int64)
+        tgt_in = src.copy()
+        tgt_out = src.copy()
+        lens = np.array([len(s) for s in group], dtype=np.int64)
+        for i, s in enumerate(group):
+            n = len(s)
+            src[i, :n] = s
+            tgt_out[i, :n] = s
+            tgt_in[i, 0] = self.bos
+            tgt_in[i, 1:n] = s[:n - 1]
+        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt_out, src_len=lens, pad_id=self.pad_id)
+
+    def possible_shapes(self) -> list:
+        return sorted({tuple(np.asarray(b.src).shape) for b in self.batches})
+
+    def batch(self, step: int) -> Batch:
+        return self.batches[step % len(self.batches)]
+
+
+class WmtShapedTask:
+    """Synthetic WMT-shaped batches: per step, a bucket length is
+    drawn with the counter RNG (lengths 8..max_len, bucketed to multiples of 4,
+    F/data.py:19,46-48) and the batch packs as many sequences of that bucket as fit
+    batch_tokens (the FileTask grouping rule); real lengths inside a batch vary,
+    the rest is padding.  A pure function of (seed, step), so resume is exact."""
+
+    def __init__(self, batch_tokens: int, max_len: int, vocab: int, seed: int = 0,
+                 pad_id: int = 0, min_len: int = 8):
+        self.tokens, self.max_len, self.v, self.seed = batch_tokens, max_len, vocab, seed
+        self.pad_id, self.bos = pad_id, bos_id(pad_id, vocab)
+        self.min_len = min_len
+        self.buckets = sorted({bucket_len(m, max_len) for m in range(min_len, max_len + 1)})
+
+    def possible_shapes(self) -> list:
+        return [(max(1, self.tokens // lb), lb) for lb in self.buckets]
+
+    def batch(self, step: int) -> Batch:
+        u = _uniform(derive_seed(self.seed, step, 9), 1)[0]
+        lb = self.buckets[min(int(u * len(self.buckets)), len(self.buckets) - 1)]
+        b = max(1, self.tokens // lb)
+        r = _uniform(derive_seed(self.seed, step, 10), b * (lb + 1))
+        lens = np.maximum(lb - 3, 1) + (r[:b] * min(4, lb)).astype(np.int64)
+        lens = np.minimum(lens, lb)
+        tok = 2 + (r[b:] * (self.v - 2)).astype(np.int64).reshape(b, lb)
+        src = np.full((b, lb), self.pad_id, dtype=np.int64)
+        tgt_in, tgt_out = src.copy(), src.copy()
+        for i in range(b):
+            n = int(lens[i])
+            src[i, :n] = tok[i, :n]
+            tgt_out[i, :n] = tok[i, :n]
+            tgt_in[i, 0] = self.bos
+            tgt_in[i, 1:n] = tok[i, :n - 1]
+        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt_out, src_len=lens, pad_id=self.pad_id)
+
+
 def make_task(run_cfg):
     if run_cfg.data.task == "file":
-        raise DataError("file task: use load_token_file + a custom batcher (not on the hot path)")
+        return FileTask(run_cfg)
     if run_cfg.data.task == "fixed":
         m = run_cfg.model
         return FixedShapeTask(max(1, run_cfg.train.batch_tokens // m.max_len), m.max_len, m.vocab,

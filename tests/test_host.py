@@ -167,3 +167,61 @@ def test_oracle_never_imports_product():
     src = open(os.path.join(ROOT, "oracle", "lsport.py")).read()
     mods = re.findall(r"^\s*(?:from|import)\s+([\w.]+)", src, re.M)
     assert not any(m.startswith("paper_2110_05722_b200") for m in mods), mods
+
+
+def test_file_task_matches_reference_golden(tmp_path):
+    """FileTask (F/data.py:105-155) vs the reference's own batches on the same token
+    file (tests/golden/data.npz, written by tests/golden/make_golden_data.py)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2110_05722_b200.config import RunConfig
+    from paper_2110_05722_b200.data import FileTask
+    g = np.load(os.path.join(GOLDEN, "data.npz"))
+    path = tmp_path / "tokens.txt"
+    path.write_bytes(g["file_text"].tobytes())
+    run = RunConfig()
+    run.model.vocab, run.model.max_len = 50, 24
+    run.train.batch_tokens = 96
+    run.data.task, run.data.path = "file", str(path)
+    ft = FileTask(run)
+    assert len(ft.batches) == int(g["file_n"][0])
+    for i, b in enumerate(ft.batches):
+        for k in ("src", "tgt_in", "tgt_out", "src_len"):
+            assert np.array_equal(np.asarray(getattr(b, k)), g[f"file_{i}_{k}"]), (i, k)
+    assert ft.possible_shapes() == sorted({g[f"file_{i}_src"].shape
+                                           for i in range(int(g["file_n"][0]))})
+
+
+@pytest.mark.parametrize("task", ["copy", "reverse"])
+def test_synthetic_task_matches_reference_golden(task):
+    import os
+    from conftest import GOLDEN
+    from paper_2110_05722_b200.config import RunConfig
+    from paper_2110_05722_b200.data import SyntheticTask
+    g = np.load(os.path.join(GOLDEN, "data.npz"))
+    run = RunConfig()
+    run.data.task = task
+    st = SyntheticTask(run)
+    for step in (0, 1, 7):
+        b = st.batch(step)
+        for k in ("src", "tgt_in", "tgt_out", "src_len"):
+            assert np.array_equal(np.asarray(getattr(b, k)), g[f"{task}_{step}_{k}"]), (step, k)
+
+
+def test_wmt_shaped_task_buckets_and_budget():
+    from paper_2110_05722_b200.data import WmtShapedTask
+    t = WmtShapedTask(4096, 64, 32000, seed=3)
+    shapes = set(t.possible_shapes())
+    seen = set()
+    for s in range(40):
+        b = t.batch(s)
+        src = np.asarray(b.src)
+        assert tuple(src.shape) in shapes
+        assert src.shape[1] % 4 == 0 and src.size <= 4096
+        lens = np.asarray(b.src_len)
+        assert lens.min() >= 1 and lens.max() <= src.shape[1]
+        assert np.all(src[np.arange(src.shape[1])[None, :] >= lens[:, None]] == 0)
+        seen.add(tuple(src.shape))
+        b2 = t.batch(s)
+        assert np.array_equal(np.asarray(b2.src), src)      # pure function of step
+    assert len(seen) > 4
