@@ -562,7 +562,10 @@ int launch_bwd(const AttnBwdArgs& a, int nbh, cudaStream_t st) {
       const char* e = getenv("LS2_ATTN_PERSIST");
       return !(e && e[0] == '0');
     }();
-    if (persist) {
+    // persistent only while the items roughly fill the resident CTA slots: with
+    // many small items (short sequences, e.g. L = 8 -> 4096 (batch, head) pairs)
+    // one CTA per item keeps them all in flight instead of serialising ~14 per CTA
+    if (persist && nbh <= 4 * kNumSMs) {
       constexpr int LQ = 16 * QT, LK = 16 * KT, PLD = LK + kPad;
       constexpr int NW = QT > KT ? QT : KT;
       const size_t sm = (size_t)(2 * (2 * LQ * kRow + 2 * LK * kRow + LQ * PLD) + LQ * PLD) * 2 +
