@@ -265,10 +265,22 @@ int ls2_gemm(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
  * (ptrs_ready=1: the caller guarantees ptr_scratch already holds this call's
  *  A/B/C pointer arrays, e.g. cached per static arena address) */
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2);
-/* weight-gradient GEMM on tcgen05/TMEM/TMA (hand-written, gemm_tc.cu): C[m x n] (f32,
- * row-major) = A^T B (+ C when beta), A [k x m] and B [k x n] fp16 row-major; a cluster
- * of S CTAs splits K and reduces through DSMEM (deterministic).  ls2_wgrad_tc_split
- * returns S, or 0 when the shape is not covered (m, n multiples of 128, one wave). */
+/* dense GEMM on tcgen05/TMEM/TMA (hand-written, gemm_tc.cu), the row-major
+ * convention of ls2_gemm_lt: C[m x n] = alpha*op(A)@op(B) (+ bias[n]) (+ C when beta = 1),
+ * A/B fp16 or bf16, C the same type or f32, fp32 accumulation in tensor memory.
+ * split = 0 picks the cluster split-K factor (1/2/4/8; small-output, long-K products
+ * reduce the partial tiles through DSMEM in rank order, deterministic).
+ * ls2_gemm_tc_supported: 1 when the shape/dtype/alignment is covered (n a multiple of 128,
+ * 16-byte aligned operands, ld multiples of 8; m and k arbitrary). */
+int ls2_gemm_tc_supported(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                          const void* A, int64_t lda, const void* B, int64_t ldb, double beta,
+                          const void* C, int64_t ldc, int tab, int tc);
+int ls2_gemm_tc(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+                const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                int64_t ldc, const void* bias, int tab, int tc, int split, void* stream);
+/* weight-gradient form of ls2_gemm_tc: C (f32) = A^T B (+ C when beta), A [k x m],
+ * B [k x n] fp16 row-major.  ls2_wgrad_tc_split returns the split factor it uses,
+ * or 0 when m, n are not multiples of 128. */
 int ls2_wgrad_tc_split(int64_t m, int64_t n, int64_t k);
 int ls2_wgrad_tc(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                  int64_t m, int64_t n, int64_t k, int beta, void* stream);

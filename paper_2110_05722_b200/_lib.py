@@ -79,6 +79,8 @@ _SIGS = {
     "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, I, P],
     "ls2_gemm_lt": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, P],
     "ls2_gemm_scratch_bytes": [L, L],
+    "ls2_gemm_tc_supported": [I, I, L, L, L, P, L, P, L, D, P, L, I, I],
+    "ls2_gemm_tc": [I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, I, P],
     "ls2_wgrad_tc_split": [L, L, L],
     "ls2_wgrad_tc": [P, L, P, L, P, L, L, L, L, I, P],
     "ls2_comm_load": [ctypes.c_char_p],
@@ -92,6 +94,7 @@ _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_
              "ls2_colsum_ws_bytes": L, "ls2_layernorm_bwd_ws_bytes": L,
              "ls2_attention_supported": ctypes.c_int, "ls2_colsum_nblk": ctypes.c_int,
              "ls2_layernorm_bwd_nblk": ctypes.c_int, "ls2_wgrad_tc_split": ctypes.c_int,
+             "ls2_gemm_tc_supported": ctypes.c_int,
              "ls2_gemm_scratch_bytes": L}
 
 _lib = None

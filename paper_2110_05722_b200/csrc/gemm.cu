@@ -233,12 +233,37 @@ static void lt_tune(Blas* bl, LtPlan* plan, const cublasLtMatmulHeuristicResult_
 
 /* C = alpha*op(A)@op(B) + beta*C (+ bias[n] broadcast over rows) on cuBLASLt, row-major.
  * Returns LS2_ERR_CUBLAS when no Lt algorithm supports the combination (caller falls back). */
+// which operand-major combinations go to the hand-written tcgen05 GEMM
+// (LS2_TC_GEMM: 'f' forward X W^T, 'd' data gradient dY W, 'w' weight gradient
+// dY^T X, 'a' all of them, '0' none)
+static bool tc_route(int trans_a, int trans_b) {
+  static int mask = [] {
+    const char* e = std::getenv("LS2_TC_GEMM");
+    const std::string s = e ? e : "";
+    int m = 0;
+    if (s.find('f') != std::string::npos) m |= 1;
+    if (s.find('d') != std::string::npos) m |= 2;
+    if (s.find('w') != std::string::npos) m |= 4;
+    if (s.find('a') != std::string::npos) m |= 7;
+    return m;
+  }();
+  if (!trans_a && trans_b) return mask & 1;
+  if (!trans_a && !trans_b) return mask & 2;
+  if (trans_a && !trans_b) return mask & 4;
+  return false;
+}
+
 static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
                      double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
                      double beta, void* C, int64_t ldc, const void* bias, int tab, int tc,
                      cudaStream_t st) {
-  if (!bl || !bl->lt) return fail(LS2_ERR_CUBLAS, "gemm_lt: no cublasLt handle");
   if (m <= 0 || n <= 0) return LS2_OK;
+  if (tc_route(trans_a, trans_b) &&
+      ls2_gemm_tc_supported(trans_a, trans_b, m, n, k, A, lda, B, ldb, beta, C, ldc, tab, tc) &&
+      (!bias || aligned16(bias)))
+    return ls2_gemm_tc(trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, bias, tab,
+                       tc, 0, st);
+  if (!bl || !bl->lt) return fail(LS2_ERR_CUBLAS, "gemm_lt: no cublasLt handle");
   if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_CUBLAS, "gemm_lt: f64 not routed to Lt");
   const int al = std::min(std::min(align_of(A), align_of(B)), std::min(align_of(C),
                           bias ? align_of(bias) : 256));

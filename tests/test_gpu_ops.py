@@ -547,3 +547,55 @@ def test_wgrad_tc_vs_torch(m, n, k, beta):
     _lib.call("ls2_wgrad_tc", a.data_ptr(), m, b.data_ptr(), n, c2.data_ptr(), n, m, n, k, beta,
               _lib.stream_handle())
     assert torch.equal(c, c2)
+
+
+# --- tcgen05 dense GEMM (all operand majors, tails, bias, beta, dtypes) -----------
+
+_TC_CASES = [
+    # (trans_a, trans_b, m, n, k)
+    (0, 1, 4096, 512, 512), (0, 1, 4068, 1536, 512), (0, 1, 300, 256, 2048),
+    (0, 1, 4096, 2048, 512), (0, 0, 4096, 512, 2048), (0, 0, 4068, 512, 512),
+    (0, 0, 1000, 512, 32000), (1, 0, 512, 512, 4096), (1, 0, 512, 2048, 4068),
+    (1, 0, 1536, 512, 4096), (1, 0, 128, 128, 100),
+]
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k", _TC_CASES)
+@pytest.mark.parametrize("variant", ["plain", "bias", "beta", "f32out", "bf16"])
+def test_gemm_tc_vs_torch(ta, tb, m, n, k, variant):
+    """ls2_gemm_tc (row-major, ls2_gemm_lt convention) against torch's fp32 product
+    of the same 16-bit operands: 1e-5 relative for f32 output, one output
+    rounding (2^-8 / 2^-11 relative) for 16-bit output; deterministic bits."""
+    from paper_2110_05722_b200 import _lib
+    lib = _lib.load_library()
+    torch.manual_seed(m + 7 * n + 13 * k + ta + 2 * tb)
+    dt = torch.bfloat16 if variant == "bf16" else torch.float16
+    odt = torch.float32 if variant in ("f32out", "beta") else dt
+    A = (torch.randn(k, m, device="cuda") if ta else torch.randn(m, k, device="cuda")) * 0.5
+    B = (torch.randn(n, k, device="cuda") if tb else torch.randn(k, n, device="cuda")) * 0.5
+    A, B = A.to(dt), B.to(dt)
+    bias = (torch.randn(n, device="cuda") * 2).to(odt) if variant == "bias" else None
+    c0 = torch.randn(m, n, device="cuda").to(odt)
+    c = c0.clone()
+    beta = 1.0 if variant == "beta" else 0.0
+    alpha = 0.75 if variant == "f32out" else 1.0
+    args = (ta, tb, m, n, k, alpha, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], beta,
+            c.data_ptr(), n, _lib.ptr(bias), _lib.dtype_code(dt), _lib.dtype_code(odt), 0,
+            _lib.stream_handle())
+    assert lib.ls2_gemm_tc_supported(ta, tb, m, n, k, A.data_ptr(), A.shape[1], B.data_ptr(),
+                                     B.shape[1], beta, c.data_ptr(), n, _lib.dtype_code(dt),
+                                     _lib.dtype_code(odt))
+    _lib.call("ls2_gemm_tc", *args)
+    opA = A.float().t() if ta else A.float()
+    opB = B.float().t() if tb else B.float()
+    want = alpha * (opA @ opB)
+    if bias is not None:
+        want = want + bias.float()
+    if beta:
+        want = want + c0.float()
+    err = ((c.float() - want).abs().max() / want.abs().max()).item()
+    tol = 1e-5 if odt == torch.float32 else (8e-3 if dt == torch.bfloat16 else 1e-3)
+    assert err <= tol, err
+    c2 = c0.clone()
+    _lib.call("ls2_gemm_tc", *args[:11], c2.data_ptr(), *args[12:])
+    assert torch.equal(c, c2)
