@@ -595,9 +595,18 @@ int launch_bwd(const AttnBwdArgs& a, int nbh, cudaStream_t st) {
   X(1, 1, __VA_ARGS__) X(1, 2, __VA_ARGS__) X(1, 4, __VA_ARGS__) X(1, 8, __VA_ARGS__)      \
   X(2, 1, __VA_ARGS__) X(2, 2, __VA_ARGS__) X(2, 4, __VA_ARGS__) X(2, 8, __VA_ARGS__)      \
   X(4, 1, __VA_ARGS__) X(4, 2, __VA_ARGS__) X(4, 4, __VA_ARGS__) X(4, 8, __VA_ARGS__)      \
-  X(8, 1, __VA_ARGS__) X(8, 2, __VA_ARGS__) X(8, 4, __VA_ARGS__) X(8, 8, __VA_ARGS__)
+  X(8, 1, __VA_ARGS__) X(8, 2, __VA_ARGS__) X(8, 4, __VA_ARGS__) X(8, 8, __VA_ARGS__)      \
+  X(3, 3, __VA_ARGS__)
 
+// 16-row tile counts per (lq, lk): powers of two, plus 48 x 48 for the square
+// 33..48 buckets of length-bucketed batches (L = 36 would otherwise pad to 64
+// and spend 1.8x the work)
 inline int tiles_of(int L) { return L <= 16 ? 1 : L <= 32 ? 2 : L <= 64 ? 4 : 8; }
+inline void tile_pair(int lq, int lk, int& qt, int& kt) {
+  qt = tiles_of(lq);
+  kt = tiles_of(lk);
+  if (qt == 4 && kt == 4 && lq <= 48 && lk <= 48) qt = kt = 3;
+}
 
 }  // namespace ls2
 
@@ -620,7 +629,8 @@ int ls2_attention_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, co
   AttnArgs a{(const __half*)q, (const __half*)k, (const __half*)v, ldq, ldk, ldv,
              (__half*)probs, (__half*)o, ldo, (int)heads, (int)lq, (int)lk, mask_kind, lens,
              (float)scale};
-  const int qt = tiles_of((int)lq), kt = tiles_of((int)lk);
+  int qt, kt;
+  tile_pair((int)lq, (int)lk, qt, kt);
   const int nbh = (int)(batch * heads);
   cudaStream_t st = as_stream(stream);
 #define LS2_FWD_CASE(QT_, KT_, ...) if (qt == QT_ && kt == KT_) return launch_fwd<QT_, KT_>(a, nbh, st);
@@ -651,7 +661,8 @@ int ls2_attention_bwd_bias(const void* q, int64_t ldq, const void* k, int64_t ld
                 (const __half*)dout, ldq, ldk, ldv, lddo, (__half*)dq, (__half*)dk, (__half*)dv,
                 lddq, lddk, lddv, (int)heads, (int)lq, (int)lk, (float)scale,
                 csq, csk, csv, ldcsq, ldcsk, ldcsv};
-  const int qt = tiles_of((int)lq), kt = tiles_of((int)lk);
+  int qt, kt;
+  tile_pair((int)lq, (int)lk, qt, kt);
   const int nbh = (int)(batch * heads);
   cudaStream_t st = as_stream(stream);
 #define LS2_BWD_CASE(QT_, KT_, ...) if (qt == QT_ && kt == KT_) return launch_bwd<QT_, KT_>(a, nbh, st);

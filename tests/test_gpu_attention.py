@@ -35,7 +35,8 @@ def _ref(q, k, v, keep, dout, scale):
 @pytest.mark.parametrize("B,NH,Lq,Lk,kind", [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"),
                                              (3, 2, 37, 37, "causal"), (4, 16, 128, 128, "padding"),
                                              (5, 3, 20, 52, "padding"), (2, 4, 7, 100, "none"),
-                                             (2, 2, 128, 16, "none")])
+                                             (2, 2, 128, 16, "none"), (113, 8, 36, 36, "padding"),
+                                             (10, 8, 48, 48, "causal"), (7, 2, 33, 45, "padding")])
 def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind):
     rng = np.random.default_rng(B * 100 + Lq)
     d = 64 * NH
