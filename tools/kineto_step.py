@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--top", type=int, default=45)
     ap.add_argument("--model", default="tbase", choices=["tbase", "tbig"])
+    ap.add_argument("--shape", default=None, help="BxL batch shape (e.g. 512x8, a WMT bucket)")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -30,6 +31,8 @@ def main():
 
     from paper_2110_05722_b200.config import transformer_big
     B, L, V = (64, 64, 32000) if a.model == "tbase" else (64, 128, 32000)
+    if a.shape:
+        B, L = (int(x) for x in a.shape.lower().split("x"))
     run = RunConfig(model=transformer_base(V, 256) if a.model == "tbase" else
                     transformer_big(V, 256),
                     train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L))
