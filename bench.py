@@ -47,6 +47,14 @@ MODELS = {"tbase": (64, 64, "Transformer-base 6e6d, d512 h8 f2048 V32000"),
           "bert512": (16, 512, "BERT-base-shaped 12e, d768 h12 f3072 V30522, MLM 15%")}
 
 
+def _step_tokens(bt, bert: bool) -> int:
+    """tokens a step counts: non-pad target tokens (the reference's tokens_per_sec,
+    F/engine.py:164-167); for the BERT-shaped MLM model every non-pad input token
+    (the usual BERT convention; only 15% of positions carry targets)."""
+    a = np.asarray(bt.src) if bert else np.asarray(bt.tgt_out)
+    return int((a != bt.pad_id).sum())
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -278,7 +286,7 @@ def run_ours(args):
         k = ("train",) + tuple(np.asarray(bt.src).shape)
         plan.append((k, [torch.as_tensor(np.asarray(a), dtype=torch.int64).cuda()
                          for a in (bt.src, bt.tgt_in, bt.tgt_out, bt.src_len)],
-                     int((np.asarray(bt.tgt_out) != bt.pad_id).sum())))
+                     _step_tokens(bt, bert)))
     step_tokens = sum(t for _, _, t in plan)
     st = torch.cuda.current_stream()
     launches0 = _lib.launches()
@@ -318,7 +326,9 @@ def run_ours(args):
     e2e_tokens = 0
     for s in range(args.steps):
         m = eng.train_step(10_000 + s)   # each step ends with a blocking D2H of its metrics
-        e2e_tokens += m.tokens
+        # BERT: every input token (MLMTask inputs carry no padding); Transformer:
+        # the step's non-pad targets
+        e2e_tokens += m.tokens if not bert else B * L
     e1.record(st)
     torch.cuda.synchronize()
     wall_ms = 1e3 * (time.perf_counter() - t0) / args.steps

@@ -88,6 +88,43 @@ struct alignas(16) Pack8 {
   T v[8];
 };
 
+// elements 2e, 2e+1 of a pack widened to fp32 (one packed conversion for 16-bit types)
+template <typename T> __device__ __forceinline__ float2 pair_f2(const Pack8<T>& p, int e);
+template <> __device__ __forceinline__ float2 pair_f2<__half>(const Pack8<__half>& p, int e) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&p.v[2 * e]));
+}
+template <> __device__ __forceinline__ float2 pair_f2<__nv_bfloat16>(const Pack8<__nv_bfloat16>& p, int e) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&p.v[2 * e]));
+}
+template <> __device__ __forceinline__ float2 pair_f2<float>(const Pack8<float>& p, int e) {
+  return make_float2(p.v[2 * e], p.v[2 * e + 1]);
+}
+
+// packed fp32 pair arithmetic (sm_100 FFMA2 / FADD2 / FMUL2), each lane rounded
+// exactly like its scalar counterpart
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
+
 template <typename T>
 __device__ __forceinline__ Pack8<T> ld8(const T* p) {
   Pack8<T> r;

@@ -429,45 +429,52 @@ ln_bwd_stage(
       }
       const float m_r = (float)mu[r];
       const float rs = (float)(1.0 / (double)sigma[r]);
-      float r1 = 0.f, r3 = 0.f;
+      // packed pair math: xh = x*rs - m*rs, gg = w*dy, sums of gg and gg*xh
+      const float2 rs2 = f2s(rs), nmrs2 = f2s(-m_r * rs);
+      float2 r1v = f2s(0.f), r3v = f2s(0.f);
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         const int64_t g = lane + 32 * it;
         if (g < cgs) {
-          float c0[8], c1[8];
+          float2 c0[4], c1[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float dv = cvt<float>(cd[it].v[e]);
-            const float xh = (cvt<float>(cx[it].v[e]) - m_r) * rs;
-            const float gg = cvt<float>(wv[it].v[e]) * dv;
-            r1 += gg;
-            r3 += gg * xh;
-            c0[e] = dv * xh;
+          for (int e = 0; e < 4; ++e) {
+            const float2 dv = pair_f2(cd[it], e);
+            const float2 xh = f2fma(pair_f2(cx[it], e), rs2, nmrs2);
+            const float2 gg = f2mul(pair_f2(wv[it], e), dv);
+            r1v = f2add(r1v, gg);
+            r3v = f2fma(gg, xh, r3v);
+            c0[e] = f2mul(dv, xh);
             c1[e] = dv;
           }
           float4* d0 = reinterpret_cast<float4*>(my + g * 8);
-          d0[0] = make_float4(c0[0], c0[1], c0[2], c0[3]);
-          d0[1] = make_float4(c0[4], c0[5], c0[6], c0[7]);
+          d0[0] = make_float4(c0[0].x, c0[0].y, c0[1].x, c0[1].y);
+          d0[1] = make_float4(c0[2].x, c0[2].y, c0[3].x, c0[3].y);
           float4* d1 = reinterpret_cast<float4*>(my + cols + g * 8);
-          d1[0] = make_float4(c1[0], c1[1], c1[2], c1[3]);
-          d1[1] = make_float4(c1[4], c1[5], c1[6], c1[7]);
+          d1[0] = make_float4(c1[0].x, c1[0].y, c1[1].x, c1[1].y);
+          d1[1] = make_float4(c1[2].x, c1[2].y, c1[3].x, c1[3].y);
         }
       }
-      r1 = warp_sum(r1) * inv_m;
-      r3 = warp_sum(r3) * inv_m;
+      const float r1 = warp_sum(r1v.x + r1v.y) * inv_m;
+      const float r3 = warp_sum(r3v.x + r3v.y) * inv_m;
+      const float2 nr1 = f2s(-r1), nr3 = f2s(-r3);
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         const int64_t g = lane + 32 * it;
         if (g < cgs) {
           Pack8<Tout> o;
+          float2 ov[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float dv = cvt<float>(cd[it].v[e]);
-            const float xh = (cvt<float>(cx[it].v[e]) - m_r) * rs;
-            const float gg = cvt<float>(wv[it].v[e]) * dv;
-            float v = (gg - r1 - xh * r3) * rs;
-            if (RES) v += cvt<float>(cr[it].v[e]);
-            o.v[e] = cvt<Tout>(v);
+          for (int e = 0; e < 4; ++e) {
+            const float2 dv = pair_f2(cd[it], e);
+            const float2 xh = f2fma(pair_f2(cx[it], e), rs2, nmrs2);
+            const float2 gg = f2mul(pair_f2(wv[it], e), dv);
+            // (gg - r1 - xh*r3) * rs (+ dres)
+            float2 v = f2mul(f2fma(xh, nr3, f2add(gg, nr1)), rs2);
+            if (RES) v = f2add(v, pair_f2(cr[it], e));
+            o.v[2 * e] = cvt<Tout>(v.x);
+            o.v[2 * e + 1] = cvt<Tout>(v.y);
+            ov[e] = v;
           }
           st8(dx + r * cols + g * 8, o);
           if (BDR) {
@@ -481,6 +488,7 @@ ln_bwd_stage(
               c2[e] = v;
               pj.v[e] = cvt<Tout>(v);
             }
+            (void)ov;
             st8(dproj + r * cols + g * 8, pj);
             float4* d2 = reinterpret_cast<float4*>(my + 2 * cols + g * 8);
             d2[0] = make_float4(c2[0], c2[1], c2[2], c2[3]);
