@@ -33,6 +33,44 @@ __device__ __forceinline__ void st_group(T* p, const C (&v)[8]) {
   st8(p, q);
 }
 
+// fp32 LayerNorm row pieces in packed f32x2 pair math (per-lane rounding identical
+// to the scalar expressions they replace; the statistics accumulate even/odd
+// elements in two partial sums)
+template <typename T, int ITERS>
+__device__ __forceinline__ void row_stats_f2(const Pack8<T> (&v)[ITERS], int lane, int64_t cgs,
+                                             float pivot, float& s1, float& s2) {
+  float2 a = f2s(0.f), q = f2s(0.f);
+  const float2 np = f2s(-pivot);
+#pragma unroll
+  for (int it = 0; it < ITERS; ++it) {
+    if (lane + 32 * it < cgs) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 d = f2add(pair_f2(v[it], e), np);
+        a = f2add(a, d);
+        q = f2fma(d, d, q);
+      }
+    }
+  }
+  s1 = a.x + a.y;
+  s2 = q.x + q.y;
+}
+
+// o = ((v - pivot) - msh) * rs * w + b for 8 elements
+template <typename T, typename TW>
+__device__ __forceinline__ void ln_norm8_f2(const Pack8<T>& v, const Pack8<TW>& w,
+                                            const Pack8<TW>& b, float pivot, float msh, float rs,
+                                            float* o) {
+  const float2 np = f2s(-pivot), nm = f2s(-msh), r2 = f2s(rs);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = f2mul(f2add(f2add(pair_f2(v, e), np), nm), r2);
+    const float2 y = f2fma(t, pair_f2(w, e), pair_f2(b, e));
+    o[2 * e] = y.x;
+    o[2 * e + 1] = y.y;
+  }
+}
+
 template <typename Tin, typename Tout, typename Tstat, int ITERS>
 __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_warp(
     const Tin* __restrict__ x, const Tin* __restrict__ w, const Tin* __restrict__ b,
@@ -62,14 +100,18 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_warp(
     }
     const C pivot = __shfl_sync(0xffffffffu, cvt<C>(v[0].v[0]), 0);
     C s1 = 0, s2 = 0;
+    if constexpr (std::is_same<C, float>::value) {
+      row_stats_f2(v, lane, cgs, pivot, s1, s2);
+    } else {
 #pragma unroll
-    for (int it = 0; it < ITERS; ++it) {
-      if (lane + 32 * it < cgs) {
+      for (int it = 0; it < ITERS; ++it) {
+        if (lane + 32 * it < cgs) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const C d = cvt<C>(v[it].v[e]) - pivot;
-          s1 += d;
-          s2 += d * d;
+          for (int e = 0; e < 8; ++e) {
+            const C d = cvt<C>(v[it].v[e]) - pivot;
+            s1 += d;
+            s2 += d * d;
+          }
         }
       }
     }
@@ -93,9 +135,13 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_warp(
       if (g < cgs) {
         C o[8];
         const Pack8<Tin> wq = sw[g], bq = sb[g];
+        if constexpr (std::is_same<C, float>::value) {
+          ln_norm8_f2(v[it], wq, bq, pivot, msh, rs, o);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
+          for (int e = 0; e < 8; ++e)
+            o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
+        }
         st_group(yr + g * 8, o);
       }
     }
@@ -136,9 +182,8 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
       if (g < cgs) {
-        C xv[8], rv[8];
-        ld_group(x + r * cols + g * 8, xv);
-        ld_group(res + r * cols + g * 8, rv);
+        const Pack8<Tin> px = ld8(x + r * cols + g * 8);
+        const Pack8<Tin> pr = ld8(res + r * cols + g * 8);
         uint32_t kb = 0xFF;
         if (DROP) {
           if (GEN) {
@@ -150,11 +195,27 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
         }
         Pack8<Tout> q;
         const Pack8<Tin> cq = sc[g];
+        if constexpr (std::is_same<C, float>::value) {
+          const float2 ds2 = f2s(dscale);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          C a = add_rn(xv[e], cvt<C>(cq.v[e]));
-          if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), dscale);
-          q.v[e] = cvt<Tout>(add_rn(a, rv[e]));
+          for (int e = 0; e < 4; ++e) {
+            float2 a = f2add(pair_f2(px, e), pair_f2(cq, e));
+            if (DROP) {
+              const float2 k2 = make_float2(__uint_as_float(((kb >> (2 * e)) & 1u) * 0x3f800000u),
+                                            __uint_as_float(((kb >> (2 * e + 1)) & 1u) * 0x3f800000u));
+              a = f2mul(f2mul(a, k2), ds2);
+            }
+            const float2 y = f2add(a, pair_f2(pr, e));
+            q.v[2 * e] = cvt<Tout>(y.x);
+            q.v[2 * e + 1] = cvt<Tout>(y.y);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            C a = add_rn(cvt<C>(px.v[e]), cvt<C>(cq.v[e]));
+            if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), dscale);
+            q.v[e] = cvt<Tout>(add_rn(a, cvt<C>(pr.v[e])));
+          }
         }
         v[it] = q;
         st8(yres + r * cols + g * 8, q);
@@ -162,14 +223,18 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
     }
     const C pivot = __shfl_sync(0xffffffffu, cvt<C>(v[0].v[0]), 0);
     C s1 = 0, s2 = 0;
+    if constexpr (std::is_same<C, float>::value) {
+      row_stats_f2(v, lane, cgs, pivot, s1, s2);
+    } else {
 #pragma unroll
-    for (int it = 0; it < ITERS; ++it) {
-      if (lane + 32 * it < cgs) {
+      for (int it = 0; it < ITERS; ++it) {
+        if (lane + 32 * it < cgs) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const C d = cvt<C>(v[it].v[e]) - pivot;
-          s1 += d;
-          s2 += d * d;
+          for (int e = 0; e < 8; ++e) {
+            const C d = cvt<C>(v[it].v[e]) - pivot;
+            s1 += d;
+            s2 += d * d;
+          }
         }
       }
     }
@@ -191,9 +256,13 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
       if (g < cgs) {
         C o[8];
         const Pack8<Tin> wq = sw[g], bq = sb[g];
+        if constexpr (std::is_same<C, float>::value) {
+          ln_norm8_f2(v[it], wq, bq, pivot, msh, rs, o);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
+          for (int e = 0; e < 8; ++e)
+            o[e] = ((cvt<C>(v[it].v[e]) - pivot) - msh) * rs * cvt<C>(wq.v[e]) + cvt<C>(bq.v[e]);
+        }
         st_group(u + r * cols + g * 8, o);
       }
     }
