@@ -153,6 +153,9 @@ __device__ __forceinline__ void cta_colsum_store(const C (&acc)[8], int64_t cgs,
   }
 }
 
+// rows a thread of the vectorised elementwise kernels has in flight per pass
+constexpr int kRowsInFlight = 4;
+
 template <typename C>
 __device__ __forceinline__ C* colsum_smem() {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(1024) brd_fwd_vec(const Tin* __restrict__ x, c
   const int64_t cg = threadIdx.x % cgs;
   C b[8];
   load_row_group(bias + cg * 8, b);
+  // (one row per pass: unrolling 4 rows in flight measured slower here, 7.97 -> 8.34 us)
   for (int64_t r = (int64_t)blockIdx.x * rpp + lane_row; r < rows; r += (int64_t)gridDim.x * rpp) {
     const int64_t g = r * cgs + cg;
     C xv[8];
@@ -361,19 +365,38 @@ __global__ void __launch_bounds__(1024) brd_bwd_vec(const Tin* __restrict__ dy, 
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0;
   if (lane_row < rpp) {
-    for (int64_t r = (int64_t)blockIdx.x * rpp + lane_row; r < rows; r += (int64_t)gridDim.x * rpp) {
-      const int64_t g = r * cgs + cg;
-      C d[8];
-      load_row_group(dy + g * 8, d);
-      const uint32_t rb = rbits[g];
-      const uint32_t kb = DROP ? kbits[g] : 0xFF;
+    // kRowsInFlight rows per pass: all their loads issue before any use, so a
+    // thread keeps several 16-byte reads in flight (same row order as a plain
+    // grid-stride loop: the column sums are unchanged bit for bit)
+    const int64_t stride = (int64_t)gridDim.x * rpp;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpp + lane_row; r0 < rows; r0 += kRowsInFlight * stride) {
+      Pack8<Tin> pd[kRowsInFlight];
+      uint32_t rb[kRowsInFlight], kb[kRowsInFlight];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        d[e] = mul_rn(d[e], (C)((rb >> e) & 1));
-        if (DROP) d[e] = mul_rn(mul_rn(d[e], (C)((kb >> e) & 1)), scale);
-        acc[e] += d[e];
+      for (int u = 0; u < kRowsInFlight; ++u) {
+        const int64_t r = r0 + u * stride;
+        if (r < rows) {
+          const int64_t g = r * cgs + cg;
+          pd[u] = ld8_stream(dy + g * 8);
+          rb[u] = rbits[g];
+          kb[u] = DROP ? kbits[g] : 0xFF;
+        }
       }
-      store_row_group(dx + g * 8, d);
+#pragma unroll
+      for (int u = 0; u < kRowsInFlight; ++u) {
+        const int64_t r = r0 + u * stride;
+        if (r < rows) {
+          const int64_t g = r * cgs + cg;
+          C d[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            d[e] = mul_rn(cvt<C>(pd[u].v[e]), (C)((rb[u] >> e) & 1));
+            if (DROP) d[e] = mul_rn(mul_rn(d[e], (C)((kb[u] >> e) & 1)), scale);
+            acc[e] += d[e];
+          }
+          store_row_group(dx + g * 8, d);
+        }
+      }
     }
   }
   cta_colsum_store(acc, cgs, rpp, cols, partial, colsum_smem<C>());
