@@ -16,6 +16,9 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
+#include <cstring>
+#include <string>
 
 #include <algorithm>
 
@@ -152,10 +155,55 @@ static bool tuning_enabled(int tc = -1) {
 // not the few microseconds of host overhead per cublasLtMatmul call.
 constexpr int kTuneReps = 8;
 
+// LS2_GEMM_PICK="<tag substring>=<heuristic index>;..." pins the algorithm of the
+// plans whose tag contains the substring (in-step A/B experiments, see
+// tools/gemm_pick_sweep.sh); LS2_GEMM_LIST=1 prints every plan's candidates.
+static std::vector<std::pair<std::string, int>> gemm_picks() {
+  std::vector<std::pair<std::string, int>> out;
+  const char* e = getenv("LS2_GEMM_PICK");
+  if (!e) return out;
+  std::string s(e);
+  size_t pos = 0;
+  while (pos < s.size()) {
+    size_t end = s.find(';', pos);
+    if (end == std::string::npos) end = s.size();
+    const std::string item = s.substr(pos, end - pos);
+    const size_t eq = item.rfind('=');
+    if (eq != std::string::npos) out.emplace_back(item.substr(0, eq), std::atoi(item.c_str() + eq + 1));
+    pos = end + 1;
+  }
+  return out;
+}
+
+static void lt_describe(const cublasLtMatmulAlgo_t& a, int& tile, int& stages, int& splitk) {
+  size_t w = 0;
+  tile = stages = splitk = 0;
+  cublasLtMatmulAlgoConfigGetAttribute(&a, CUBLASLT_ALGO_CONFIG_TILE_ID, &tile, sizeof(tile), &w);
+  cublasLtMatmulAlgoConfigGetAttribute(&a, CUBLASLT_ALGO_CONFIG_STAGES_ID, &stages, sizeof(stages), &w);
+  cublasLtMatmulAlgoConfigGetAttribute(&a, CUBLASLT_ALGO_CONFIG_SPLITK_NUM, &splitk, sizeof(splitk), &w);
+}
+
 static void lt_tune(Blas* bl, LtPlan* plan, const cublasLtMatmulHeuristicResult_t* res, int found,
                     const void* A, const void* B, double beta, void* C, int64_t m, int64_t ldc,
                     int tc, cudaStream_t st) {
   plan->algo = res[0].algo;
+  static const bool list = getenv("LS2_GEMM_LIST") != nullptr;
+  if (list) {
+    for (int i = 0; i < found; ++i) {
+      int tile, stages, splitk;
+      lt_describe(res[i].algo, tile, stages, splitk);
+      fprintf(stderr, "[ls2 gemm list] %s #%d tile=%d stages=%d splitk=%d ws=%zu\n", plan->tag, i,
+              tile, stages, splitk, res[i].workspaceSize);
+    }
+  }
+  static const std::vector<std::pair<std::string, int>> picks = gemm_picks();
+  for (const auto& pk : picks) {
+    if (strstr(plan->tag, pk.first.c_str()) && pk.second >= 0 && pk.second < found &&
+        res[pk.second].workspaceSize <= bl->ws_bytes) {
+      plan->algo = res[pk.second].algo;
+      return;
+    }
+  }
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
   if (found <= 1 || !tuning_enabled(tc) || cap != cudaStreamCaptureStatusNone) return;
