@@ -325,7 +325,9 @@ def run_ours(args):
     e0.record(st)
     e2e_tokens = 0
     for s in range(args.steps):
-        m = eng.train_step(10_000 + s)   # each step ends with a blocking D2H of its metrics
+        # the same step numbers (so the same WMT bucket sequence) as the value loop:
+        # e2e - value is then the host-side cost alone, not a different bucket mix
+        m = eng.train_step(warm + s)     # each step ends with a blocking D2H of its metrics
         # BERT: every input token (MLMTask inputs carry no padding); Transformer:
         # the step's non-pad targets
         e2e_tokens += m.tokens if not bert else B * L
