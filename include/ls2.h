@@ -284,6 +284,15 @@ int ls2_gemm_tc(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, doubl
 int ls2_wgrad_tc_split(int64_t m, int64_t n, int64_t k);
 int ls2_wgrad_tc(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                  int64_t m, int64_t n, int64_t k, int beta, void* stream);
+/* GEMM on cuBLASLt that also writes a bias gradient from its epilogue (BGRADA/B):
+ * which = 0 -> bgrad[i] = sum_k op(A)[i, k] (length m), 1 -> bgrad[j] = sum_k op(B)[k, j]
+ * (length n); bgrad has type tc (fp32 accumulation).  The weight gradient dW = dY^T X
+ * with which = 0 yields the layer's bias gradient sum_rows dY in the same pass
+ * (F/model.py:501,726,766).  LS2_ERR_CUBLAS if Lt has no algorithm for it. */
+int ls2_gemm_lt_bgrad(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                      double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                      double beta, void* C, int64_t ldc, void* bgrad, int which, int tab, int tc,
+                      void* stream);
 /* plain GEMM on cuBLASLt with an optional fused bias epilogue (C += bias[n] per row);
  * LS2_ERR_CUBLAS if no Lt algorithm supports the combination (caller falls back) */
 int ls2_gemm_lt(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,

@@ -301,12 +301,15 @@ static bool tc_route(int trans_a, int trans_b) {
   return false;
 }
 
+// bmode: 0 none, 1 bias add (bias[n]), 2 bias gradient of op(A) (sum over K -> [m]),
+// 3 bias gradient of op(B) (sum over K -> [n]); the gradient vector has type tc
 static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
                      double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
                      double beta, void* C, int64_t ldc, const void* bias, int tab, int tc,
-                     cudaStream_t st) {
+                     cudaStream_t st, int bmode = -1) {
+  if (bmode < 0) bmode = bias ? 1 : 0;
   if (m <= 0 || n <= 0) return LS2_OK;
-  if (tc_route(trans_a, trans_b) &&
+  if (bmode <= 1 && tc_route(trans_a, trans_b) &&
       ls2_gemm_tc_supported(trans_a, trans_b, m, n, k, A, lda, B, ldb, beta, C, ldc, tab, tc) &&
       (!bias || aligned16(bias)))
     return ls2_gemm_tc(trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, bias, tab,
@@ -315,7 +318,7 @@ static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, i
   if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_CUBLAS, "gemm_lt: f64 not routed to Lt");
   const int al = std::min(std::min(align_of(A), align_of(B)), std::min(align_of(C),
                           bias ? align_of(bias) : 256));
-  LtKey key{trans_a, trans_b, m, n, k, lda, ldb, ldc, tab, tc, bias != nullptr, beta != 0.0, al};
+  LtKey key{trans_a, trans_b, m, n, k, lda, ldb, ldc, tab, tc, bmode, beta != 0.0, al};
   LtPlan* plan;
   {
     std::lock_guard<std::mutex> g(bl->mu);
@@ -327,14 +330,16 @@ static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, i
       cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_TRANSA, &opA, sizeof(opA));
       cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_TRANSB, &opB, sizeof(opB));
       if (bias) {
-        cublasLtEpilogue_t ep = CUBLASLT_EPILOGUE_BIAS;
+        // row-major A/B are Lt's B/A (the product is computed transposed)
+        cublasLtEpilogue_t ep = bmode == 2 ? CUBLASLT_EPILOGUE_BGRADB
+                              : bmode == 3 ? CUBLASLT_EPILOGUE_BGRADA : CUBLASLT_EPILOGUE_BIAS;
         cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof(ep));
         cudaDataType_t bt = cuda_type(tc);
         cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt));
         cublasLtMatmulDescSetAttribute(plan->op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
       }
       snprintf(plan->tag, sizeof(plan->tag), "ta=%d tb=%d m=%lld n=%lld k=%lld tab=%d tc=%d bias=%d",
-               trans_a, trans_b, (long long)m, (long long)n, (long long)k, tab, tc, bias != nullptr);
+               trans_a, trans_b, (long long)m, (long long)n, (long long)k, tab, tc, bmode);
       const cudaDataType_t tAB = cuda_type(tab), tC = cuda_type(tc);
       cublasLtMatrixLayoutCreate(&plan->a, tAB, trans_b ? k : n, trans_b ? n : k, ldb);
       cublasLtMatrixLayoutCreate(&plan->b, tAB, trans_a ? m : k, trans_a ? k : m, lda);
@@ -377,6 +382,15 @@ int ls2_gemm_lt(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_
                 int64_t ldc, const void* bias, int tab, int tc, void* stream) {
   return lt_matmul(reinterpret_cast<Blas*>(hp), trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb,
                    beta, C, ldc, bias, tab, tc, as_stream(stream));
+}
+
+int ls2_gemm_lt_bgrad(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                      double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                      double beta, void* C, int64_t ldc, void* bgrad, int which, int tab, int tc,
+                      void* stream) {
+  if (!bgrad) return fail(LS2_ERR_SHAPE, "gemm_lt_bgrad: null gradient vector");
+  return lt_matmul(reinterpret_cast<Blas*>(hp), trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb,
+                   beta, C, ldc, bgrad, tab, tc, as_stream(stream), which ? 3 : 2);
 }
 
 int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2) { return 3 * n1 * n2 * (int64_t)sizeof(void*); }
