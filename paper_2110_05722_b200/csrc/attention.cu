@@ -247,26 +247,42 @@ struct AttnBwdArgs {
 };
 
 // column sums of one warp's 16-row tile of a result (the fp16-rounded values
-// the kernel stores; rows >= valid excluded), folded over the 8 row lanes in a
-// fixed order; lanes 0..3 leave columns 8j + 2t, +1 in cs[0..63]
+// the kernel stores; rows >= valid excluded).  Each thread holds rows g, g+8 of
+// columns 8j + 2t, +1 (j < 8); the sum over the 8 row groups g is a fixed-order
+// reduce-scatter (halve the columns per xor-16/8/4 round: 8 + 4 + 2 shuffles
+// instead of 48), after which lane (g, t) owns columns 8g + 2t, +1 -> cs[0..63].
 __device__ __forceinline__ void tile_colsum(const float (&acc)[8][4], int r0, int valid,
                                             float* cs, int lane) {
   const int g = lane >> 2, t = lane & 3;
+  float v[16];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float2 v0 = r0 < valid ? unpack_h2(pack_h2(acc[j][0], acc[j][1])) : make_float2(0.f, 0.f);
     const float2 v1 = r0 + 8 < valid ? unpack_h2(pack_h2(acc[j][2], acc[j][3])) : make_float2(0.f, 0.f);
-    float sx = v0.x + v1.x, sy = v0.y + v1.y;
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      sx += __shfl_xor_sync(0xffffffffu, sx, o);
-      sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    }
-    if (g == 0) {
-      cs[8 * j + 2 * t] = sx;
-      cs[8 * j + 2 * t + 1] = sy;
-    }
+    v[2 * j] = v0.x + v1.x;
+    v[2 * j + 1] = v0.y + v1.y;
   }
+  const bool h2 = (g & 4) != 0, h1 = (g & 2) != 0, h0 = (g & 1) != 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {            // xor 16: keep half [8*h2, 8*h2 + 8)
+    const float send = h2 ? v[q] : v[8 + q];
+    const float keep = h2 ? v[8 + q] : v[q];
+    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {            // xor 8
+    const float send = h1 ? v[q] : v[4 + q];
+    const float keep = h1 ? v[4 + q] : v[q];
+    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {            // xor 4
+    const float send = h0 ? v[q] : v[2 + q];
+    const float keep = h0 ? v[2 + q] : v[q];
+    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  cs[8 * g + 2 * t] = v[0];
+  cs[8 * g + 2 * t + 1] = v[1];
 }
 
 // fold the per-warp tile sums in warp order and write the f64 partial rows
