@@ -55,6 +55,22 @@ def _step_tokens(bt, bert: bool) -> int:
     return int((a != bt.pad_id).sum())
 
 
+def warm_up(eng, keys, min_steps: int, dp, cap: int = 4000) -> int:
+    """Untimed steps until at least `min_steps` ran and every bucket shape in `keys`
+    has its CUDA graph, on EVERY rank: with WMT-shaped data each rank draws its
+    own bucket sequence, so the stop decision is a max over ranks (otherwise a rank
+    that is done would leave the others blocked in the gradient all-reduce).
+    Returns the number of steps run (the same on all ranks)."""
+    s = 0
+    while True:
+        missing = any(k not in eng._graphs for k in keys)
+        need = 1.0 if (s < min_steps or (missing and s < cap)) else 0.0
+        if dp.max_scalar(need, device=getattr(eng, "device", None)) <= 0.0:
+            return s
+        eng.train_step(s)
+        s += 1
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -271,11 +287,7 @@ def run_ours(args):
     # warm-up (first step of a bucket eager, then graph capture, then replays);
     # WMT-shaped data keeps stepping until every bucket shape has its graph
     keys = [("train",) + tuple(sh) for sh in task.possible_shapes()]
-    s = 0
-    while s < max(args.warmup, 3) or (any(k not in eng._graphs for k in keys) and s < 4000):
-        eng.train_step(s)
-        s += 1
-    warm = s
+    warm = warm_up(eng, keys, max(args.warmup, 3), dp)
     torch.cuda.synchronize()
     dev_graphs = {k: eng.capture_device_graph(k) for k in keys}
     dev_graph = dev_graphs.get(key)

@@ -153,3 +153,54 @@ def test_grad_exchange_plan_small_buckets_cover_exactly():
     assert spans[0][1] == n and spans[-1][0] == 0
     assert all(a[0] == b[1] for a, b in zip(spans, spans[1:]))
     assert all(e - s >= 40 for s, e in spans[:-1])
+
+
+def _warm_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_2110_05722_b200.data import WmtShapedTask
+    from paper_2110_05722_b200.dist import DataParallel
+
+    class FakeEngine:
+        """train_step = the first step of a new bucket records its graph; every step
+        runs one all-reduce (the gradient exchange) like the real DP step."""
+        device = None
+
+        def __init__(self, task):
+            self.task, self._graphs, self.steps = task, {}, 0
+
+        def train_step(self, s):
+            key = ("train",) + tuple(np.asarray(self.task.batch(s).src).shape)
+            self._graphs.setdefault(key, True)
+            t = torch.ones(1)
+            dist.all_reduce(t)
+            assert t.item() == world
+            self.steps += 1
+
+    task = WmtShapedTask(4096, 64, 32000, seed=17 + rank)   # per-rank bucket sequences
+    eng = FakeEngine(task)
+    keys = [("train",) + tuple(sh) for sh in task.possible_shapes()]
+    n = bench.warm_up(eng, keys, 3, DataParallel())
+    out_q.put((rank, n, eng.steps, all(k in eng._graphs for k in keys)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_warm_up_stops_together_on_all_ranks():
+    """WMT-shaped data draws a different bucket sequence per rank; the bench's
+    warm-up must stop on the same step everywhere (a max over ranks), or the rank
+    that finished first leaves the others blocked in the gradient all-reduce."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_warm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, n0, s0, all0), (_, n1, s1, all1) = res
+    assert n0 == n1 == s0 == s1 and all0 and all1
