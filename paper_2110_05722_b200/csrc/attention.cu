@@ -123,10 +123,14 @@ __global__ void __launch_bounds__(32 * QT) attn_fwd_kernel(AttnArgs a) {
   __half* Ps = Vs + LK * kRow;             // [LQ][LK+8]
   const int bh = blockIdx.x, b = bh / a.H, h = bh % a.H;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // Q, K first (one cp.async group), V second: S = QK^T and the softmax run
+  // while V is still in flight
   load_tile(Qs, a.q + (int64_t)b * a.Lq * a.ldq + h * kHd, a.ldq, a.Lq, LQ);
   load_tile(Ks, a.k + (int64_t)b * a.Lk * a.ldk + h * kHd, a.ldk, a.Lk, LK);
+  asm volatile("cp.async.commit_group;\n" ::);
   load_tile(Vs, a.v + (int64_t)b * a.Lk * a.ldv + h * kHd, a.ldv, a.Lk, LK);
-  cp_async_wait_all();
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 1;\n" ::);
   __syncthreads();
 
   // S = Q K^T for rows [16w, 16w+16)
@@ -191,6 +195,8 @@ __global__ void __launch_bounds__(32 * QT) attn_fwd_kernel(AttnArgs a) {
     *reinterpret_cast<uint32_t*>(Ps + r0 * PLD + 8 * j + 2 * t) = p[j][0];
     *reinterpret_cast<uint32_t*>(Ps + r1 * PLD + 8 * j + 2 * t) = p[j][1];
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
   // O = P V (P fragments reused as A operands: C layout of two n-tiles == A layout)
   float o[8][4];
 #pragma unroll
@@ -317,12 +323,12 @@ __device__ __forceinline__ void store_rows(__half* gbase, int64_t ld, const __ha
 //            key warps:   dK = dS^T Q
 // so the dependent chain per CTA is two 32-MMA steps, not two 64-MMA steps.
 // issue the cp.async loads of one (batch, head) item: Q, K, V, dO tiles and P
+// (split: V, dO, P form one cp.async group and Q, K a second one, so phase A,
+// which needs only the first, can start while Q and K are still in flight)
 __device__ __forceinline__ void attn_bwd_issue(const AttnBwdArgs& a, int bh, __half* Qs, __half* Ks,
                                                __half* Vs, __half* Os, __half* Ps, int LQ, int LK,
-                                               int PLD) {
+                                               int PLD, bool split = false) {
   const int b = bh / a.H, h = bh % a.H;
-  load_tile(Qs, a.q + (int64_t)b * a.Lq * a.ldq + h * kHd, a.ldq, a.Lq, LQ);
-  load_tile(Ks, a.k + (int64_t)b * a.Lk * a.ldk + h * kHd, a.ldk, a.Lk, LK);
   load_tile(Vs, a.v + (int64_t)b * a.Lk * a.ldv + h * kHd, a.ldv, a.Lk, LK);
   load_tile(Os, a.dout + (int64_t)b * a.Lq * a.lddo + h * kHd, a.lddo, a.Lq, LQ);
   const __half* pg = a.probs + (int64_t)bh * a.Lq * a.Lk;
@@ -339,6 +345,9 @@ __device__ __forceinline__ void attn_bwd_issue(const AttnBwdArgs& a, int bh, __h
       Ps[r * PLD + c] = (r < a.Lq && c < a.Lk) ? pg[(int64_t)r * a.Lk + c] : __float2half(0.f);
     }
   }
+  if (split) asm volatile("cp.async.commit_group;\n" ::);
+  load_tile(Qs, a.q + (int64_t)b * a.Lq * a.ldq + h * kHd, a.ldq, a.Lq, LQ);
+  load_tile(Ks, a.k + (int64_t)b * a.Lk * a.ldk + h * kHd, a.ldk, a.Lk, LK);
   asm volatile("cp.async.commit_group;\n" ::);
 }
 
@@ -348,7 +357,7 @@ __device__ __forceinline__ void attn_bwd_issue(const AttnBwdArgs& a, int bh, __h
 //   phase B  query warps: dQ = dS K
 //            key warps:   dK = dS^T Q
 // so the dependent chain per item is two 32-MMA steps, not two 64-MMA steps.
-template <int QT, int KT>
+template <int QT, int KT, bool WAIT_QK = false>
 __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, const __half* Qs,
                                                  const __half* Ks, const __half* Vs,
                                                  const __half* Os, const __half* Ps, __half* Ss,
@@ -426,6 +435,7 @@ __device__ __forceinline__ void attn_bwd_compute(const AttnBwdArgs& a, int bh, c
     }
     if (a.csv) tile_colsum(dv, r0, a.Lk, cs + (2 * NW + tw) * 64, lane);
   }
+  if (WAIT_QK) asm volatile("cp.async.wait_group 0;\n" ::);   // Q, K (second group)
   __syncthreads();
   // ---- phase B ----
   if (qw && tw < QT) {
@@ -494,10 +504,10 @@ attn_bwd_kernel(AttnBwdArgs a) {
   __half* Ps = Os + LQ * kRow;        // [LQ][LK+8]
   __half* Ss = Ps + LQ * PLD;         // dS [LQ][LK+8]
   float* cs = reinterpret_cast<float*>(Ss + LQ * PLD);   // [3][NW][64] bias-grad tile sums
-  attn_bwd_issue(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD);
-  asm volatile("cp.async.wait_group 0;\n" ::);
+  attn_bwd_issue(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, LQ, LK, PLD, true);
+  asm volatile("cp.async.wait_group 1;\n" ::);        // V, dO, P
   __syncthreads();
-  attn_bwd_compute<QT, KT>(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, Ss, cs);
+  attn_bwd_compute<QT, KT, true>(a, blockIdx.x, Qs, Ks, Vs, Os, Ps, Ss, cs);
   if (a.csq || a.csk || a.csv) {
     __syncthreads();
     attn_bwd_colsum_store<QT, KT>(a, blockIdx.x, cs);
