@@ -627,3 +627,28 @@ def test_gemm_lt_bgrad_vs_torch(m, n, k):
     want_b = dy.double().sum(0)
     assert ((c - want_w).abs().max() / want_w.abs().max()).item() <= 1e-5
     assert ((bg.double() - want_b).abs().max() / want_b.abs().max()).item() <= 1e-6
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 512, 512), (4068, 1536, 512), (300, 256, 2048),
+                                   (4096, 2048, 512), (512, 32000 // 125 * 125 // 256 * 256, 512)])
+@pytest.mark.parametrize("variant", ["plain", "bias", "f32out", "bf16"])
+@pytest.mark.parametrize("split", [-2, -3], ids=["two_sm", "two_sm_persistent"])
+def test_gemm_tc_two_sm_vs_torch(m, n, k, variant, split):
+    """cta_group::2 kernels (split = -2 one tile per pair, -3 persistent pairs with
+    double-buffered TMEM): 256-row tiles over an SM pair, forward layout (K-major
+    A and B), against torch's fp32 product."""
+    from paper_2110_05722_b200 import _lib
+    torch.manual_seed(m + n + k)
+    dt = torch.bfloat16 if variant == "bf16" else torch.float16
+    odt = torch.float32 if variant == "f32out" else dt
+    A = (torch.randn(m, k, device="cuda") * 0.5).to(dt)
+    B = (torch.randn(n, k, device="cuda") * 0.5).to(dt)
+    bias = (torch.randn(n, device="cuda") * 2).to(odt) if variant == "bias" else None
+    c = torch.zeros(m, n, device="cuda", dtype=odt)
+    _lib.call("ls2_gemm_tc", 0, 1, m, n, k, 1.0, A.data_ptr(), k, B.data_ptr(), k, 0.0,
+              c.data_ptr(), n, _lib.ptr(bias), _lib.dtype_code(dt), _lib.dtype_code(odt), split,
+              _lib.stream_handle())
+    want = A.float() @ B.float().t() + (bias.float() if bias is not None else 0)
+    err = ((c.float() - want).abs().max() / want.abs().max()).item()
+    tol = 1e-5 if odt == torch.float32 else (8e-3 if dt == torch.bfloat16 else 1e-3)
+    assert err <= tol, err

@@ -2,6 +2,7 @@
 GEMM shapes: CUDA-graph timing of 20 back-to-back launches each, plus an
 error check against torch fp32.  Env LS2_TC_BN picks the tile width."""
 import json
+import os
 import sys
 
 import torch
@@ -38,9 +39,13 @@ def main():
         c2 = torch.zeros(m, n, device=dev, dtype=odt)
         lda, ldb = A.shape[1], B.shape[1]
 
+        split = int(os.environ.get("LS2_TC_SPLIT", "0"))
+        if split == -2 and (ta or not tb or n % 256):
+            continue
+
         def tc():
             _lib.call("ls2_gemm_tc", ta, tb, m, n, k, 1.0, A.data_ptr(), lda, B.data_ptr(), ldb, 0.0,
-                      c1.data_ptr(), n, None, 0, oc, 0, st())
+                      c1.data_ptr(), n, None, 0, oc, split, st())
 
         def lt():
             _lib.call("ls2_gemm_lt", h, ta, tb, m, n, k, 1.0, A.data_ptr(), lda, B.data_ptr(), ldb,
