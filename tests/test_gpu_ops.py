@@ -630,7 +630,8 @@ def test_gemm_lt_bgrad_vs_torch(m, n, k):
 
 
 @pytest.mark.parametrize("m,n,k", [(4096, 512, 512), (4068, 1536, 512), (300, 256, 2048),
-                                   (4096, 2048, 512), (512, 32000 // 125 * 125 // 256 * 256, 512)])
+                                   (4096, 2048, 512), (512, 32000 // 125 * 125 // 256 * 256, 512),
+                                   (1000, 384, 512)])
 @pytest.mark.parametrize("variant", ["plain", "bias", "f32out", "bf16"])
 @pytest.mark.parametrize("split", [-2, -3], ids=["two_sm", "two_sm_persistent"])
 def test_gemm_tc_two_sm_vs_torch(m, n, k, variant, split):
