@@ -653,3 +653,31 @@ def test_gemm_tc_two_sm_vs_torch(m, n, k, variant, split):
     err = ((c.float() - want).abs().max() / want.abs().max()).item()
     tol = 1e-5 if odt == torch.float32 else (8e-3 if dt == torch.bfloat16 else 1e-3)
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k", [(0, 0, 4096, 512, 512), (0, 0, 4068, 512, 2048),
+                                         (0, 0, 1000, 512, 32000), (1, 0, 512, 512, 4096),
+                                         (1, 0, 1536, 512, 4068), (1, 0, 2048, 2048, 1024),
+                                         (1, 1, 512, 256, 512)])
+@pytest.mark.parametrize("variant", ["plain", "bias", "f32out", "bf16"])
+def test_gemm_tc_two_sm_persistent_all_majors(ta, tb, m, n, k, variant):
+    """Persistent cta_group::2 kernel (split = -3) with MN-major operands (data and
+    weight gradient layouts) against torch's fp32 product."""
+    from paper_2110_05722_b200 import _lib
+    torch.manual_seed(m + n + k + ta + 2 * tb)
+    dt = torch.bfloat16 if variant == "bf16" else torch.float16
+    odt = torch.float32 if variant == "f32out" else dt
+    A = ((torch.randn(k, m, device="cuda") if ta else torch.randn(m, k, device="cuda")) * 0.5).to(dt)
+    B = ((torch.randn(n, k, device="cuda") if tb else torch.randn(k, n, device="cuda")) * 0.5).to(dt)
+    bias = (torch.randn(n, device="cuda") * 2).to(odt) if variant == "bias" else None
+    c = torch.zeros(m, n, device="cuda", dtype=odt)
+    _lib.call("ls2_gemm_tc", ta, tb, m, n, k, 1.0, A.data_ptr(), A.shape[1], B.data_ptr(),
+              B.shape[1], 0.0, c.data_ptr(), n, _lib.ptr(bias), _lib.dtype_code(dt),
+              _lib.dtype_code(odt), -3, _lib.stream_handle())
+    opA = A.float().t() if ta else A.float()
+    opB = B.float().t() if tb else B.float()
+    want = opA @ opB + (bias.float() if bias is not None else 0)
+    err = ((c.float() - want).abs().max() / want.abs().max()).item()
+    tol = (6e-5 if k > 8192 else 1e-5) if odt == torch.float32 else \
+        (8e-3 if dt == torch.bfloat16 else 1e-3)
+    assert err <= tol, err
