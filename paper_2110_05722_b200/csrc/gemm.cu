@@ -309,11 +309,21 @@ static int lt_matmul(Blas* bl, int trans_a, int trans_b, int64_t m, int64_t n, i
                      cudaStream_t st, int bmode = -1) {
   if (bmode < 0) bmode = bias ? 1 : 0;
   if (m <= 0 || n <= 0) return LS2_OK;
-  if (bmode <= 1 && tc_route(trans_a, trans_b) &&
+  // LS2_TC_MIN_MACS: route only products of at least this many MACs;
+  // LS2_TC_2SM=1: use the persistent two-SM kernel for the routed ones
+  static const double tc_min_macs = [] {
+    const char* e = std::getenv("LS2_TC_MIN_MACS");
+    return e ? std::atof(e) : 0.0;
+  }();
+  static const bool tc_2sm = [] {
+    const char* e = std::getenv("LS2_TC_2SM");
+    return e && e[0] == '1';
+  }();
+  if (bmode <= 1 && tc_route(trans_a, trans_b) && (double)m * n * k >= tc_min_macs &&
       ls2_gemm_tc_supported(trans_a, trans_b, m, n, k, A, lda, B, ldb, beta, C, ldc, tab, tc) &&
-      (!bias || aligned16(bias)))
+      (!bias || aligned16(bias)) && (!tc_2sm || n % 128 == 0))
     return ls2_gemm_tc(trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, bias, tab,
-                       tc, 0, st);
+                       tc, tc_2sm ? -3 : 0, st);
   if (!bl || !bl->lt) return fail(LS2_ERR_CUBLAS, "gemm_lt: no cublasLt handle");
   if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_CUBLAS, "gemm_lt: f64 not routed to Lt");
   const int al = std::min(std::min(align_of(A), align_of(B)), std::min(align_of(C),
