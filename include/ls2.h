@@ -269,7 +269,10 @@ int64_t ls2_gemm_scratch_bytes(int64_t n1, int64_t n2);
  * convention of ls2_gemm_lt: C[m x n] = alpha*op(A)@op(B) (+ bias[n]) (+ C when beta = 1),
  * A/B fp16 or bf16, C the same type or f32, fp32 accumulation in tensor memory.
  * split = 0 picks the cluster split-K factor (1/2/4/8; small-output, long-K products
- * reduce the partial tiles through DSMEM in rank order, deterministic).
+ * reduce the partial tiles through DSMEM in rank order, deterministic); split = -1 the
+ * persistent one-SM kernel (double-buffered TMEM accumulator); -2 / -3 the cta_group::2
+ * kernels over SM pairs (256-row tiles; -2 one tile per pair, K-major A and B only;
+ * -3 persistent with a TMA-store epilogue, every operand layout, n % 128 == 0).
  * ls2_gemm_tc_supported: 1 when the shape/dtype/alignment is covered (n a multiple of 128,
  * 16-byte aligned operands, ld multiples of 8; m and k arbitrary). */
 int ls2_gemm_tc_supported(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
