@@ -633,12 +633,14 @@ def test_gemm_lt_bgrad_vs_torch(m, n, k):
                                    (4096, 2048, 512), (512, 32000 // 125 * 125 // 256 * 256, 512),
                                    (1000, 384, 512)])
 @pytest.mark.parametrize("variant", ["plain", "bias", "f32out", "bf16"])
-@pytest.mark.parametrize("split", [-2, -3], ids=["two_sm", "two_sm_persistent"])
+@pytest.mark.parametrize("split", [-2, -3, -4], ids=["two_sm", "two_sm_persistent", "two_pair_mc"])
 def test_gemm_tc_two_sm_vs_torch(m, n, k, variant, split):
     """cta_group::2 kernels (split = -2 one tile per pair, -3 persistent pairs with
     double-buffered TMEM): 256-row tiles over an SM pair, forward layout (K-major
     A and B), against torch's fp32 product."""
     from paper_2110_05722_b200 import _lib
+    if split == -4 and n % 256:
+        pytest.skip("the two-pair multicast kernel takes n % 256 == 0")
     torch.manual_seed(m + n + k)
     dt = torch.bfloat16 if variant == "bf16" else torch.float16
     odt = torch.float32 if variant == "f32out" else dt
