@@ -135,8 +135,13 @@ class ClockSampler:
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 
-def oracle_sample_setup(sample_seqs: int):
+def oracle_sample_setup(sample_seqs: int, wmt: bool = False):
+    """A bounded CPU sample of the T-base step: `sample_seqs` x 64 tokens per step
+    (fixed 64-token sequences, or, with wmt, the leading sequences of that step's
+    WMT-shaped batch up to the same token budget) plus narrow + Adam on the
+    matching fraction of the workspace."""
     from oracle import lsport as O
+    from paper_2110_05722_b200.data import WmtShapedTask
     shapes = O.model_param_shapes(6, 6, 512, 2048, V, 256)
     P = {k: O.to_half(v) for k, v in O.model_init(shapes, 0).items()}
     n = sum(int(np.prod(s)) for _, s in shapes)
@@ -149,14 +154,24 @@ def oracle_sample_setup(sample_seqs: int):
     st = dict(O=O, shapes=shapes, P=P, model=O.OracleTransformer(6, 6, 512, 8, 2048, V, 256),
               batch=(src, tin, tgt, np.full(sample_seqs, L)), n_s=n_s,
               p16=np.concatenate([P[k].reshape(-1) for k, _ in shapes])[:n_s].copy(),
-              m=np.zeros(n_s, np.float32), v=np.zeros(n_s, np.float32), tokens=sample_seqs * L)
+              m=np.zeros(n_s, np.float32), v=np.zeros(n_s, np.float32), tokens=sample_seqs * L,
+              budget=sample_seqs * L, wmt=WmtShapedTask(B * L, L, V, seed=17) if wmt else None,
+              counted=0)
     return st
 
 
 def oracle_sample_step(st, step: int):
-    """fwd+bwd on the sample batch + narrow + Adam on the matching workspace slice."""
+    """fwd+bwd on the sample batch + narrow + Adam on the matching workspace slice;
+    adds the step's non-pad target tokens to st["counted"]."""
     O = st["O"]
-    src, tin, tgt, lens = st["batch"]
+    if st["wmt"] is not None:
+        bt = st["wmt"].batch(step)
+        lb = np.asarray(bt.src).shape[1]
+        k = max(1, st["budget"] // lb)
+        src, tin, tgt = (np.asarray(a)[:k] for a in (bt.src, bt.tgt_in, bt.tgt_out))
+        lens = np.asarray(bt.src_len)[:k]
+    else:
+        src, tin, tgt, lens = st["batch"]
     loss, cnt, _, G = st["model"].forward_backward(st["P"], src, tin, tgt, lens, pad_id=0, p=0.1,
                                                    alpha=0.1, seed=0, step=step)
     acc = np.concatenate([np.asarray(G[k], np.float32).reshape(-1) for k, _ in st["shapes"]])
@@ -164,6 +179,7 @@ def oracle_sample_step(st, step: int):
     g16 = O.to_half(acc)
     O.adam_flat(st["p16"], g16, st["m"], st["v"], lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
                 wd=0.0, loss_scale=1.0, t=step + 1)
+    st["counted"] += int(cnt)
     return loss / cnt
 
 
@@ -175,22 +191,27 @@ def run_reference(args):
     # the whole --steps/--warmup run near 2.5 minutes (~0.27 s per sequence on
     # 16 host cores), between 1 and 8 (numpy/OpenBLAS run bigger batches better)
     seqs = max(1, min(8, int(150.0 / (0.27 * (args.steps + args.warmup)))))
-    st = oracle_sample_setup(seqs)
+    wmt = args.data == "wmt"            # the same batch shapes as our arm's default
+    st = oracle_sample_setup(seqs, wmt=wmt)
     for s in range(args.warmup):
         oracle_sample_step(st, s)
+    st["counted"] = 0
     t0 = time.perf_counter()
     for s in range(args.steps):
         oracle_sample_step(st, args.warmup + s)
     dt = time.perf_counter() - t0
-    tps = st["tokens"] * args.steps / dt
+    tps = st["counted"] / dt
     cores = os.cpu_count() or 1
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp16 workspace / f32 compute", "data": "synthetic",
-            "config": {"workload": "Transformer-base 6e6d V32k, 4096 tok/GPU step (sampled)",
-                       "sample": f"{seqs} x {L} tokens fwd+bwd + Adam on {seqs}/{B} of the "
-                                 f"60.66M-param workspace (= 1/{B // seqs} of a step)"},
+            "config": {"workload": "Transformer-base 6e6d V32k, 4096 tok/GPU step (sampled)"
+                                   + (", synthetic WMT-shaped batches" if wmt else ""),
+                       "sample": f"{'up to ' if wmt else ''}{seqs * L} tokens fwd+bwd per step "
+                                 f"({'leading sequences of the step WMT-shaped batch' if wmt else f'{seqs} x {L}'}) "
+                                 f"+ Adam on {seqs}/{B} of the 60.66M-param workspace; "
+                                 "non-pad target tokens counted"},
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"{seqs}x{L} tokens fwd+bwd + Adam on 1/{B // seqs} of the "
                                        f"workspace per step, {args.steps} steps"},
@@ -200,18 +221,21 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline():
-    st = oracle_sample_setup(8)
+def cpu_baseline(wmt: bool = False):
+    st = oracle_sample_setup(8, wmt=wmt)
     oracle_sample_step(st, 0)
+    st["counted"] = 0
     t0 = time.perf_counter()
     n = 2
     for s in range(n):
         oracle_sample_step(st, 1 + s)
     dt = time.perf_counter() - t0
-    return {"value": st["tokens"] * n / dt, "unit": "tokens/s", "cores": os.cpu_count() or 1,
+    what = "up to 512 tokens of each step's WMT-shaped batch" if wmt else "8x64 tokens"
+    return {"value": st["counted"] / dt, "unit": "tokens/s", "cores": os.cpu_count() or 1,
             "kind": "port",
-            "sample": f"oracle/lsport.py: 8x64 tokens fwd+bwd + narrow + Adam on 1/8 of the "
-                      f"workspace per step, 1 warm-up + {n} timed steps (numpy/OpenBLAS)"}
+            "sample": f"oracle/lsport.py: {what} fwd+bwd + narrow + Adam on 1/8 of the "
+                      f"workspace per step, 1 warm-up + {n} timed steps (numpy/OpenBLAS); "
+                      "non-pad target tokens counted"}
 
 
 # ---------------------------------------------------------------------------
@@ -392,7 +416,7 @@ def run_ours(args):
                              "traffic": traffic, "launch_ms": adam_ms},
                 }
         if world == 1 and not args.no_cpu_baseline and args.model == "tbase":
-            line["cpu_baseline"] = cpu_baseline()
+            line["cpu_baseline"] = cpu_baseline(wmt)
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()
