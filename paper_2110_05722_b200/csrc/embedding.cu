@@ -172,11 +172,11 @@ __global__ void emb_bwd_pos(const Tin* __restrict__ dy, const uint8_t* __restric
 // grid (len, S): a cluster of S CTAs splits one position's batch sum (short
 // buckets have few positions: L = 8 -> 8 x 8 CTAs instead of 8); rank 0 folds
 // the S partials through DSMEM in rank order (deterministic).
-template <typename Tin, typename Tg, bool DROP>
-__global__ void __launch_bounds__(256) emb_bwd_pos_vec(
+template <typename Tin, typename Tg, bool DROP, int NT>
+__global__ void __launch_bounds__(NT) emb_bwd_pos_vec(
     const Tin* __restrict__ dy, const uint8_t* __restrict__ bits, Tg* __restrict__ dP,
     int64_t batch_all, int64_t len, int64_t max_len, int64_t d, Tg ds, int beta) {
-  __shared__ Tg part[256 * 8];
+  __shared__ Tg part[NT * 8];
   __shared__ __align__(16) Tg fin[256 * 8];
   const int64_t l = blockIdx.x;
   const int S = (int)gridDim.y, q = (int)blockIdx.y;
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) emb_bwd_pos_vec(
   dy += bq0 * len * d;
   if (DROP) bits += (bq0 * len * d) >> 3;
   const int cgs = (int)(d / 8);
-  const int ngrp = 256 / cgs;                  // batch groups
+  const int ngrp = NT / cgs;                   // batch groups
   const int cg = threadIdx.x % cgs, grp = threadIdx.x / cgs;
   Tg* out = dP + l * d + cg * 8;
   if (!beta && grp == 0 && q == 0) {          // grid.x = len: CTA l also clears l + k*len >= len
@@ -365,11 +365,15 @@ int ls2_embedding_bwd(const void* dy, const int64_t* tokens, const uint8_t* keep
         at[0].val.clusterDim.y = S;
         at[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3((unsigned)len, (unsigned)S);
-        cfg.blockDim = dim3(256);
+        // one CTA per position (S = 1): 512 threads = twice the batch rows in flight
+        cfg.blockDim = dim3(S == 1 ? 512 : 256);
         cfg.stream = st;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        auto kern = use_drop ? emb_bwd_pos_vec<Tin, Tg, true> : emb_bwd_pos_vec<Tin, Tg, false>;
+        auto kern = S == 1 ? (use_drop ? emb_bwd_pos_vec<Tin, Tg, true, 512>
+                                       : emb_bwd_pos_vec<Tin, Tg, false, 512>)
+                           : (use_drop ? emb_bwd_pos_vec<Tin, Tg, true, 256>
+                                       : emb_bwd_pos_vec<Tin, Tg, false, 256>);
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (const Tin*)dy, keep_bits, (Tg*)dP, batch,
                                            len, max_len, d, ds, beta_pos);
         if (e != cudaSuccess) return fail(LS2_ERR_CUDA, std::string("embedding_bwd_pos: ") + cudaGetErrorString(e));
