@@ -463,6 +463,8 @@ class OracleTransformer:
         self.vocab, self.max_len, self.eps = vocab, max_len, eps
         self.learned, self.tied = learned, tied
         self.scale = math.sqrt(d) if scale is None else scale
+        self.relu_inject = None          # test hook, see _relu_site
+        self.relu_flips = {}
 
     # -- attention core -------------------------------------------------------
     def _split(self, x):
@@ -504,6 +506,29 @@ class OracleTransformer:
         return dy.reshape(-1, dy.shape[-1]).astype(np.float64).sum(axis=0).astype(t)
 
     # -- layers ---------------------------------------------------------------
+    def _relu_site(self, pre, x, bias, keep, p):
+        """bias_relu_dropout_fwd, optionally with injected ReLU decisions.
+
+        relu_inject[pre] (bool [B, L, F]) replaces the oracle's own (a > 0) test,
+        keeping F/kernels.py:385-403's op order for everything else; relu_flips[pre]
+        records where the injected decisions differ from the oracle's own and how
+        far from 0 those pre-activations were (relative to the site's RMS)."""
+        inj = self.relu_inject.get(pre) if self.relu_inject else None
+        if inj is None:
+            return bias_relu_dropout_fwd(x, bias, keep, p)
+        t = ctype(x, bias)
+        a = cast(x, t) + cast(bias, t)
+        own = a > 0
+        diff = own != inj
+        rms = float(np.sqrt(np.mean(np.square(a, dtype=np.float64))))
+        self.relu_flips[pre] = (int(diff.sum()), int(diff.size),
+                                float(np.abs(a[diff]).max() / rms) if diff.any() else 0.0)
+        relu = inj.astype(t)
+        y = a * relu
+        if p > 0.0:
+            y = (y * cast(keep, t)) * t(1.0 / (1.0 - p))
+        return y, relu
+
     def _tail_fwd(self, x, wn, bn, res, p, seed, t):
         keep = dropout_keep(x.shape, p, seed, t)
         return bias_dropout_residual_fwd(x, bn, res, keep, p).astype(t), keep
@@ -519,7 +544,7 @@ class OracleTransformer:
                                         P[pre + "attn.bo"], x, p, fold_seed(seed, site, 0), t)
         u2, c["mu2"], c["sg2"] = layernorm_fwd(y1, P[pre + "ln2.w"], P[pre + "ln2.b"], self.eps)
         keep2 = dropout_keep(u2.shape[:-1] + (self.dff,), p, fold_seed(seed, site, 1), t)
-        z, relu = bias_relu_dropout_fwd(self._lin(u2, P[pre + "ffn.w1"]), P[pre + "ffn.b1"], keep2, p)
+        z, relu = self._relu_site(pre, self._lin(u2, P[pre + "ffn.w1"]), P[pre + "ffn.b1"], keep2, p)
         y2, c["keep3"] = self._tail_fwd(self._lin(z.astype(t), P[pre + "ffn.w2"]), None,
                                         P[pre + "ffn.b2"], y1, p, fold_seed(seed, site, 2), t)
         c.update(u1=u1, qkv=qkv, ctxm=ctxm, y1=y1, u2=u2, keep2=keep2, relu=relu, z=z)
@@ -579,7 +604,7 @@ class OracleTransformer:
                                         P[pre + "cross.bo"], y1, p, fold_seed(seed, site, 1), t)
         u3, c["mu3"], c["sg3"] = layernorm_fwd(y2, P[pre + "ln3.w"], P[pre + "ln3.b"], self.eps)
         keep2 = dropout_keep(u3.shape[:-1] + (self.dff,), p, fold_seed(seed, site, 2), t)
-        z, relu = bias_relu_dropout_fwd(self._lin(u3, P[pre + "ffn.w1"]), P[pre + "ffn.b1"], keep2, p)
+        z, relu = self._relu_site(pre, self._lin(u3, P[pre + "ffn.w1"]), P[pre + "ffn.b1"], keep2, p)
         y3, c["keep3"] = self._tail_fwd(self._lin(z.astype(t), P[pre + "ffn.w2"]), None,
                                         P[pre + "ffn.b2"], y2, p, fold_seed(seed, site, 3), t)
         c.update(u1=u1, qkv=qkv, ctxm=ctxm, y1=y1, u2=u2, qc=qc, ctxm_x=ctxm_x, y2=y2,

@@ -910,6 +910,17 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     return y1, u2
 
 
+# Test hook: when a dict, every FFN forward stores a copy of its ReLU bit mask
+# (byte i>>3, bit i&7 of the flat [B, L, F] index) under its stash prefix, so a
+# parity test can hand the GPU's ReLU decisions to the oracle (a pre-activation
+# within rounding of 0 may fall on either side; see tests/test_gpu_headline.py).
+RELU_TAP: dict | None = None
+# Test hook: when a dict, the decoder backward stores copies of the gradient
+# entering each decoder layer ("ddec", "dg5", ..., "dg0" = the layer's output
+# gradient) and of each cross-attention query gradient ("dqc:dec{i}.").
+GRAD_TAP: dict | None = None
+
+
 def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p, next_ln=None):
     """FFN sublayer on the already-normalized input u = LN(y_in).
 
@@ -931,6 +942,10 @@ def _ffn_fwd(y_in, u, w, p_drop, seed, site, k_relu, k_tail, arena, stash, p, ne
                         mask=None if banked is None else
                         DropoutMask(p=p_drop, bits=keep_r, shape=(b, l, dff)))
     arena.free(a1)
+    if RELU_TAP is not None:
+        # under graph capture the copy lands in the graph's pool and is
+        # refreshed by every replay
+        RELU_TAP[("graph:" if torch.cuda.is_current_stream_capturing() else "") + p] = relum.clone()
     stash.push(p + "keepr", keep_r); stash.push(p + "relum", relum); stash.push(p + "z", z)
     f = arena.alloc((b, l, d), dt)
     _linear(z.view(r, dff), w.w2, None, f.view(r, d))
@@ -1276,6 +1291,8 @@ def decoder_layer_backward(dy, w: DecoderLayerWeights, kv, stash: ActivationStas
         K.gemm(dscores_x, _heads(qc, n_heads), trans_a=True, out=_heads(dk_i, n_heads))
         K.gemm(probs_x, dctx_x, trans_a=True, out=_heads(dv_i, n_heads))
         arena.free(dscores_x); arena.free(probs_x); arena.free(dctxm_x); arena.free(qc)
+    if GRAD_TAP is not None:
+        GRAD_TAP["dqc:" + p] = dqc.clone()
     du2 = arena.alloc((b, l, d), dt)
     K.gemm(dqc.view(r, d), _as_dt(w.cross_wq, dt), out=du2.view(r, d))
     _wgrad(sink, pp + "cross.wq", dqc.view(r, d), u2.view(r, d))
@@ -1649,6 +1666,9 @@ class Transformer:
                                None, stash, (f"dec{nd - 1}.", f"dec{nd - 1}."), p_drop, arena)
         else:
             _ln_bwd(sink, "", "dec_ln", ddec, g_in, params["dec_ln.w"], mu_d, sg_d, dg, None)
+        if GRAD_TAP is not None:
+            GRAD_TAP["ddec"] = ddec.clone()
+            GRAD_TAP[f"dg{cfg.n_dec}"] = dg.clone()
         arena.free(ddec); arena.free(mu_d); arena.free(sg_d); arena.free(g_in)
         _ready(sink, "dec_ln.", "out_proj.")
 
@@ -1672,6 +1692,8 @@ class Transformer:
                 dg, dks[i], dvs[i], df = res
             else:
                 (dg, dks[i], dvs[i]), df = res, None
+            if GRAD_TAP is not None:
+                GRAD_TAP[f"dg{i}"] = dg.clone()
             join()
             _ready(sink, f"dec{i}.")
             emit(("dec_layer_backward_done", i))
