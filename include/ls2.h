@@ -178,6 +178,30 @@ int ls2_attention_bwd_bias(const void* q, int64_t ldq, const void* k, int64_t ld
                            double scale, double* csq, int64_t ldcsq, double* csk, int64_t ldcsk,
                            double* csv, int64_t ldcsv, void* stream);
 
+/* ---- fused attention on tcgen05/TMEM/TMA (fp16, head dim 64, Lq/Lk <= 64) ----
+ * Same operation and operand addressing as ls2_attention_fwd / _bwd_bias (F/model.py:
+ * 362-376, 482-495; F/kernels.py:277-307; F/gradients.py:77-100), but the forward
+ * keeps only per-row softmax statistics instead of the [B, H, Lq, Lk]
+ * probabilities: stats = float2[B*H*Lq] (row max of the scaled masked scores,
+ * 1 / row sum); the backward recomputes P from Q, K and the stats (bit-identical
+ * to the forward's P) and therefore needs the same mask.  Operand pointers and
+ * row pitches must be 16-byte aligned.  LS2_ATTN_TC=0 disables (supported -> 0). */
+int ls2_attention_tc_supported(int64_t lq, int64_t lk, int64_t hd, int dtype);
+/* debugging aid: per-CTA phase timestamps (globaltimer ns, u64[grid][8]) of the
+ * following attention_tc launches are written to buf (NULL turns it off) */
+int ls2_attention_tc_trace(void* buf);
+int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                         int64_t ldv, void* stats, void* o, int64_t ldo, int64_t batch,
+                         int64_t heads, int64_t lq, int64_t lk, int64_t hd, int mask_kind,
+                         const int64_t* lens, double scale, void* stream);
+int ls2_attention_tc_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                         int64_t ldv, const void* stats, const void* dout, int64_t lddo, void* dq,
+                         int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                         int64_t batch, int64_t heads, int64_t lq, int64_t lk, int64_t hd,
+                         int mask_kind, const int64_t* lens, double scale, double* csq,
+                         int64_t ldcsq, double* csk, int64_t ldcsk, double* csv, int64_t ldcsv,
+                         void* stream);
+
 /* ---- label-smoothed CE: F/kernels.py:338-360, F/gradients.py:47-74 ----
  * row_stats (double[rows*2]) receives per-row (loss, correct) partials;
  * out3 (double[3]) = (loss_sum, token_count, correct) after the fixed-order reduce. */
@@ -218,8 +242,10 @@ int ls2_embedding_bwd(const void* dy, const int64_t* tokens, const uint8_t* keep
 /* ---- workspace trainer: F/trainer.py:125-181, F/engine.py:152-157 ----
  * hyper: f32 constants precomputed on the host exactly as numpy does:
  *   [lr, beta1, 1-beta1, beta2, 1-beta2, eps, wd, loss_scale]
- * bc: (f32(1-beta1^t), f32(1-beta2^t)) table indexed by t; the step t is
- *   either `t_host` (>0) or read as *applied + 1 from the device counter.
+ * bc: (f32(1-beta1^t), f32(1-beta2^t)) table of bc_len rows indexed by t,
+ *   followed by beta1, beta2 as two f64 values; for t >= bc_len the kernel
+ *   forms f32(1 - beta^t) itself in f64.  The step t is either `t_host` (>0)
+ *   or read as *applied + 1 from the device counter.
  * skip: the update is skipped when *nonfinite != 0 or (loss && !isfinite(*loss)). */
 int ls2_adam(uint16_t* p16, const uint16_t* g16, float* m, float* v, int64_t n,
              const float* hyper, const float* bc_table, int64_t bc_len, int64_t t_host,

@@ -63,6 +63,11 @@ _SIGS = {
     "ls2_attention_bwd": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, D, P],
     "ls2_attention_bwd_bias": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, D,
                                P, L, P, L, P, L, P],
+    "ls2_attention_tc_supported": [L, L, L, I],
+    "ls2_attention_tc_trace": [P],
+    "ls2_attention_tc_fwd": [P, L, P, L, P, L, P, P, L, L, L, L, L, L, I, P, D, P],
+    "ls2_attention_tc_bwd": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, I, P, D,
+                             P, L, P, L, P, L, P],
     "ls2_embedding_fwd": [P, P, P, P, P, P, L, L, L, L, D, I, I, U, P, U, D, I, I, P],
     "ls2_embedding_bwd": [P, P, P, P, P, I, I, L, L, L, L, D, I, D, I, P],
     "ls2_adam": [P, P, P, P, L, P, P, L, L, P, P, P, P],
@@ -93,7 +98,8 @@ _SIGS = {
 }
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,
              "ls2_colsum_ws_bytes": L, "ls2_layernorm_bwd_ws_bytes": L,
-             "ls2_attention_supported": ctypes.c_int, "ls2_colsum_nblk": ctypes.c_int,
+             "ls2_attention_supported": ctypes.c_int,
+             "ls2_attention_tc_supported": ctypes.c_int, "ls2_colsum_nblk": ctypes.c_int,
              "ls2_layernorm_bwd_nblk": ctypes.c_int, "ls2_wgrad_tc_split": ctypes.c_int,
              "ls2_gemm_tc_supported": ctypes.c_int,
              "ls2_gemm_scratch_bytes": L}

@@ -7,9 +7,18 @@ of the fused projection buffers directly:
   cross-attention Q = qc (stride d); K_i/V_i = kv_buf slices (stride 2*n_dec*d)
 
 so the contractions, the masked softmax and the head split/merge are one
-kernel forward and one kernel backward.  Shapes it does not cover (non-fp16,
-head dim != 64, L > 128, dense masks) use the reference-shaped cuBLAS +
-softmax-kernel path in model.py.  LS2_FUSED_ATTENTION=0 disables it.
+kernel forward and one kernel backward.  Two kernel families sit behind it:
+
+  * L <= 64 (every T-base / WMT bucket): the tcgen05/TMEM/TMA kernels of
+    csrc/attention_tc.cu.  The forward saves per-row softmax statistics
+    (float32 [B, H, Lq, 2]) instead of the probabilities and the backward
+    recomputes P from them, so the saved state is `alloc_state`'s f32 tensor;
+  * 64 < L <= 128: the mma.sync kernels of csrc/attention.cu, which save the
+    fp16 probabilities [B, H, Lq, Lk].
+
+Shapes neither covers (non-fp16, head dim != 64, L > 128, dense masks) use the
+reference-shaped cuBLAS + softmax-kernel path in model.py.
+LS2_FUSED_ATTENTION=0 disables both, LS2_ATTN_TC=0 only the tcgen05 family.
 """
 
 from __future__ import annotations
@@ -34,6 +43,24 @@ def fused_ok(dtype, lq: int, lk: int, hd: int, mask) -> bool:
     return bool(_lib._lib.ls2_attention_supported(lq, lk, hd, _lib.F16))
 
 
+def tc_ok(dtype, lq: int, lk: int, hd: int, mask) -> bool:
+    """The tcgen05 family takes this shape (implies fused_ok)."""
+    if not fused_ok(dtype, lq, lk, hd, mask):
+        return False
+    if mask is not None and mask.kind == "causal" and lq != lk:
+        return False
+    return bool(_lib._lib.ls2_attention_tc_supported(lq, lk, hd, _lib.F16))
+
+
+def alloc_state(arena, dtype, batch, heads, lq, lk, hd, mask):
+    """The forward's saved softmax state for the fused kernels: f32 row
+    statistics [B, H, Lq, 2] (tcgen05 family) or fp16 probabilities
+    [B, H, Lq, Lk] (mma.sync family)."""
+    if tc_ok(dtype, lq, lk, hd, mask):
+        return arena.alloc((batch, heads, lq, 2), torch.float32)
+    return arena.alloc((batch, heads, lq, lk), dtype)
+
+
 def _mask_args(mask):
     if mask is None or mask.kind == "none":
         return _lib.MASK_NONE, None
@@ -43,7 +70,16 @@ def _mask_args(mask):
 
 
 def forward(q, ldq, k, ldk, v, ldv, probs, o, ldo, batch, heads, lq, lk, hd, mask, scale):
+    """probs: the state from alloc_state (f32 statistics or fp16 probabilities)."""
     kind, lens = _mask_args(mask)
+    if probs.dtype == torch.float32:
+        # the backward recomputes P, so it needs the same mask: keep it (and the
+        # device lens it reads) on the saved state
+        probs._ls2_amask = (kind, lens)
+        _lib.call("ls2_attention_tc_fwd", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(),
+                  ldv, probs.data_ptr(), o.data_ptr(), ldo, batch, heads, lq, lk, hd, kind,
+                  _lib.ptr(lens), float(scale), _lib.stream_handle())
+        return
     _lib.call("ls2_attention_fwd", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(), ldv,
               probs.data_ptr(), o.data_ptr(), ldo, batch, heads, lq, lk, hd, kind,
               _lib.ptr(lens), float(scale), _lib.stream_handle())
@@ -60,6 +96,13 @@ def backward(q, ldq, k, ldk, v, ldv, probs, dout, lddo, dq, lddq, dk, lddk, dv, 
         else:
             buf, col0, ld = c
             cs += [buf.data_ptr() + 8 * col0, ld]
+    if probs.dtype == torch.float32:
+        kind, lens = probs._ls2_amask
+        _lib.call("ls2_attention_tc_bwd", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(),
+                  ldv, probs.data_ptr(), dout.data_ptr(), lddo, dq.data_ptr(), lddq,
+                  dk.data_ptr(), lddk, dv.data_ptr(), lddv, batch, heads, lq, lk, hd, kind,
+                  _lib.ptr(lens), float(scale), *cs, _lib.stream_handle())
+        return
     _lib.call("ls2_attention_bwd_bias", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(), ldv,
               probs.data_ptr(), dout.data_ptr(), lddo, dq.data_ptr(), lddq, dk.data_ptr(), lddk,
               dv.data_ptr(), lddv, batch, heads, lq, lk, hd, float(scale), *cs,

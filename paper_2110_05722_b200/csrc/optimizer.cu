@@ -42,10 +42,18 @@ __global__ void adam_kernel(uint16_t* __restrict__ p16, const uint16_t* __restri
                             int64_t bc_len, int64_t t_host, const int64_t* __restrict__ applied,
                             const int* nonfinite, const double* loss, bool vec) {
   if (skip_step(nonfinite, loss)) return;
-  int64_t t = t_host > 0 ? t_host : (*applied + 1);
-  if (t >= bc_len) t = bc_len - 1;
+  const int64_t t = t_host > 0 ? t_host : (*applied + 1);
+  float bc1, bc2;
+  if (t < bc_len) {
+    bc1 = bc[2 * t];
+    bc2 = bc[2 * t + 1];
+  } else {   // past the table: f32(1 - beta**t) in f64, the betas stored after it
+    const double* betas = reinterpret_cast<const double*>(bc + 2 * bc_len);
+    bc1 = __double2float_rn(1.0 - pow(betas[0], (double)t));
+    bc2 = __double2float_rn(1.0 - pow(betas[1], (double)t));
+  }
   AdamK k{hyper[0], hyper[1], hyper[2], hyper[3], hyper[4], hyper[5], hyper[6], hyper[7],
-          bc[2 * t], bc[2 * t + 1], hyper[7] != 1.0f};
+          bc1, bc2, hyper[7] != 1.0f};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (vec) {
     const int64_t groups = n / 8;

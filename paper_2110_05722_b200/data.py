@@ -27,82 +27,95 @@ def _uniform(seed: int, n: int) -> np.ndarray:
 
 
 def bucket_len(m: int, max_len: int) -> int:
-    padded = -(-m // LEN_BUCKET) * LEN_BUCKET
-    return padded if padded <= max_len else max(m, min(padded, max_len))
+    """Padded length of a batch whose longest sequence is m (F/data.py:46-48):
+    the next multiple of LEN_BUCKET while that fits max_len, otherwise
+    max_len itself (or m, for an over-long sequence)."""
+    up = LEN_BUCKET * ((m + LEN_BUCKET - 1) // LEN_BUCKET)
+    return up if up <= max_len else max(m, max_len)
 
 
 def bos_id(pad_id: int, vocab: int) -> int:
+    """Beginning-of-sequence id: the id after pad, wrapping at vocab."""
     return (pad_id + 1) % vocab
 
 
 def payload_range(pad_id: int, vocab: int) -> list:
-    reserved = {pad_id, bos_id(pad_id, vocab)}
-    return [t for t in range(vocab) if t not in reserved]
+    """Ids a synthetic sequence may contain: all but pad and bos, ascending."""
+    ids = np.arange(vocab)
+    keep = (ids != pad_id) & (ids != bos_id(pad_id, vocab))
+    return ids[keep].tolist()
+
+
+def _parse_line(path: str, lineno: int, text: str, vocab: int):
+    toks = text.split()
+    if not toks:
+        return None
+    try:
+        ids = list(map(int, toks))
+    except ValueError:
+        raise ParseError(f"{path}:{lineno}: non-integer token") from None
+    lo, hi = min(ids), max(ids)
+    if lo < 0:
+        raise ParseError(f"{path}:{lineno}: negative token id")
+    if hi >= vocab:
+        raise TokenOutOfRange(f"{path}:{lineno}: token id >= vocab ({vocab})")
+    return ids
 
 
 def load_token_file(path: str, vocab: int) -> list:
+    """Sequences of a token file (F/data.py:22-43): one per non-blank line,
+    whitespace-separated ids in [0, vocab); same exceptions and messages."""
     try:
-        with open(path) as fh:
-            lines = fh.readlines()
+        text = open(path).read()
     except OSError as exc:
         raise DataError(f"cannot read {path}: {exc}") from exc
-    seqs = []
-    for ln, line in enumerate(lines, start=1):
-        parts = line.split()
-        if not parts:
-            continue
-        try:
-            ids = [int(p) for p in parts]
-        except ValueError:
-            raise ParseError(f"{path}:{ln}: non-integer token") from None
-        if min(ids) < 0:
-            raise ParseError(f"{path}:{ln}: negative token id")
-        if max(ids) >= vocab:
-            raise TokenOutOfRange(f"{path}:{ln}: token id >= vocab ({vocab})")
-        seqs.append(ids)
-    return seqs
+    parsed = (_parse_line(path, n, line, vocab) for n, line in enumerate(text.splitlines(), 1))
+    return [ids for ids in parsed if ids is not None]
 
 
 class SyntheticTask:
-    """copy: target = source; reverse: target reversed (F/data.py:61-102)."""
+    """copy / reverse batches as a pure function of (seed, step) (F/data.py:61-102).
+
+    Lengths come from counter-RNG stream 101, payload symbols from stream 102
+    (one draw per padded cell, row-major); the batch is assembled with
+    whole-array index arithmetic rather than a per-sequence loop.
+    """
 
     def __init__(self, run_cfg):
-        m, t, d = run_cfg.model, run_cfg.train, run_cfg.data
-        if m.vocab < 4:
+        model, train, data = run_cfg.model, run_cfg.train, run_cfg.data
+        if model.vocab < 4:
             raise DataError("synthetic tasks need vocab >= 4")
-        self.task = d.task
-        self.pad_id = d.pad_id
-        self.bos = bos_id(d.pad_id, m.vocab)
-        self.symbols = np.array(payload_range(d.pad_id, m.vocab))
-        self.min_len = max(1, d.min_len)
-        self.max_len = m.max_len
-        self.batch_size = max(1, t.batch_tokens // m.max_len)
-        self.seed = t.seed
+        self.task = data.task
+        self.pad_id = data.pad_id
+        self.bos = bos_id(data.pad_id, model.vocab)
+        self.symbols = np.asarray(payload_range(data.pad_id, model.vocab))
+        self.min_len = max(1, data.min_len)
+        self.max_len = model.max_len
+        self.batch_size = max(1, train.batch_tokens // model.max_len)
+        self.seed = train.seed
 
     def possible_shapes(self) -> list:
-        return [(self.batch_size, l) for l in
-                sorted({bucket_len(m, self.max_len) for m in range(self.min_len, self.max_len + 1)})]
+        lens = range(self.min_len, self.max_len + 1)
+        return [(self.batch_size, L) for L in sorted(set(bucket_len(n, self.max_len) for n in lens))]
 
     def batch(self, step: int) -> Batch:
-        b = self.batch_size
-        span = self.max_len - self.min_len + 1
-        lens = (_uniform(derive_seed(self.seed, step, 101), b) * span).astype(int) + self.min_len
-        lb = bucket_len(int(lens.max()), self.max_len)
-        u = _uniform(derive_seed(self.seed, step, 102), b * lb)
-        body = self.symbols[(u * len(self.symbols)).astype(int)].reshape(b, lb)
-        src = np.full((b, lb), self.pad_id, dtype=np.int64)
-        tgt_out = np.full((b, lb), self.pad_id, dtype=np.int64)
-        tgt_in = np.full((b, lb), self.pad_id, dtype=np.int64)
-        for i in range(b):
-            n = int(lens[i])
-            seq = body[i, :n]
-            out = seq if self.task == "copy" else seq[::-1]
-            src[i, :n] = seq
-            tgt_out[i, :n] = out
-            tgt_in[i, 0] = self.bos
-            tgt_in[i, 1:n] = out[:n - 1]
-        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt_out, src_len=lens.astype(np.int64),
-                     pad_id=self.pad_id)
+        nseq = self.batch_size
+        nlen = self.max_len - self.min_len + 1
+        lens = self.min_len + np.floor(_uniform(derive_seed(self.seed, step, 101), nseq) * nlen).astype(np.int64)
+        width = bucket_len(int(lens.max()), self.max_len)
+        draw = _uniform(derive_seed(self.seed, step, 102), nseq * width)
+        payload = self.symbols[np.floor(draw * len(self.symbols)).astype(np.int64)].reshape(nseq, width)
+        col = np.arange(width)[None, :]
+        inside = col < lens[:, None]
+        if self.task == "copy":
+            target = payload
+        else:                                  # position j reads payload[n - 1 - j]
+            target = np.take_along_axis(payload, np.where(inside, lens[:, None] - 1 - col, 0), 1)
+        src = np.where(inside, payload, self.pad_id).astype(np.int64)
+        tgt_out = np.where(inside, target, self.pad_id).astype(np.int64)
+        shifted = np.concatenate([np.full((nseq, 1), self.bos), target[:, :-1]], axis=1)
+        tgt_in = np.where(inside, shifted, self.pad_id).astype(np.int64)
+        return Batch(src=src, tgt_in=tgt_in, tgt_out=tgt_out, src_len=lens, pad_id=self.pad_id)
 
 
 class FixedShapeTask:

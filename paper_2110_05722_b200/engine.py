@@ -28,7 +28,7 @@ from .dist import DataParallel
 from .errors import DataError
 from .memplan import PlannedArena, RecordingArena, TensorTag, classify, estimate_capacity
 from .model import Batch, MaskBank, SeedTable, Transformer, _ViewSink, make_model, validate_batch
-from .trainer import OptimConfig, Workspace, _state, workspace_pack
+from .trainer import OptimConfig, Workspace, _state, bias_correction_rows, workspace_pack
 
 EVAL_STEP_BASE = 1 << 30
 
@@ -391,7 +391,7 @@ class TrainingEngine:
             _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
                       ws.m32.data_ptr(), ws.v32.data_ptr(), ws.n_elements,
                       self._opt.hyper.data_ptr(), self._opt.bc.data_ptr(),
-                      self._opt.bc.numel() // 2, 0, self._applied_dev.data_ptr(),
+                      bias_correction_rows(self._opt.bc), 0, self._applied_dev.data_ptr(),
                       self._nonfinite.data_ptr(), loss_ptr, st)
         else:
             _lib.call("ls2_sgd", ws.params16.data_ptr(), ws.grads16.data_ptr(), ws.m32.data_ptr(),

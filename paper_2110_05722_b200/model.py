@@ -887,13 +887,14 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     qkv = arena.alloc((b, l, 3 * d), dt)
     _linear(u1.view(r, d), w.wqkv, w.bqkv, qkv.view(r, 3 * d))
     stash.push(p + "qkv", qkv)
-    scores = arena.alloc((b, n_heads, l, l), dt)
     if ATT.fused_ok(dt, l, l, hd, mask):
+        scores = ATT.alloc_state(arena, dt, b, n_heads, l, l, hd, mask)
         ctxm = arena.alloc((b, l, d), dt)
         ATT.forward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
                     scores, ctxm, d, b, n_heads, l, l, hd, mask, 1.0 / math.sqrt(hd))
         stash.push(p + "probs", scores)
     else:
+        scores = arena.alloc((b, n_heads, l, l), dt)
         qh, kh, vh = _qkv_heads(qkv, n_heads)
         K.gemm(qh, kh, trans_b=True, out=scores, alpha=1.0 / math.sqrt(hd))
         K.softmax_forward(scores, mask=mask, out=scores)
@@ -1201,13 +1202,14 @@ def decoder_layer_forward(x, w: DecoderLayerWeights, kv, self_mask, cross_mask, 
     qc = arena.alloc((b, l, d), dt)
     _linear(u2.view(r, d), w.cross_wq, w.cross_bq, qc.view(r, d))
     stash.push(p + "qc", qc)
-    scores_x = arena.alloc((b, n_heads, l, ls), dt)
     if ATT.fused_ok(dt, l, ls, hd, cross_mask) and k_i.dtype == dt and v_i.dtype == dt:
+        scores_x = ATT.alloc_state(arena, dt, b, n_heads, l, ls, hd, cross_mask)
         ctxm_x = arena.alloc((b, l, d), dt)
         ATT.forward(qc, d, k_i, k_i.stride(1), v_i, v_i.stride(1), scores_x, ctxm_x, d, b,
                     n_heads, l, ls, hd, cross_mask, 1.0 / math.sqrt(hd))
         stash.push(p + "probs_x", scores_x)
     else:
+        scores_x = arena.alloc((b, n_heads, l, ls), dt)
         K.gemm(_heads(qc, n_heads), _heads(_as_dt(k_i, dt), n_heads), trans_b=True,
                out=scores_x, alpha=1.0 / math.sqrt(hd))
         K.softmax_forward(scores_x, mask=cross_mask, out=scores_x)

@@ -32,12 +32,25 @@ def _ref(q, k, v, keep, dout, scale):
         np.einsum("bhqk,bhqd->bhkd", p, dout)
 
 
-@pytest.mark.parametrize("B,NH,Lq,Lk,kind", [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"),
-                                             (3, 2, 37, 37, "causal"), (4, 16, 128, 128, "padding"),
-                                             (5, 3, 20, 52, "padding"), (2, 4, 7, 100, "none"),
-                                             (2, 2, 128, 16, "none"), (113, 8, 36, 36, "padding"),
-                                             (10, 8, 48, 48, "causal"), (7, 2, 33, 45, "padding")])
-def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind):
+class _Alloc:
+    def alloc(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device="cuda")
+
+
+CASES = [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"), (3, 2, 37, 37, "causal"),
+         (4, 16, 128, 128, "padding"), (5, 3, 20, 52, "padding"), (2, 4, 7, 100, "none"),
+         (2, 2, 128, 16, "none"), (113, 8, 36, 36, "padding"), (10, 8, 48, 48, "causal"),
+         (7, 2, 33, 45, "padding"),
+         # tcgen05 packing: G = 64 // max(Lq, Lk) sequences per tile, ragged last
+         # group, odd tile counts, cross-attention with Lq != Lk
+         (512, 8, 8, 8, "padding"), (341, 8, 12, 12, "causal"), (3, 2, 5, 5, "none"),
+         (33, 4, 16, 24, "padding"), (5, 3, 64, 64, "none"), (9, 1, 30, 31, "padding"),
+         (17, 8, 60, 60, "causal"), (1, 1, 1, 1, "none")]
+
+
+@pytest.mark.parametrize("impl", ["tc", "mma"])
+@pytest.mark.parametrize("B,NH,Lq,Lk,kind", CASES)
+def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind, impl):
     rng = np.random.default_rng(B * 100 + Lq)
     d = 64 * NH
     # self-attention style packed [B, L, 3d] for q/k/v when Lq == Lk, separate otherwise
@@ -53,26 +66,91 @@ def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind):
     kv = torch.tensor(np.concatenate([kd, vd], axis=-1), device="cuda")   # strided K/V views
     q = torch.tensor(qd, device="cuda")
     k, v = kv[..., :d], kv[..., d:]
-    probs = torch.empty((B, NH, Lq, Lk), dtype=torch.float16, device="cuda")
+    assert ATT.fused_ok(torch.float16, Lq, Lk, 64, mask)
+    if impl == "tc":
+        if not ATT.tc_ok(torch.float16, Lq, Lk, 64, mask):
+            assert max(Lq, Lk) > 64
+            pytest.skip("beyond the tcgen05 family (L > 64)")
+        probs = ATT.alloc_state(_Alloc(), torch.float16, B, NH, Lq, Lk, 64, mask)
+        assert probs.dtype == torch.float32 and probs.shape == (B, NH, Lq, 2)
+    else:
+        probs = torch.empty((B, NH, Lq, Lk), dtype=torch.float16, device="cuda")
     o = torch.empty((B, Lq, d), dtype=torch.float16, device="cuda")
     scale = 1.0 / math.sqrt(64)
-    assert ATT.fused_ok(torch.float16, Lq, Lk, 64, mask)
     ATT.forward(q, d, k, 2 * d, v, 2 * d, probs, o, d, B, NH, Lq, Lk, 64, mask, scale)
     dq = torch.empty_like(q)
     dkv = torch.zeros((B, Lk, 2 * d), dtype=torch.float16, device="cuda")
     dout = torch.tensor(dod, device="cuda")
+    cs = torch.full((B, 3 * d), float("nan"), dtype=torch.float64, device="cuda")
     ATT.backward(q, d, k, 2 * d, v, 2 * d, probs, dout, d, dq, d, dkv[..., :d], 2 * d,
-                 dkv[..., d:], 2 * d, B, NH, Lq, Lk, 64, scale)
+                 dkv[..., d:], 2 * d, B, NH, Lq, Lk, 64, scale,
+                 colsums=((cs, 0, 3 * d), (cs, d, 3 * d), (cs, 2 * d, 3 * d)))
     hs = lambda x, L: x.astype(np.float32).reshape(B, L, NH, 64).transpose(0, 2, 1, 3)  # noqa
     p, oo, dqq, dkk, dvv = _ref(hs(qd, Lq), hs(kd, Lk), hs(vd, Lk), keep, hs(dod, Lq), scale)
     merge = lambda x: x.transpose(0, 2, 1, 3).reshape(B, x.shape[2], d)  # noqa
-    assert np.abs(H(probs).astype(np.float32) - p).max() <= 2e-3
-    if keep is not None:
-        assert np.all(H(probs)[~np.broadcast_to(keep, p.shape)] == 0)
+    if impl == "mma":
+        assert np.abs(H(probs).astype(np.float32) - p).max() <= 2e-3
+        if keep is not None:
+            assert np.all(H(probs)[~np.broadcast_to(keep, p.shape)] == 0)
+    else:
+        # stats = (max of the scaled unmasked scores in the log2 domain, i.e. times
+        # log2(e), and 1 / sum exp(s - max)) per row
+        s = np.einsum("bhqd,bhkd->bhqk", hs(qd, Lq), hs(kd, Lk)) * np.float32(scale)
+        if keep is not None:
+            s = np.where(np.broadcast_to(keep, s.shape), s, -np.inf)
+        m = s.max(-1)
+        iz = 1.0 / np.exp(s - m[..., None]).sum(-1)
+        st = H(probs)
+        m2 = m * np.float32(1.4426950408889634)
+        assert np.abs(st[..., 0] - m2).max() <= 1e-2 * max(1.0, np.abs(m2).max())
+        assert np.abs(st[..., 1] - iz).max() <= 1e-2 * np.abs(iz).max()
     for got, want in ((H(o), merge(oo)), (H(dq), merge(dqq)), (H(dkv[..., :d]), merge(dkk)),
                       (H(dkv[..., d:]), merge(dvv))):
         got = got.astype(np.float32)
         assert np.abs(got - want).max() <= 2e-2 * max(1.0, np.abs(want).max())
+    # bias-gradient partials: column sums of the stored fp16 dQ / dK / dV.  The
+    # mma.sync family leaves one row per batch; the tcgen05 family one row per
+    # packed group of G sequences (at the group's first batch, zeros in the
+    # others).  Either way the B rows sum to the bias gradient.
+    want_cs = np.concatenate([H(dq).astype(np.float64).sum(1), H(dkv).astype(np.float64).sum(1)],
+                             axis=1)
+    got_cs = H(cs)
+    assert np.isfinite(got_cs).all()
+    tol = 1e-3 * max(1.0, np.abs(want_cs).sum(0).max())
+    assert np.abs(got_cs.sum(0) - want_cs.sum(0)).max() <= tol
+    if impl == "mma":
+        assert np.abs(got_cs - want_cs).max() <= 1e-3 * max(1.0, np.abs(want_cs).max())
+    else:
+        G = 64 // max(Lq, Lk)
+        grp = np.add.reduceat(want_cs, np.arange(0, B, G), axis=0)
+        assert np.abs(got_cs[::G] - grp).max() <= 1e-3 * max(1.0, np.abs(grp).max())
+        assert np.all(np.delete(got_cs, np.arange(0, B, G), axis=0) == 0)
+
+
+@pytest.mark.parametrize("B,NH,L,kind", [(64, 8, 64, "padding"), (512, 8, 8, "causal"),
+                                         (113, 8, 36, "padding"), (341, 8, 12, "none")])
+def test_tc_attention_matches_mma_kernels(B, NH, L, kind):
+    """The tcgen05 and mma.sync families on the same inputs: outputs and
+    gradients agree to fp16 rounding (both accumulate in fp32)."""
+    rng = np.random.default_rng(7 + L)
+    d = 64 * NH
+    qkv = torch.tensor((rng.normal(size=(B, L, 3 * d)) * 0.8).astype(np.float16), device="cuda")
+    dout = torch.tensor(rng.normal(size=(B, L, d)).astype(np.float16), device="cuda")
+    lens = torch.tensor(rng.integers(1, L + 1, B), device="cuda")
+    mask = AttentionMask(kind, lens) if kind == "padding" else AttentionMask(kind)
+    q, k, v = qkv[..., :d], qkv[..., d:2 * d], qkv[..., 2 * d:]
+    outs = {}
+    for impl in ("tc", "mma"):
+        st = ATT.alloc_state(_Alloc(), torch.float16, B, NH, L, L, 64, mask) if impl == "tc" \
+            else torch.empty((B, NH, L, L), dtype=torch.float16, device="cuda")
+        o = torch.empty((B, L, d), dtype=torch.float16, device="cuda")
+        ATT.forward(q, 3 * d, k, 3 * d, v, 3 * d, st, o, d, B, NH, L, L, 64, mask, 0.125)
+        dqkv = torch.empty_like(qkv)
+        ATT.backward(q, 3 * d, k, 3 * d, v, 3 * d, st, dout, d, dqkv[..., :d], 3 * d,
+                     dqkv[..., d:2 * d], 3 * d, dqkv[..., 2 * d:], 3 * d, B, NH, L, L, 64, 0.125)
+        outs[impl] = (H(o).astype(np.float32), H(dqkv).astype(np.float32))
+    for a, b in zip(outs["tc"], outs["mma"]):
+        assert np.abs(a - b).max() <= 1e-2 * max(1.0, np.abs(b).max())
 
 
 def test_fused_attention_gates():

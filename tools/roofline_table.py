@@ -33,6 +33,10 @@ def algo_table(model: str):
      5 * N * D * 2 + N * D // 8 + 8 * N),
     (r"ln_bwd_stage<[^>]*, true, false, false>", "LayerNorm bwd + residual", 4 * N * D * 2 + 8 * N),
     (r"ln_bwd_stage<[^>]*, false, false, false>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
+    (r"attn_tc_fwd_kernel", "fused attention fwd, tcgen05 (QK^T, mask, softmax, PV; row stats)",
+     4 * N * D * 2 + N * H * 8),
+    (r"attn_tc_bwd_kernel", "fused attention bwd, tcgen05 (P recomputed; + bias partials)",
+     7 * N * D * 2 + N * H * 8),
     (r"attn_fwd_kernel", "fused attention fwd (QK^T, mask, softmax, PV)", 4 * N * D * 2 + BHL2 * 2),
     (r"attn_bwd_kernel|attn_bwd_persist", "fused attention bwd", 7 * N * D * 2 + BHL2 * 2),
     (r"criterion_rows_kernel|criterion_kernel", "fused LS cross-entropy fwd+bwd (in place)",
@@ -51,10 +55,16 @@ def algo_table(model: str):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("json")
-    ap.add_argument("--peak", type=float, default=6449.4)
+    ap.add_argument("--peak", type=float, default=None,
+                    help="HBM GB/s (default: MEASURED_PEAKS.json hbm_gbs, else 6449.4)")
     ap.add_argument("--md", default=None)
     ap.add_argument("--model", default="tbase", choices=sorted(SIZES))
     a = ap.parse_args()
+    if a.peak is None:
+        import os
+        mp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                          "MEASURED_PEAKS.json")
+        a.peak = json.load(open(mp))["hbm_gbs"] if os.path.exists(mp) else 6449.4
     ALGO = algo_table(a.model)
     d = json.load(open(a.json))
     lines = ["| kernel | what | launches/step | µs/launch (in situ) | algorithmic MB/launch | "
