@@ -13,10 +13,19 @@ training step (forward, backward, scale/narrow, [all-reduce], Adam).
 * e2e      : the public API call TrainingEngine.train_step(step) per step: host
              batch -> pinned -> H2D inside the graph -> D2H of (loss, count,
              correct, applied, nonfinite); wall/event time over K steps.
-* roofline : the dominant hand-written kernel (workspace Adam, 22 B/param)
-             re-timed live with CUDA events at the production size.
-* cpu_baseline / --impl reference : the CPU oracle port of the reference
-             (oracle/lsport.py) on a bounded sample of the same step.
+* roofline : `kernels` = every hand-written kernel of the step (CUPTI durations
+             over CUDA-graph replays of the 64 x 64 bucket, algorithmic bytes per
+             launch, fraction of the measured HBM peak), largest step share
+             first; the dominant one (by step share) is re-timed live with CUDA
+             events on its launching stream for `achieved` / `frac`.
+* steps_applied : optimizer updates applied over the timed steps (device
+             counter; a non-finite gradient skips the update, F/trainer.py:53-56).
+* cpu_baseline : the CPU oracle port of the reference (oracle/lsport.py) on a
+             bounded sample of the same step, on the box's host cores.
+* --impl reference : the CPU oracle port on FULL 4096-token T-base steps
+             (1 warm-up + timed steps; the timed count is
+             min(--steps, what fits the time budget)), plus the host record
+             (lscpu model, cores, numpy / BLAS).
 """
 
 from __future__ import annotations
@@ -183,38 +192,70 @@ def oracle_sample_step(st, step: int):
     return loss / cnt
 
 
+def host_record() -> dict:
+    """CPU model, core count, numpy and BLAS versions of the host running the CPU arm."""
+    rec = {"cores": os.cpu_count() or 1, "numpy": np.__version__}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                rec[k.strip().lower().replace(" ", "_").replace("(s)", "s")] = v.strip()
+    except Exception:
+        pass
+    try:
+        cfg = np.show_config(mode="dicts")
+        blas = cfg.get("Build Dependencies", {}).get("blas", {})
+        rec["blas"] = f"{blas.get('name', '?')} {blas.get('version', '')}".strip()
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        rec["blas_threads"] = [(i.get("internal_api"), i.get("version"), i.get("num_threads"))
+                               for i in threadpool_info()]
+    except Exception:
+        pass
+    return rec
+
+
 def run_reference(args):
+    """the CPU arm on FULL T-base steps (the same WMT-shaped
+    batches as our arm's default, all their sequences), 1 warm-up, then
+    min(--steps, as many as fit REF_BUDGET_S seconds) timed steps, at least 2."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    # each step is a bounded sample of the T-base step: as many sequences as keep
-    # the whole --steps/--warmup run near 2.5 minutes (~0.27 s per sequence on
-    # 16 host cores), between 1 and 8 (numpy/OpenBLAS run bigger batches better)
-    seqs = max(1, min(8, int(150.0 / (0.27 * (args.steps + args.warmup)))))
+    budget = float(os.environ.get("REF_BUDGET_S", "150"))
     wmt = args.data == "wmt"            # the same batch shapes as our arm's default
-    st = oracle_sample_setup(seqs, wmt=wmt)
-    for s in range(args.warmup):
-        oracle_sample_step(st, s)
+    st = oracle_sample_setup(B, wmt=wmt)           # B sequences = the whole 4096-token step
+    t_w = time.perf_counter()
+    oracle_sample_step(st, 0)                      # 1 warm-up (BASELINE.md §4)
+    per = time.perf_counter() - t_w
+    nsteps = max(2, min(args.steps, int(budget / max(per, 1e-3))))
     st["counted"] = 0
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        oracle_sample_step(st, args.warmup + s)
+    for s in range(nsteps):
+        oracle_sample_step(st, 1 + s)
     dt = time.perf_counter() - t0
     tps = st["counted"] / dt
-    cores = os.cpu_count() or 1
+    host = host_record()
+    cores = host["cores"]
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": args.gpus, "steps": nsteps, "steps_requested": args.steps, "warmup": 1,
+            "warmup_requested": args.warmup,
+            "ms_per_step": 1e3 * dt / nsteps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp16 workspace / f32 compute", "data": "synthetic",
-            "config": {"workload": "Transformer-base 6e6d V32k, 4096 tok/GPU step (sampled)"
-                                   + (", synthetic WMT-shaped batches" if wmt else ""),
-                       "sample": f"{'up to ' if wmt else ''}{seqs * L} tokens fwd+bwd per step "
-                                 f"({'leading sequences of the step WMT-shaped batch' if wmt else f'{seqs} x {L}'}) "
-                                 f"+ Adam on {seqs}/{B} of the 60.66M-param workspace; "
-                                 "non-pad target tokens counted"},
+            "config": {"workload": "Transformer-base 6e6d V32k, full <= 4096-target-token step"
+                                   + (", synthetic WMT-shaped batches" if wmt else " (64 x 64)"),
+                       "protocol": "BASELINE.md §4: full T-base step (fwd+bwd over every "
+                                   "sequence of the batch, narrow, Adam over the whole 60.66M "
+                                   "workspace), 1 warm-up + min(--steps, budget) timed steps; "
+                                   "non-pad target tokens counted"},
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"{seqs}x{L} tokens fwd+bwd + Adam on 1/{B // seqs} of the "
-                                       f"workspace per step, {args.steps} steps"},
+                             "sample": f"full steps ({nsteps} timed after 1 warm-up) of the "
+                                       "oracle port oracle/lsport.py (numpy/OpenBLAS, all "
+                                       "host threads)"},
+            "host": host,
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -246,6 +287,7 @@ def time_adam(eng, reps=20):
     """Dominant hand-written kernel, timed live with CUDA events at P = 60.66M."""
     import torch
     from paper_2110_05722_b200 import _lib
+    from paper_2110_05722_b200.trainer import bias_correction_rows
     n = eng.ws.n_elements
     dev = eng.device
     p = torch.randn(n, device=dev).half()
@@ -257,7 +299,7 @@ def time_adam(eng, reps=20):
 
     def launch():
         _lib.call("ls2_adam", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), n,
-                  opt.hyper.data_ptr(), opt.bc.data_ptr(), opt.bc.numel() // 2, 1, None, None,
+                  opt.hyper.data_ptr(), opt.bc.data_ptr(), bias_correction_rows(opt.bc), 1, None, None,
                   None, st.cuda_stream)
     for _ in range(3):
         launch()
@@ -326,6 +368,7 @@ def run_ours(args):
     step_tokens = sum(t for _, _, t in plan)
     st = torch.cuda.current_stream()
     launches0 = _lib.launches()
+    applied0 = int(eng._applied_dev.item())
 
     # --- value: device-resident inputs, CUDA-graph replays, CUDA events ---
     dp.barrier()
@@ -346,6 +389,7 @@ def run_ours(args):
         if prof_range:
             torch.cuda.profiler.stop()
     dp.barrier()
+    steps_applied = int(eng._applied_dev.item()) - applied0
     ms = e0.elapsed_time(e1) / args.steps
     ms = dp.max_scalar(ms, device=eng.device)
     per_step_launches = max(eng.launches_per_step(k) for k in keys)
@@ -360,6 +404,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     e0.record(st)
     e2e_tokens = 0
+    e2e_skipped = 0
     for s in range(args.steps):
         # the same step numbers (so the same WMT bucket sequence) as the value loop:
         # e2e - value is then the host-side cost alone, not a different bucket mix
@@ -367,6 +412,7 @@ def run_ours(args):
         # BERT: every input token (MLMTask inputs carry no padding); Transformer:
         # the step's non-pad targets
         e2e_tokens += m.tokens if not bert else B * L
+        e2e_skipped += int(m.skipped)
     e1.record(st)
     torch.cuda.synchronize()
     wall_ms = 1e3 * (time.perf_counter() - t0) / args.steps
@@ -378,17 +424,28 @@ def run_ours(args):
     e2e = etok.item() / args.steps / (e2e_ms / 1e3)
     io = eng._io_for(B, L)
 
-    # --- roofline of the dominant hand-written kernel ---
-    nbytes, adam_ms = time_adam(eng)
+    # --- roofline: every hand-written kernel of the step (CUPTI, in situ), the
+    # dominant one (largest step share) re-timed live with CUDA events ---
+    from paper_2110_05722_b200 import roofline as RL
     peak, peak_kind = _peaks()
-    achieved = nbytes / (adam_ms / 1e3) / 1e9
+    mc = run.model
+    algo = RL.algo_table(B * L, mc.d_model, mc.d_ff, V, B, L, mc.n_heads, eng.ws.n_elements)
+    table = RL.kernel_table(RL.profile_graph(dev_graphs[key]), algo, peak)
+    dom = next((r for r in table if r["bytes_per_launch"] is not None), None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "adam_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    if dom is not None and "adam" in dom["kernel"]:
+        nbytes, dom_ms = time_adam(eng)
+        timing = "CUDA events on the launching stream, 20 back-to-back launches at P = 60.66M"
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+    else:
+        nbytes, dom_ms = dom["bytes_per_launch"], dom["us_per_launch"] / 1e3
+        timing = "CUPTI in situ (graph replay)"
+    achieved = nbytes / (dom_ms / 1e3) / 1e9
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -410,10 +467,15 @@ def run_ours(args):
                         "d2h_bytes_per_step": 40, "ms_per_step": e2e_ms,
                         "last_loss": m.loss},
                 "gpu_launches": per_step_launches * args.steps,
-                "roofline": {"kernel": "ls2_adam (workspace Adam, 22 B/param)",
+                "steps_applied": steps_applied, "e2e_steps_applied": args.steps - e2e_skipped,
+                "roofline": {"kernel": dom["kernel"] if dom else None,
+                             "what": dom["what"] if dom else None,
+                             "dominant_by": "largest hand-written share of the step (CUPTI)",
                              "bound": "hbm", "achieved": achieved, "peak": peak,
                              "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                             "traffic": traffic, "launch_ms": adam_ms},
+                             "traffic": traffic, "launch_ms": dom_ms, "timing": timing,
+                             "kernels_shape": f"{B}x{L} bucket",
+                             "kernels": table},
                 }
         if world == 1 and not args.no_cpu_baseline and args.model == "tbase":
             line["cpu_baseline"] = cpu_baseline(wmt)

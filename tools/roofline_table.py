@@ -10,7 +10,12 @@ reports achieved GB/s and the fraction of the measured HBM peak.
 
 import argparse
 import json
+import os
 import re
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2110_05722_b200.roofline import algo_table as _algo  # noqa: E402
 
 SIZES = {   # tokens, d, ffn, vocab, batch, len, heads, parameters (learned positions, max_len 256)
     "tbase": (4096, 512, 2048, 32000, 64, 64, 8, 60_655_616),
@@ -19,37 +24,7 @@ SIZES = {   # tokens, d, ffn, vocab, batch, len, heads, parameters (learned posi
 
 
 def algo_table(model: str):
-    N, D, F, V, B, L, H, P = SIZES[model]
-    BHL2 = B * H * L * L
-    # (regex on the kernel name, description, algorithmic bytes per launch)
-    return [
-    (r"bdr_fwd_vec", "bias+dropout+residual fwd", 3 * N * D * 2 + N * D // 8),
-    (r"bdr_bwd_vec", "bias+dropout+residual bwd (+dbias partials)", 2 * N * D * 2 + N * D // 8),
-    (r"brd_fwd_vec", "bias+ReLU+dropout fwd", 2 * N * F * 2 + 2 * N * F // 8),
-    (r"brd_bwd_vec", "bias+ReLU+dropout bwd (+dbias partials)", 2 * N * F * 2 + 2 * N * F // 8),
-    (r"ln_fwd_bdr_warp", "bias+dropout+residual -> LayerNorm fwd", 4 * N * D * 2 + N * D // 8 + 8 * N),
-    (r"ln_fwd_warp", "LayerNorm fwd", 2 * N * D * 2 + 8 * N),
-    (r"ln_bwd_stage<[^>]*, true, true, true>", "LayerNorm bwd + residual + bdr bwd",
-     5 * N * D * 2 + N * D // 8 + 8 * N),
-    (r"ln_bwd_stage<[^>]*, true, false, false>", "LayerNorm bwd + residual", 4 * N * D * 2 + 8 * N),
-    (r"ln_bwd_stage<[^>]*, false, false, false>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
-    (r"attn_tc_fwd_kernel", "fused attention fwd, tcgen05 (QK^T, mask, softmax, PV; row stats)",
-     4 * N * D * 2 + N * H * 8),
-    (r"attn_tc_bwd_kernel", "fused attention bwd, tcgen05 (P recomputed; + bias partials)",
-     7 * N * D * 2 + N * H * 8),
-    (r"attn_fwd_kernel", "fused attention fwd (QK^T, mask, softmax, PV)", 4 * N * D * 2 + BHL2 * 2),
-    (r"attn_bwd_kernel|attn_bwd_persist", "fused attention bwd", 7 * N * D * 2 + BHL2 * 2),
-    (r"criterion_rows_kernel|criterion_kernel", "fused LS cross-entropy fwd+bwd (in place)",
-     2 * N * V * 2),
-    (r"adam_kernel", "workspace Adam (22 B/param)", 22 * P),
-    (r"scale_narrow_kernel", "fp32 grad accumulators -> scaled fp16 workspace", 6 * P),
-    (r"emb_fwd_vec", "embedding fwd (gather, scale, pos, dropout)", 8 * N + 3 * N * D * 2 + N * D // 8),
-    (r"emb_bwd_scatter", "embedding bwd scatter (fp32 RMW)", N * D * 2 + 2 * N * D * 4 + N * D // 8),
-    (r"emb_bwd_pos", "positional-table grad", N * D * 2 + N * D // 8),
-    # ALU-bound (integer splitmix64 draws), reported below the HBM table
-    (r"dropout_bits_multi", "mask bank", None),
-    (r"finish_narrow", "deferred bias/LN column sums -> fp16 workspace", None),
-    ]
+    return _algo(*SIZES[model])
 
 
 def main():
@@ -61,7 +36,6 @@ def main():
     ap.add_argument("--model", default="tbase", choices=sorted(SIZES))
     a = ap.parse_args()
     if a.peak is None:
-        import os
         mp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                           "MEASURED_PEAKS.json")
         a.peak = json.load(open(mp))["hbm_gbs"] if os.path.exists(mp) else 6449.4
