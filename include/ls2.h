@@ -26,7 +26,8 @@ enum {
   LS2_F16 = 0,
   LS2_BF16 = 1,
   LS2_F32 = 2,
-  LS2_F64 = 3
+  LS2_F64 = 3,
+  LS2_I32 = 4                 /* collectives only (the non-finite counter) */
 };
 
 /* status codes (F/errors.py) */
@@ -49,6 +50,16 @@ enum {
   LS2_MASK_CAUSAL = 1,        /* keep col <= row % lq                          */
   LS2_MASK_PADDING = 2,       /* keep col < valid_len[row / (heads * lq)]     */
   LS2_MASK_DENSE = 3          /* uint8 keep[rows, cols]                        */
+};
+
+/* softmax reduction strategies (F/kernels.py:23-24,80-106): AUTO = the shape rule
+ * (register template while the row fits, else one CTA per row); SERIAL = the
+ * register template where it fits; TREE = one CTA per row (3 passes).  Both keep
+ * f64 partition sums, so outputs agree to 1 ULP (T/test_kernels.py:160-171). */
+enum {
+  LS2_SOFTMAX_AUTO = 0,
+  LS2_SOFTMAX_SERIAL = 1,     /* "row_serial"        */
+  LS2_SOFTMAX_TREE = 2        /* "row_parallel_tree" */
 };
 
 const char* ls2_last_error(void);
@@ -150,6 +161,13 @@ int ls2_softmax_bwd(const void* dy, const void* q, void* dx, int64_t rows, int64
                     double out_scale, int tin, int tout, void* stream);
 int ls2_log_softmax_fwd(const void* h, void* y, int64_t rows, int64_t cols, int tin,
                         int tout, void* stream);
+/* the same with an explicit LS2_SOFTMAX_* strategy (the `strategy=` argument) */
+int ls2_softmax_fwd_strategy(const void* x, void* y, int64_t rows, int64_t cols, int mask_kind,
+                             int64_t lq, int64_t heads, const int64_t* valid_lens,
+                             const uint8_t* dense_keep, double in_scale, int* all_masked,
+                             int strategy, int tin, int tout, void* stream);
+int ls2_log_softmax_fwd_strategy(const void* h, void* y, int64_t rows, int64_t cols, int strategy,
+                                 int tin, int tout, void* stream);
 
 /* ---- fused short-sequence attention (fp16, head dim 64, Lq/Lk <= 128) ----
  * Replaces scores = QK^T/sqrt(hd) -> softmax_forward(mask) -> P V -> merge heads
@@ -250,6 +268,12 @@ int ls2_embedding_bwd(const void* dy, const int64_t* tokens, const uint8_t* keep
 int ls2_adam(uint16_t* p16, const uint16_t* g16, float* m, float* v, int64_t n,
              const float* hyper, const float* bc_table, int64_t bc_len, int64_t t_host,
              const int64_t* applied, const int* nonfinite, const double* loss, void* stream);
+/* ls2_adam over the rank's shard of a sharded-optimizer step: spans = n_spans {offset,
+ * length} int64 pairs (device) of the flat workspace, max_len = the longest span */
+int ls2_adam_spans(uint16_t* p16, const uint16_t* g16, float* m, float* v, const int64_t* spans,
+                   int64_t n_spans, int64_t max_len, const float* hyper, const float* bc_table,
+                   int64_t bc_len, int64_t t_host, const int64_t* applied, const int* nonfinite,
+                   const double* loss, void* stream);
 int ls2_sgd(uint16_t* p16, const uint16_t* g16, float* vel, int64_t n, const float* hyper,
             const int* nonfinite, const double* loss, void* stream);
 /* applied += (nonfinite==0 && loss finite)  — one thread */
@@ -272,6 +296,10 @@ int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chun
                       const double* partial_base, uint16_t* g16, double loss_scale,
                       const double* out3, int64_t count_host, float post, int* nonfinite,
                       void* stream);
+/* the same column sums unscaled into the fp32 accumulator: acc32[dst + c] = f32(sum_g ...)
+ * (data parallelism reduces them in fp32 with the rest of the bucket, then narrows) */
+int ls2_finish_acc32(const int64_t* desc, const int32_t* chunks, int64_t n_chunks,
+                     const double* partial_base, float* acc32, void* stream);
 /* number of partial rows the column-sum producers write (0: shape not deferrable) */
 int ls2_colsum_nblk(int64_t rows, int64_t cols, int dtype);
 int ls2_layernorm_bwd_nblk(int64_t rows, int64_t cols);
@@ -339,6 +367,13 @@ int ls2_comm_unique_id(uint8_t* out128);
 int ls2_comm_init(void** comm_out, int nranks, int rank, const uint8_t* id128, int device);
 int ls2_comm_allreduce(void* comm, const void* send, void* recv, int64_t count, int dtype,
                        void* stream);
+/* sharded-optimizer exchange (SPEC.md:573 makes the 1/N element shard legal):
+ * reduce-scatter (sum; rank r gets [r*count, (r+1)*count) of the sum, in place when
+ * recv == send + rank*count) and all-gather (in place when send == recv + rank*count) */
+int ls2_comm_reduce_scatter(void* comm, const void* send, void* recv, int64_t count, int dtype,
+                            void* stream);
+int ls2_comm_all_gather(void* comm, const void* send, void* recv, int64_t count, int dtype,
+                        void* stream);
 int ls2_comm_destroy(void* comm);
 
 #ifdef __cplusplus

@@ -21,6 +21,7 @@ F16, BF16, F32, F64 = 0, 1, 2, 3
 MASK_NONE, MASK_CAUSAL, MASK_PADDING, MASK_DENSE = 0, 1, 2, 3
 
 _TORCH_CODE = {torch.float16: F16, torch.bfloat16: BF16, torch.float32: F32, torch.float64: F64}
+I32 = 4             # collectives only (LS2_I32)
 
 P = ctypes.c_void_p
 I = ctypes.c_int
@@ -54,6 +55,8 @@ _SIGS = {
     "ls2_softmax_fwd": [P, P, L, L, I, L, L, P, P, D, P, I, I, P],
     "ls2_softmax_bwd": [P, P, P, L, L, D, I, I, P],
     "ls2_log_softmax_fwd": [P, P, L, L, I, I, P],
+    "ls2_softmax_fwd_strategy": [P, P, L, L, I, L, L, P, P, D, P, I, I, I, P],
+    "ls2_log_softmax_fwd_strategy": [P, P, L, L, I, I, I, P],
     "ls2_ls_ce_fwd": [P, P, P, P, P, L, L, D, L, I, I, P],
     "ls2_ls_ce_bwd": [P, P, P, P, L, L, D, L, I, D, I, I, P],
     "ls2_criterion_fused": [P, P, P, P, P, P, P, L, L, D, L, I, D, I, P],
@@ -71,12 +74,14 @@ _SIGS = {
     "ls2_embedding_fwd": [P, P, P, P, P, P, L, L, L, L, D, I, I, U, P, U, D, I, I, P],
     "ls2_embedding_bwd": [P, P, P, P, P, I, I, L, L, L, L, D, I, D, I, P],
     "ls2_adam": [P, P, P, P, L, P, P, L, L, P, P, P, P],
+    "ls2_adam_spans": [P, P, P, P, P, L, L, P, P, L, L, P, P, P, P],
     "ls2_sgd": [P, P, P, L, P, P, P, P],
     "ls2_step_commit": [P, P, P, P, P],
     "ls2_step_report": [P, P, P, P, P],
     "ls2_scale_narrow": [P, P, L, D, P, L, Fl, P, P],
     "ls2_count_nonfinite_f16": [P, L, P, P],
     "ls2_finish_narrow": [P, P, L, P, P, D, P, L, Fl, P, P],
+    "ls2_finish_acc32": [P, P, L, P, P, P],
     "ls2_colsum_nblk": [L, L, I],
     "ls2_layernorm_bwd_nblk": [L, L],
     "ls2_blas_create": [],
@@ -94,6 +99,8 @@ _SIGS = {
     "ls2_comm_unique_id": [P],
     "ls2_comm_init": [P, I, I, P, I],
     "ls2_comm_allreduce": [P, P, P, L, I, P],
+    "ls2_comm_reduce_scatter": [P, P, P, L, I, P],
+    "ls2_comm_all_gather": [P, P, P, L, I, P],
     "ls2_comm_destroy": [P],
 }
 _RESTYPES = {"ls2_last_error": ctypes.c_char_p, "ls2_blas_create": P, "ls2_blas_destroy": None,

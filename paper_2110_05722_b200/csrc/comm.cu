@@ -29,6 +29,9 @@ struct NcclApi {
   ncclResult_t (*get_unique_id)(NcclUid*) = nullptr;
   ncclResult_t (*comm_init_rank)(ncclComm_t*, int, NcclUid, int) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, int, int, ncclComm_t,
+                                 cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
   ncclResult_t (*get_version)(int*) = nullptr;
@@ -38,7 +41,7 @@ NcclApi g_nccl;
 std::mutex g_nccl_mu;
 
 // NCCL's ncclDataType_t / ncclRedOp_t values (stable across NCCL 2.x)
-constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclBfloat16 = 9;
+constexpr int kNcclInt32 = 2, kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclBfloat16 = 9;
 constexpr int kNcclSum = 0;
 
 int nccl_dtype(int dtype) {
@@ -47,6 +50,7 @@ int nccl_dtype(int dtype) {
     case LS2_BF16: return kNcclBfloat16;
     case LS2_F32: return kNcclFloat32;
     case LS2_F64: return kNcclFloat64;
+    case LS2_I32: return kNcclInt32;
     default: return -1;
   }
 }
@@ -63,10 +67,13 @@ int load_nccl(const char* path) {
   api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
   api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
   api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
+  api.reduce_scatter = (decltype(api.reduce_scatter))dlsym(h, "ncclReduceScatter");
+  api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
   api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
   api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
   api.get_version = (decltype(api.get_version))dlsym(h, "ncclGetVersion");
-  if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+  if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.reduce_scatter ||
+      !api.all_gather || !api.comm_destroy)
     return ls2::fail(LS2_ERR_CUDA, "libnccl.so.2 lacks the required entry points");
   g_nccl = api;
   return LS2_OK;
@@ -122,6 +129,36 @@ int ls2_comm_allreduce(void* comm, const void* send, void* recv, int64_t count, 
   if (ncclResult_t r = g_nccl.all_reduce(send, recv, (size_t)count, dt, kNcclSum, comm,
                                          ls2::as_stream(stream)))
     return nccl_fail("ncclAllReduce", r);
+  return LS2_OK;
+}
+
+// Sum-reduce-scatter: rank r receives elements [r*count, (r+1)*count) of the sum of
+// every rank's `send` (N*count elements).  In place when recv == send + rank*count:
+// the sharded-optimizer exchange reduces each fp32 gradient bucket this way.
+int ls2_comm_reduce_scatter(void* comm, const void* send, void* recv, int64_t count, int dtype,
+                            void* stream) {
+  if (count <= 0) return LS2_OK;
+  if (!comm || !g_nccl.reduce_scatter)
+    return ls2::fail(LS2_ERR_CUDA, "reduce_scatter: no communicator");
+  int dt = nccl_dtype(dtype);
+  if (dt < 0) return ls2::fail(LS2_ERR_DTYPE, "reduce_scatter: unsupported dtype");
+  if (ncclResult_t r = g_nccl.reduce_scatter(send, recv, (size_t)count, dt, kNcclSum, comm,
+                                             ls2::as_stream(stream)))
+    return nccl_fail("ncclReduceScatter", r);
+  return LS2_OK;
+}
+
+// All-gather: every rank's `count` elements land at recv + r*count on all ranks.  In
+// place when send == recv + rank*count (the updated params16 shard of a bucket).
+int ls2_comm_all_gather(void* comm, const void* send, void* recv, int64_t count, int dtype,
+                        void* stream) {
+  if (count <= 0) return LS2_OK;
+  if (!comm || !g_nccl.all_gather) return ls2::fail(LS2_ERR_CUDA, "all_gather: no communicator");
+  int dt = nccl_dtype(dtype);
+  if (dt < 0) return ls2::fail(LS2_ERR_DTYPE, "all_gather: unsupported dtype");
+  if (ncclResult_t r = g_nccl.all_gather(send, recv, (size_t)count, dt, comm,
+                                         ls2::as_stream(stream)))
+    return nccl_fail("ncclAllGather", r);
   return LS2_OK;
 }
 

@@ -36,12 +36,9 @@ __device__ __forceinline__ void adam_elem(float& p, float g, float& m, float& v,
   p = __fsub_rn(p, __fmul_rn(k.lr, __fadd_rn(q, __fmul_rn(k.wd, p))));
 }
 
-__global__ void adam_kernel(uint16_t* __restrict__ p16, const uint16_t* __restrict__ g16,
-                            float* __restrict__ m, float* __restrict__ v, int64_t n,
-                            const float* __restrict__ hyper, const float* __restrict__ bc,
-                            int64_t bc_len, int64_t t_host, const int64_t* __restrict__ applied,
-                            const int* nonfinite, const double* loss, bool vec) {
-  if (skip_step(nonfinite, loss)) return;
+__device__ __forceinline__ AdamK adam_constants(const float* __restrict__ hyper,
+                                                 const float* __restrict__ bc, int64_t bc_len,
+                                                 int64_t t_host, const int64_t* applied) {
   const int64_t t = t_host > 0 ? t_host : (*applied + 1);
   float bc1, bc2;
   if (t < bc_len) {
@@ -52,12 +49,22 @@ __global__ void adam_kernel(uint16_t* __restrict__ p16, const uint16_t* __restri
     bc1 = __double2float_rn(1.0 - pow(betas[0], (double)t));
     bc2 = __double2float_rn(1.0 - pow(betas[1], (double)t));
   }
-  AdamK k{hyper[0], hyper[1], hyper[2], hyper[3], hyper[4], hyper[5], hyper[6], hyper[7],
-          bc1, bc2, hyper[7] != 1.0f};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  return AdamK{hyper[0], hyper[1], hyper[2], hyper[3], hyper[4], hyper[5], hyper[6], hyper[7],
+               bc1, bc2, hyper[7] != 1.0f};
+}
+
+// Adam over elements [0, n) of the given spans; CTA `bid` of `nblk` grid-strides.
+__device__ __forceinline__ void adam_range(uint16_t* __restrict__ p16,
+                                           const uint16_t* __restrict__ g16,
+                                           float* __restrict__ m, float* __restrict__ v,
+                                           int64_t n, const AdamK& k, bool vec, int64_t bid,
+                                           int64_t nblk) {
+  const int64_t stride = nblk * blockDim.x;
+  const int64_t first = bid * (int64_t)blockDim.x + threadIdx.x;
+  int64_t tail = 0;
   if (vec) {
     const int64_t groups = n / 8;
-    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+    for (int64_t gi = first; gi < groups; gi += stride) {
       const uint4 pp = __ldcs(reinterpret_cast<const uint4*>(p16) + gi);
       const uint4 gg = __ldcs(reinterpret_cast<const uint4*>(g16) + gi);
       float4 m0 = __ldcs(reinterpret_cast<const float4*>(m) + 2 * gi);
@@ -82,18 +89,39 @@ __global__ void adam_kernel(uint16_t* __restrict__ p16, const uint16_t* __restri
       __stcs(reinterpret_cast<float4*>(v) + 2 * gi, v0);
       __stcs(reinterpret_cast<float4*>(v) + 2 * gi + 1, v1);
     }
-    for (int64_t i = groups * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-      float p = h2f(p16[i]);
-      adam_elem(p, h2f(g16[i]), m[i], v[i], k);
-      p16[i] = f2h(p);
-    }
-  } else {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-      float p = h2f(p16[i]);
-      adam_elem(p, h2f(g16[i]), m[i], v[i], k);
-      p16[i] = f2h(p);
-    }
+    tail = groups * 8;
   }
+  for (int64_t i = tail + first; i < n; i += stride) {
+    float p = h2f(p16[i]);
+    adam_elem(p, h2f(g16[i]), m[i], v[i], k);
+    p16[i] = f2h(p);
+  }
+}
+
+__global__ void adam_kernel(uint16_t* __restrict__ p16, const uint16_t* __restrict__ g16,
+                            float* __restrict__ m, float* __restrict__ v, int64_t n,
+                            const float* __restrict__ hyper, const float* __restrict__ bc,
+                            int64_t bc_len, int64_t t_host, const int64_t* __restrict__ applied,
+                            const int* nonfinite, const double* loss, bool vec) {
+  if (skip_step(nonfinite, loss)) return;
+  const AdamK k = adam_constants(hyper, bc, bc_len, t_host, applied);
+  adam_range(p16, g16, m, v, n, k, vec, blockIdx.x, gridDim.x);
+}
+
+// The sharded optimizer's update: the rank's element spans {offset, length}
+// (int64 pairs, device) of the flat workspace, one grid row (blockIdx.y) per span.
+__global__ void adam_spans_kernel(uint16_t* __restrict__ p16, const uint16_t* __restrict__ g16,
+                                  float* __restrict__ m, float* __restrict__ v,
+                                  const int64_t* __restrict__ spans,
+                                  const float* __restrict__ hyper, const float* __restrict__ bc,
+                                  int64_t bc_len, int64_t t_host,
+                                  const int64_t* __restrict__ applied, const int* nonfinite,
+                                  const double* loss, bool vec_ok) {
+  if (skip_step(nonfinite, loss)) return;
+  const AdamK k = adam_constants(hyper, bc, bc_len, t_host, applied);
+  const int64_t off = spans[2 * blockIdx.y], n = spans[2 * blockIdx.y + 1];
+  const bool vec = vec_ok && (off & 7) == 0;
+  adam_range(p16 + off, g16 + off, m + off, v + off, n, k, vec, blockIdx.x, gridDim.x);
 }
 
 __global__ void sgd_kernel(uint16_t* __restrict__ p16, const uint16_t* __restrict__ g16,
@@ -192,9 +220,11 @@ __global__ void scale_narrow_kernel(const float* __restrict__ acc, uint16_t* __r
 // c0 + 2l, +1 (16-byte loads), warp w sums partial rows w, w+8, ... with four
 // loads in flight, and the 8 warp sums are folded in warp order (deterministic).
 constexpr int kFinishCols = 64;
+template <bool ACC32>
 __global__ void __launch_bounds__(256) finish_narrow_kernel(
     const int64_t* __restrict__ desc, const int32_t* __restrict__ chunks,
-    const double* __restrict__ part_base, uint16_t* __restrict__ g16, double loss_scale,
+    const double* __restrict__ part_base, uint16_t* __restrict__ g16,
+    float* __restrict__ acc32, double loss_scale,
     const double* out3, int64_t count_host, float post, int* nonfinite) {
   __shared__ double red[8][kFinishCols + 1];
   const int di = chunks[2 * blockIdx.x], c0 = chunks[2 * blockIdx.x + 1];
@@ -235,6 +265,15 @@ __global__ void __launch_bounds__(256) finish_narrow_kernel(
     const int cc = lane + 32 * w;
     const int64_t col = c0 + cc;
     int bad = 0;
+    if (ACC32) {   // unscaled f32 column sums into the accumulator (reduced, then narrowed)
+      if (col < cols) {
+        double t = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += red[q][cc];
+        acc32[dst + col] = (float)t;
+      }
+      return;
+    }
     if (col < cols) {
       double t = 0;
 #pragma unroll
@@ -285,6 +324,22 @@ int ls2_adam(uint16_t* p16, const uint16_t* g16, float* m, float* v, int64_t n, 
   return check_launch("adam");
 }
 
+int ls2_adam_spans(uint16_t* p16, const uint16_t* g16, float* m, float* v, const int64_t* spans,
+                   int64_t n_spans, int64_t max_len, const float* hyper, const float* bc_table,
+                   int64_t bc_len, int64_t t_host, const int64_t* applied, const int* nonfinite,
+                   const double* loss, void* stream) {
+  if (n_spans <= 0 || max_len <= 0) return LS2_OK;
+  if (n_spans > 65535) return fail(LS2_ERR_SHAPE, "adam_spans: too many spans");
+  if (t_host <= 0 && !applied) return fail(LS2_ERR_SHAPE, "adam: need t_host or applied counter");
+  const bool vec = aligned16(p16) && aligned16(g16) && aligned16(m) && aligned16(v);
+  int64_t gx = ceil_div(ceil_div(max_len, 8), 256);
+  const int64_t cap = ceil_div((int64_t)kNumSMs * 8, n_spans);
+  gx = gx < 1 ? 1 : (gx > cap ? cap : gx);
+  adam_spans_kernel<<<dim3((unsigned)gx, (unsigned)n_spans), 256, 0, as_stream(stream)>>>(
+      p16, g16, m, v, spans, hyper, bc_table, bc_len, t_host, applied, nonfinite, loss, vec);
+  return check_launch("adam_spans");
+}
+
 int ls2_sgd(uint16_t* p16, const uint16_t* g16, float* vel, int64_t n, const float* hyper,
             const int* nonfinite, const double* loss, void* stream) {
   if (n <= 0) return LS2_OK;
@@ -322,9 +377,17 @@ int ls2_finish_narrow(const int64_t* desc, const int32_t* chunks, int64_t n_chun
                       void* stream) {
   if (n_chunks <= 0) return LS2_OK;
   if (count_host < 0 && !out3) return fail(LS2_ERR_SHAPE, "finish_narrow: no token count");
-  finish_narrow_kernel<<<(unsigned)n_chunks, 256, 0, as_stream(stream)>>>(
-      desc, chunks, partial_base, g16, loss_scale, out3, count_host, post, nonfinite);
+  finish_narrow_kernel<false><<<(unsigned)n_chunks, 256, 0, as_stream(stream)>>>(
+      desc, chunks, partial_base, g16, nullptr, loss_scale, out3, count_host, post, nonfinite);
   return check_launch("finish_narrow");
+}
+
+int ls2_finish_acc32(const int64_t* desc, const int32_t* chunks, int64_t n_chunks,
+                     const double* partial_base, float* acc32, void* stream) {
+  if (n_chunks <= 0) return LS2_OK;
+  finish_narrow_kernel<true><<<(unsigned)n_chunks, 256, 0, as_stream(stream)>>>(
+      desc, chunks, partial_base, nullptr, acc32, 1.0, nullptr, 1, 1.0f, nullptr);
+  return check_launch("finish_acc32");
 }
 
 int ls2_count_nonfinite_f16(const uint16_t* g16, int64_t n, int* nonfinite, void* stream) {

@@ -75,18 +75,21 @@ __global__ void __launch_bounds__(256) softmax_rows(const Tin* __restrict__ x, T
       }
     }
     mx = warp_max(mx, G);
-    C z = 0;
+    // the partition sum accumulates in f64 (the reference's float64 reduction), so
+    // this template and the tree kernel round it identically (1-ULP agreement)
+    double zd = 0;
 #pragma unroll
     for (int it = 0; it < ITERS; ++it)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const C ex = (v[it][e] == neg_inf<C>()) ? (C)0 : fexp(v[it][e] - mx);
         if (MODE == 0) v[it][e] = ex;
-        z += ex;
+        zd += (double)ex;
       }
-    z = warp_sum(z, G);
+    zd = warp_sum(zd, G);
     if (!live) continue;
     if (MODE == 0 && mx == neg_inf<C>() && all_masked && sub == 0) *all_masked = 1;
+    const C z = (C)zd;
     const C rz = (MODE == 0) ? (z > (C)0 ? (C)1 / z : (C)0) : flog(z);
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
@@ -168,55 +171,65 @@ __global__ void __launch_bounds__(256) softmax_bwd_rows(const Tin* __restrict__ 
 // ---------------------------------------------------------------------------
 // long rows: one CTA per row (online max/sum pass, then an output pass)
 // ---------------------------------------------------------------------------
-template <typename C>
-__device__ __forceinline__ void online_merge(C& m, C& s, C m2, C s2) {
-  const C mn = max(m, m2);
-  if (mn == neg_inf<C>()) return;
-  s = (m == neg_inf<C>() ? (C)0 : s * fexp(m - mn)) + (m2 == neg_inf<C>() ? (C)0 : s2 * fexp(m2 - mn));
-  m = mn;
-}
-
-template <typename C>
-__device__ void block_max_sum(C& m, C& s) {
-  __shared__ C sm[32], ss[32];
+// Fixed-shape CTA reductions (lane shuffles, then warp slots in order):
+// deterministic for a given blockDim.
+template <typename T>
+__device__ __forceinline__ T block_max(T v, T* red) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    C m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    online_merge(m, s, m2, s2);
-  }
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) { sm[wid] = m; ss[wid] = s; }
+  if (lane == 0) red[wid] = v;
   __syncthreads();
-  m = neg_inf<C>();
-  s = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) online_merge(m, s, sm[i], ss[i]);
+  T m = red[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, red[i]);
   __syncthreads();
+  return m;
 }
 
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  v = warp_sum(v);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  T s = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  __syncthreads();
+  return s;
+}
+
+// row_parallel_tree (F/kernels.py:63-74, selected at :80-106): one CTA per row,
+// three passes over the row (max; f64 partition sum of exp(v - max); output).
+// The statistics are the warp template's exactly (same max, same exp, an f64 sum
+// rounded once), so the two strategies agree to within 1 ULP.
 template <typename Tin, typename Tout, int MODE>
 __global__ void softmax_block(const Tin* __restrict__ x, Tout* __restrict__ y, int64_t rows,
                               int64_t cols, MaskSpec msk, double in_scale, int* all_masked) {
   using C = typename CompOf<Tin>::type;
+  __shared__ C redm[32];
+  __shared__ double reds[32];
   const C sc = (C)in_scale;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    C m = neg_inf<C>(), s = 0;
-    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
-      if (!kept(msk, r, c, cols)) continue;
-      const C v = cvt<C>(x[r * cols + c]) * sc;
-      online_merge(m, s, v, (C)1);
-    }
-    block_max_sum(m, s);
+    const Tin* xr = x + r * cols;
+    C m = neg_inf<C>();
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
+      if (kept(msk, r, c, cols)) m = max(m, cvt<C>(xr[c]) * sc);
+    m = block_max(m, redm);
+    double zd = 0;
+    if (m != neg_inf<C>())
+      for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
+        if (kept(msk, r, c, cols)) zd += (double)fexp(cvt<C>(xr[c]) * sc - m);
+    zd = block_sum(zd, reds);
     if (MODE == 0 && m == neg_inf<C>() && all_masked && threadIdx.x == 0) *all_masked = 1;
-    const C rz = (MODE == 0) ? (s > (C)0 ? (C)1 / s : (C)0) : flog(s);
+    const C z = (C)zd;
+    const C rz = (MODE == 0) ? (z > (C)0 ? (C)1 / z : (C)0) : flog(z);
     for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
-      const bool ok = kept(msk, r, c, cols);
-      const C v = cvt<C>(x[r * cols + c]) * sc;
+      const C v = cvt<C>(xr[c]) * sc;
       C o;
-      if (MODE == 0) o = ok ? fexp(v - m) * rz : (C)0;
+      if (MODE == 0) o = kept(msk, r, c, cols) ? fexp(v - m) * rz : (C)0;
       else o = (v - m) - rz;
       y[r * cols + c] = cvt<Tout>(o);
     }
-    __syncthreads();
   }
 }
 
@@ -272,10 +285,10 @@ inline int rows_grid(int64_t rows, int G) {
 
 template <int MODE, typename Tin, typename Tout>
 int launch_rows(const void* x, void* y, int64_t rows, int64_t cols, const MaskSpec& m,
-                double in_scale, int* all_masked, cudaStream_t st) {
+                double in_scale, int* all_masked, cudaStream_t st, int strategy = 0) {
   const bool v8 = cols % 8 == 0 && aligned16(x) && aligned16(y);
   RowShape s = row_shape(cols, v8);
-  if (s.block) {
+  if (s.block || strategy == LS2_SOFTMAX_TREE) {
     const int grid = (int)std::min<int64_t>(rows, kNumSMs * 16);
     softmax_block<Tin, Tout, MODE><<<grid, 512, 0, st>>>((const Tin*)x, (Tout*)y, rows, cols, m,
                                                           in_scale, all_masked);
@@ -327,22 +340,40 @@ extern "C" {
 int ls2_softmax_fwd(const void* x, void* y, int64_t rows, int64_t cols, int mask_kind, int64_t lq,
                     int64_t heads, const int64_t* valid_lens, const uint8_t* dense_keep,
                     double in_scale, int* all_masked, int tin, int tout, void* stream) {
+  return ls2_softmax_fwd_strategy(x, y, rows, cols, mask_kind, lq, heads, valid_lens, dense_keep,
+                                  in_scale, all_masked, LS2_SOFTMAX_AUTO, tin, tout, stream);
+}
+
+int ls2_softmax_fwd_strategy(const void* x, void* y, int64_t rows, int64_t cols, int mask_kind,
+                             int64_t lq, int64_t heads, const int64_t* valid_lens,
+                             const uint8_t* dense_keep, double in_scale, int* all_masked,
+                             int strategy, int tin, int tout, void* stream) {
   if (rows <= 0 || cols <= 0) return LS2_OK;
+  if (strategy < LS2_SOFTMAX_AUTO || strategy > LS2_SOFTMAX_TREE)
+    return fail(LS2_ERR_SHAPE, "softmax: unknown strategy");
   if ((mask_kind == LS2_MASK_CAUSAL || mask_kind == LS2_MASK_PADDING) && lq <= 0)
     return fail(LS2_ERR_SHAPE, "softmax: mask needs lq >= 1");
   MaskSpec m{mask_kind, lq < 1 ? 1 : lq, heads < 1 ? 1 : heads, valid_lens, dense_keep};
   return LS2_DISPATCH_IO(tin, tout, "softmax_fwd", [&] {
     return launch_rows<0, Tin, Tout>(x, y, rows, cols, m, in_scale, all_masked,
-                                     as_stream(stream));
+                                     as_stream(stream), strategy);
   });
 }
 
 int ls2_log_softmax_fwd(const void* h, void* y, int64_t rows, int64_t cols, int tin, int tout,
                         void* stream) {
+  return ls2_log_softmax_fwd_strategy(h, y, rows, cols, LS2_SOFTMAX_AUTO, tin, tout, stream);
+}
+
+int ls2_log_softmax_fwd_strategy(const void* h, void* y, int64_t rows, int64_t cols, int strategy,
+                                 int tin, int tout, void* stream) {
   if (rows <= 0 || cols <= 0) return LS2_OK;
+  if (strategy < LS2_SOFTMAX_AUTO || strategy > LS2_SOFTMAX_TREE)
+    return fail(LS2_ERR_SHAPE, "log_softmax: unknown strategy");
   MaskSpec m{LS2_MASK_NONE, 1, 1, nullptr, nullptr};
   return LS2_DISPATCH_IO(tin, tout, "log_softmax_fwd", [&] {
-    return launch_rows<1, Tin, Tout>(h, y, rows, cols, m, 1.0, nullptr, as_stream(stream));
+    return launch_rows<1, Tin, Tout>(h, y, rows, cols, m, 1.0, nullptr, as_stream(stream),
+                                     strategy);
   });
 }
 

@@ -13,11 +13,23 @@ batch shard and the exchange is overlapped with the backward pass:
      finished part of the flat workspace is always a suffix [frontier, n).
      `GradExchange` turns "these parameters are final" notices into contiguous
      buckets; for each bucket the comm stream waits on an event from the
-     compute stream, narrows fp32 accumulators (+ deferred bias/LN column
-     sums) into the fp16 workspace, sum-all-reduces it, and counts non-finite
-     values of the REDUCED bucket;
-  3. the compute stream joins the comm stream once, then runs Adam with an
-     identical skip decision on every rank.
+     compute stream, finishes the deferred bias/LN column sums into the fp32
+     accumulators, sum-reduces the fp32 bucket, narrows the reduced values into
+     the fp16 workspace and counts the non-finite ones;
+  3. the optimizer runs after the last bucket with an identical skip decision
+     on every rank (see the modes below).
+
+The bucket exchange runs in fp32 (the accumulators, narrowed after the sum, as
+the reference narrows once after its own sum: F/engine.py:152-157).  Two modes
+(`DataParallel(mode=...)`, env LS2_DP_MODE):
+  * "shard" (default): each bucket is reduce-scattered, every rank narrows and
+    Adam-updates only its 1/N chunk of each bucket (SPEC.md:573 makes the
+    element shard legal), the non-finite count is a scalar all-reduce, and the
+    updated params16 chunks are all-gathered in place;
+  * "allreduce": each bucket is all-reduced and every rank narrows and updates
+    the whole workspace.
+Buckets start on multiples of `align` = world x 64 elements (the workspace is
+padded to one), so every per-rank chunk is equal and 256-byte aligned.
 
 Everything is stream-ordered enqueue work, so the whole step — collectives
 included — is captured in the bucket's CUDA graph.  On CUDA the collectives
@@ -93,6 +105,28 @@ class NcclComm:
         _lib.call("ls2_comm_allreduce", self.handle, base, base, stop - start,
                   _lib.dtype_code(t), st)
 
+    def _span_call(self, fn, t, send_off, recv_off, count, stream):
+        from . import _lib
+        base = t.data_ptr()
+        es = t.element_size()
+        code = _lib.I32 if t.dtype == torch.int32 else _lib.dtype_code(t)
+        st = stream.cuda_stream if stream is not None else _lib.stream_handle()
+        _lib.call(fn, self.handle, base + send_off * es, base + recv_off * es, count, code, st)
+
+    def reduce_scatter(self, t: torch.Tensor, start: int, stop: int, stream=None):
+        """In place over t[start:stop]: this rank's chunk of the sum lands at
+        start + rank*c (c = (stop - start) / world)."""
+        c = (stop - start) // self.world
+        self._span_call("ls2_comm_reduce_scatter", t, start, start + self.rank * c, c, stream)
+
+    def all_gather(self, t: torch.Tensor, start: int, stop: int, stream=None):
+        """In place over t[start:stop]: every rank's chunk r*c lands everywhere."""
+        c = (stop - start) // self.world
+        self._span_call("ls2_comm_all_gather", t, start + self.rank * c, start, c, stream)
+
+    def allreduce_i32(self, t: torch.Tensor, stream=None):
+        self._span_call("ls2_comm_allreduce", t, 0, 0, t.numel(), stream)
+
     def close(self):
         if self.handle:
             from . import _lib
@@ -110,9 +144,11 @@ class GradExchange:
     elements are pending, everything pending on `flush()`.
     """
 
-    def __init__(self, links, n: int, bucket_elems: int):
+    def __init__(self, links, n: int, bucket_elems: int, align: int = 1):
         self.links = sorted(((o, o + ln, nm) for nm, o, ln in links), key=lambda x: x[0])
+        self.align = max(1, int(align))
         self.n = int(n)
+        self.n_pad = -(-self.n // self.align) * self.align
         self.bucket = max(1, int(bucket_elems))
         self.reset()
 
@@ -120,19 +156,24 @@ class GradExchange:
         self.done: set = set()
         self.idx = len(self.links)         # links[idx:] are finished
         self.frontier = self.n
-        self.issued = self.n               # [issued, n) already exchanged
+        self.issued = self.n_pad           # [issued, n_pad) already exchanged
 
     def _advance(self):
         while self.idx > 0 and self.links[self.idx - 1][2] in self.done:
             self.idx -= 1
             self.frontier = self.links[self.idx][0]
 
+    def _start(self) -> int:
+        """Lowest aligned bucket start inside the finished suffix."""
+        return -(-self.frontier // self.align) * self.align
+
     def ready(self, names) -> list:
         self.done.update(names)
         self._advance()
-        if self.issued - self.frontier >= self.bucket:
-            span = (self.frontier, self.issued)
-            self.issued = self.frontier
+        lo = self._start()
+        if self.issued - lo >= self.bucket:
+            span = (lo, self.issued)
+            self.issued = lo
             return [span]
         return []
 
@@ -153,18 +194,28 @@ class GradExchange:
         return []
 
 
-class DataParallel:
-    """Bucketed gradient all-reduce + totals all-reduce over the ranks.
+MODES = ("shard", "allreduce")
 
+
+class DataParallel:
+    """Bucketed fp32 gradient exchange + totals all-reduce over the ranks.
+
+    mode "shard": reduce-scatter buckets, Adam on the rank's chunks, all-gather
+    params16; "allreduce": all-reduce buckets, every rank updates everything.
     force=True makes a one-rank job take the exchange path too (one-rank NCCL
     communicator), so the overlapped step can be tested on a single GPU."""
 
-    def __init__(self, group=None, bucket_bytes: int = 8 << 20, force: bool = False):
+    def __init__(self, group=None, bucket_bytes: int = 16 << 20, force: bool = False,
+                 mode: str | None = None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.bucket_bytes = int(bucket_bytes)
         self.force = bool(force)
+        mode = mode or os.environ.get("LS2_DP_MODE", "shard")
+        if mode not in MODES:
+            raise ValueError(f"data-parallel mode must be one of {MODES}, got {mode!r}")
+        self.mode = mode
         self.comm: NcclComm | None = None
         self.comm_stream = None
 
@@ -185,8 +236,57 @@ class DataParallel:
         spans = [(s, min(n, s + per)) for s in range(0, n, per)]
         return list(reversed(spans))
 
-    def exchange_plan(self, links, n: int, elem_bytes: int = 2) -> GradExchange:
-        return GradExchange(links, n, max(1, self.bucket_bytes // elem_bytes))
+    @property
+    def sharded(self) -> bool:
+        return self.mode == "shard"
+
+    @property
+    def align(self) -> int:
+        """Bucket-start granularity in elements: equal, 256-byte aligned chunks."""
+        return 64 * (self.world if self.sharded else 1)
+
+    def padded(self, n: int) -> int:
+        a = self.align
+        return -(-int(n) // a) * a
+
+    def exchange_plan(self, links, n: int, elem_bytes: int = 4) -> GradExchange:
+        return GradExchange(links, n, max(1, self.bucket_bytes // elem_bytes), self.align)
+
+    def chunk(self, start: int, stop: int) -> tuple:
+        """(offset, length) of this rank's chunk of bucket [start, stop)."""
+        if not self.sharded:
+            return start, stop - start
+        c = (stop - start) // self.world
+        return start + self.rank * c, c
+
+    def reduce_scatter_span(self, flat: torch.Tensor, start: int, stop: int, stream=None):
+        if self.comm is not None:
+            self.comm.reduce_scatter(flat, start, stop, stream=stream)
+        elif self.world > 1:
+            c = (stop - start) // self.world
+            out = torch.empty(c, dtype=flat.dtype, device=flat.device)
+            dist.reduce_scatter_tensor(out, flat[start:stop].contiguous(), op=dist.ReduceOp.SUM,
+                                       group=self.group)
+            o = start + self.rank * c
+            flat[o:o + c].copy_(out)
+
+    def all_gather_span(self, flat: torch.Tensor, start: int, stop: int, stream=None):
+        if self.comm is not None:
+            self.comm.all_gather(flat, start, stop, stream=stream)
+        elif self.world > 1:
+            c = (stop - start) // self.world
+            o = start + self.rank * c
+            out = torch.empty(stop - start, dtype=flat.dtype, device=flat.device)
+            dist.all_gather_into_tensor(out, flat[o:o + c].contiguous(), group=self.group)
+            flat[start:stop].copy_(out)
+
+    def allreduce_count(self, t: torch.Tensor, stream=None):
+        """Sum an int32 counter over the ranks (the non-finite gradient count)."""
+        if self.comm is not None:
+            self.comm.allreduce_i32(t, stream=stream)
+        elif self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
 
     def allreduce_totals(self, out3: torch.Tensor, stream=None):
         if self.comm is not None:
@@ -213,9 +313,33 @@ class DataParallel:
         if self.world > 1:
             dist.barrier(group=self.group)
 
+    def shard_task(self, task):
+        """Every rank trains on its own batches: rank r's step s is the wrapped
+        task's step s * world + r (a task built from one seed would otherwise
+        hand every rank the same batch)."""
+        return task if self.world <= 1 else RankShardedTask(task, self.rank, self.world)
+
     def max_scalar(self, x: float, device=None) -> float:
         if self.world <= 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
+
+
+class RankShardedTask:
+    """Interleaves a (seed, step)-pure task over the ranks: rank r, step s reads
+    batch s * world + r.  The union of one step's batches over the ranks is a
+    contiguous run of the single-process stream."""
+
+    def __init__(self, task, rank: int, world: int):
+        self.task, self.rank, self.world = task, int(rank), int(world)
+
+    def batch(self, step: int):
+        return self.task.batch(int(step) * self.world + self.rank)
+
+    def possible_shapes(self):
+        return self.task.possible_shapes()
+
+    def __getattr__(self, name):
+        return getattr(self.task, name)

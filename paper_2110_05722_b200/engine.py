@@ -103,7 +103,9 @@ class TrainingEngine:
         ctx = _lib.context(device)
         self.device = ctx.device
         self.model = make_model(run_cfg.model)
-        self.task = task if task is not None else make_task(run_cfg)
+        self.dp = dp if dp is not None else DataParallel()
+        # under data parallelism every rank reads its own batches (dist.RankShardedTask)
+        self.task = task if task is not None else self.dp.shard_task(make_task(run_cfg))
         t = run_cfg.train
         self.optim = OptimConfig(algorithm=t.algorithm, lr=t.lr, beta1=t.beta1, beta2=t.beta2,
                                  eps_opt=t.eps_opt, weight_decay=t.weight_decay,
@@ -112,9 +114,13 @@ class TrainingEngine:
         self.ws: Workspace = workspace_pack([(n, init[n]) for n in self.model.param_names],
                                             t.algorithm)
         del init
-        self.pviews = self.ws.param_views()
         n = self.ws.n_elements
-        self.grad_acc = torch.zeros(n, dtype=torch.float32, device=self.device)
+        # the exchange's buckets split into equal aligned per-rank chunks: pad the
+        # workspace storage (never the [0, n) views) to the planner's granularity
+        n_pad = self.dp.padded(n) if self.dp.active else n
+        self.ws.pad_storage(n_pad)
+        self.pviews = self.ws.param_views()
+        self.grad_acc = torch.zeros(n_pad, dtype=torch.float32, device=self.device)
         self.gviews = {lk.name: self.grad_acc[lk.offset:lk.offset + lk.length].view(lk.shape)
                        for lk in self.ws.links}
         self._opt = _state(self.ws, self.optim)
@@ -123,8 +129,8 @@ class TrainingEngine:
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._dev_out = torch.zeros(5, dtype=torch.float64, device=self.device)
         self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
-        self.dp = dp if dp is not None else DataParallel()
         self._xplan = None
+        self._span_tables: dict = {}
         if self.dp.active:
             self.dp.setup_device(self.device)
             self._xplan = self.dp.exchange_plan(
@@ -247,6 +253,8 @@ class TrainingEngine:
             self._nonfinite.zero_()
             self._xplan.reset()
             self._totals_sent = False
+            self._deferred_done = set()
+            self._buckets, self._shard_spans = [], []
             sink.on_ready = lambda names, _s=sink: self._on_ready(_s, names)
         out = self.model.forward_backward(
             self.pviews, io.batch(), p_drop=t.p_drop, alpha=t.alpha, seed=t.seed, step=step,
@@ -294,27 +302,93 @@ class TrainingEngine:
 
     def _exchange_bucket(self, sink, start: int, stop: int):
         """On the comm stream, after everything the compute stream has enqueued so
-        far: narrow [start, stop) (+ its deferred column sums), sum-all-reduce it
-        and count non-finite values of the reduced bucket."""
+        far: finish the deferred column sums that reach into [start, stop) into the
+        fp32 accumulators, sum-reduce the fp32 bucket (reduce-scatter: this rank's
+        chunk; all-reduce: all of it), narrow the reduced values into grads16 and
+        count the non-finite ones (dist.py)."""
         t = self.cfg.train
-        cs = self.dp.comm_stream
+        dp = self.dp
+        cs = dp.comm_stream
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
         cs.wait_event(ev)
         with torch.cuda.stream(cs):
             out3 = sink.totals
             if not self._totals_sent:
-                self.dp.allreduce_totals(out3, stream=cs)
+                dp.allreduce_totals(out3, stream=cs)
                 self._totals_sent = True
             ws = self.ws
-            _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr() + 4 * start,
-                      ws.grads16.data_ptr() + 2 * start, stop - start, float(t.loss_scale),
-                      out3.data_ptr(), -1, float(1.0 / t.act_grad_scale), None, cs.cuda_stream)
-            entries = [e for e in sink.deferred if start <= self.ws.resolve(e[0])[0] < stop]
-            self._finish_deferred(sink, out3, None, entries=entries)
-            self.dp.allreduce_span(ws.grads16, start, stop, stream=cs)
-            _lib.call("ls2_count_nonfinite_f16", ws.grads16.data_ptr() + 2 * start, stop - start,
+            entries = []
+            for e in sink.deferred:
+                if e[0] in self._deferred_done:
+                    continue
+                off, ln = ws.resolve(e[0])
+                if off + ln > start:           # finished: it lies in the finished suffix
+                    entries.append(e)
+                    self._deferred_done.add(e[0])
+            if entries:
+                tab = self._finish_table(entries)
+                _lib.call("ls2_finish_acc32", tab[0].data_ptr(), tab[1].data_ptr(), tab[2], None,
+                          self.grad_acc.data_ptr(), cs.cuda_stream)
+            if dp.sharded:
+                dp.reduce_scatter_span(self.grad_acc, start, stop, stream=cs)
+            else:
+                dp.allreduce_span(self.grad_acc, start, stop, stream=cs)
+            off, c = dp.chunk(start, stop)
+            _lib.call("ls2_scale_narrow", self.grad_acc.data_ptr() + 4 * off,
+                      ws.grads16.data_ptr() + 2 * off, c, float(t.loss_scale),
+                      out3.data_ptr(), -1, float(1.0 / t.act_grad_scale),
                       self._nonfinite.data_ptr(), cs.cuda_stream)
+            self._buckets.append((start, stop))
+            self._shard_spans.append((off, c))
+
+    def _spans_table(self, spans) -> torch.Tensor:
+        key = tuple(spans)
+        tab = self._span_tables.get(key)
+        if tab is None:
+            tab = torch.tensor([x for sp in spans for x in sp], dtype=torch.int64,
+                               device=self.device)
+            self._span_tables[key] = tab
+        return tab
+
+    def _dp_update(self, loss_ptr):
+        """Data-parallel optimizer step on the comm stream, after the last bucket.
+        shard: global non-finite count (scalar all-reduce), Adam/SGD on this rank's
+        chunks, in-place all-gather of the updated params16 chunks; allreduce:
+        every rank holds the whole reduced gradient and updates everything."""
+        dp, ws, cs = self.dp, self.ws, self.dp.comm_stream
+        with torch.cuda.stream(cs):
+            st = cs.cuda_stream
+            if not dp.sharded:
+                self._optimizer(0, ws.n_elements, loss_ptr, st)
+                return
+            dp.allreduce_count(self._nonfinite, stream=cs)
+            spans = [sp for sp in self._shard_spans if sp[1] > 0]
+            if self.optim.algorithm == "adam" and spans:
+                _lib.call("ls2_adam_spans", ws.params16.data_ptr(), ws.grads16.data_ptr(),
+                          ws.m32.data_ptr(), ws.v32.data_ptr(),
+                          self._spans_table(spans).data_ptr(), len(spans),
+                          max(c for _, c in spans), self._opt.hyper.data_ptr(),
+                          self._opt.bc.data_ptr(), bias_correction_rows(self._opt.bc), 0,
+                          self._applied_dev.data_ptr(), self._nonfinite.data_ptr(), loss_ptr, st)
+            else:
+                for off, c in spans:
+                    self._optimizer(off, c, loss_ptr, st)
+            for start, stop in self._buckets:
+                dp.all_gather_span(ws.params16, start, stop, stream=cs)
+
+    def _optimizer(self, off: int, n: int, loss_ptr, st):
+        ws = self.ws
+        if self.optim.algorithm == "adam":
+            _lib.call("ls2_adam", ws.params16.data_ptr() + 2 * off,
+                      ws.grads16.data_ptr() + 2 * off, ws.m32.data_ptr() + 4 * off,
+                      ws.v32.data_ptr() + 4 * off, n, self._opt.hyper.data_ptr(),
+                      self._opt.bc.data_ptr(), bias_correction_rows(self._opt.bc), 0,
+                      self._applied_dev.data_ptr(), self._nonfinite.data_ptr(), loss_ptr, st)
+        else:
+            _lib.call("ls2_sgd", ws.params16.data_ptr() + 2 * off,
+                      ws.grads16.data_ptr() + 2 * off, ws.m32.data_ptr() + 4 * off, n,
+                      self._opt.hyper.data_ptr(), self._nonfinite.data_ptr(), loss_ptr, st)
 
     _BANK_GROUPS = {"cross_kv.": "tgt"}
 
@@ -353,6 +427,14 @@ class TrainingEngine:
         entries = sink.deferred if (entries is None and sink is not None) else entries
         if not entries:
             return
+        tab = self._finish_table(entries)
+        t = self.cfg.train
+        _lib.call("ls2_finish_narrow", tab[0].data_ptr(), tab[1].data_ptr(), tab[2], None,
+                  self.ws.grads16.data_ptr(), float(t.loss_scale), out3.data_ptr(), -1,
+                  float(1.0 / t.act_grad_scale), nonfinite_ptr, _lib.stream_handle())
+
+    def _finish_table(self, entries):
+        """(desc, chunks, n_chunks) device tables of the deferred entries (cached)."""
         key = tuple((n, buf.data_ptr(), nb, st, k, c) for n, buf, nb, st, k, c in entries)
         tab = self._finish_tables.get(key)
         if tab is None:
@@ -364,18 +446,19 @@ class TrainingEngine:
             tab = (torch.tensor(desc, dtype=torch.int64, device=self.device),
                    torch.tensor(chunks, dtype=torch.int32, device=self.device), len(chunks))
             self._finish_tables[key] = tab
-        t = self.cfg.train
-        _lib.call("ls2_finish_narrow", tab[0].data_ptr(), tab[1].data_ptr(), tab[2], None,
-                  self.ws.grads16.data_ptr(), float(t.loss_scale), out3.data_ptr(), -1,
-                  float(1.0 / t.act_grad_scale), nonfinite_ptr, _lib.stream_handle())
+        return tab
 
     def _update(self, out3: torch.Tensor, sink=None, host_copy: bool = True):
         """narrow(+scale) -> [all-reduce] -> non-finite count -> Adam/SGD -> commit."""
         st = _lib.stream_handle()
         t = self.cfg.train
         ws = self.ws
+        loss_ptr = out3.data_ptr()
+        joined = getattr(self, "_bank_done", None)
         if self.dp.active:
-            # every bucket was narrowed + reduced + checked on the comm stream
+            # every bucket was reduced + narrowed + checked on the comm stream;
+            # the optimizer (sharded or whole) follows there, then the join
+            self._dp_update(loss_ptr)
             ev = torch.cuda.Event()
             ev.record(self.dp.comm_stream)
             torch.cuda.current_stream().wait_event(ev)
@@ -385,18 +468,7 @@ class TrainingEngine:
                       ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
                       float(1.0 / t.act_grad_scale), self._nonfinite.data_ptr(), st)
             self._finish_deferred(sink, out3, self._nonfinite.data_ptr())
-        loss_ptr = out3.data_ptr()
-        joined = getattr(self, "_bank_done", None)
-        if self.optim.algorithm == "adam":
-            _lib.call("ls2_adam", ws.params16.data_ptr(), ws.grads16.data_ptr(),
-                      ws.m32.data_ptr(), ws.v32.data_ptr(), ws.n_elements,
-                      self._opt.hyper.data_ptr(), self._opt.bc.data_ptr(),
-                      bias_correction_rows(self._opt.bc), 0, self._applied_dev.data_ptr(),
-                      self._nonfinite.data_ptr(), loss_ptr, st)
-        else:
-            _lib.call("ls2_sgd", ws.params16.data_ptr(), ws.grads16.data_ptr(), ws.m32.data_ptr(),
-                      ws.n_elements, self._opt.hyper.data_ptr(), self._nonfinite.data_ptr(),
-                      loss_ptr, st)
+            self._optimizer(0, ws.n_elements, loss_ptr, st)
         _lib.call("ls2_step_report", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
                   loss_ptr, self._dev_out.data_ptr(), st)
         if joined is not None:

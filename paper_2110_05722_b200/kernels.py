@@ -108,6 +108,16 @@ def host_tokens(tokens) -> np.ndarray | None:
 # reduction strategy (F/kernels.py:80-106)
 # ---------------------------------------------------------------------------
 
+_STRATEGY_CODE = {None: 0, ROW_SERIAL: 1, ROW_PARALLEL_TREE: 2}
+
+
+def _strategy_code(strategy) -> int:
+    """`strategy=` of the softmax family -> LS2_SOFTMAX_* (None: the shape rule).
+    Any other value reduces serially, as the reference's _reduce_rows does
+    (F/kernels.py:73-77)."""
+    return _STRATEGY_CODE.get(strategy, 1)
+
+
 def select_softmax_strategy(rows: int, cols: int, autotune: bool = False) -> str:
     """Shape -> strategy.  On the GPU the two strategies are the register-cached
     sub-warp template (row_serial) and the CTA-per-row template
@@ -438,9 +448,9 @@ def softmax_forward(x, mask=None, out=None, strategy: str | None = None, in_scal
     r = xt.numel() // c
     kind, lq, heads, lens, dense = mask_spec(mask, shape)
     y, orig = _out(out, shape, tout, xt.device)
-    _lib.call("ls2_softmax_fwd", xt.data_ptr(), y.data_ptr(), r, c, kind, lq, heads,
-              _lib.ptr(lens), _lib.ptr(dense), float(in_scale), None, _lib.dtype_code(tin),
-              _lib.dtype_code(tout), _lib.stream_handle())
+    _lib.call("ls2_softmax_fwd_strategy", xt.data_ptr(), y.data_ptr(), r, c, kind, lq, heads,
+              _lib.ptr(lens), _lib.ptr(dense), float(in_scale), None, _strategy_code(strategy),
+              _lib.dtype_code(tin), _lib.dtype_code(tout), _lib.stream_handle())
     y = _finish(y, orig)
     return y, SoftmaxCache(probs=y)
 
@@ -453,8 +463,9 @@ def log_softmax_forward(h, out=None, strategy: str | None = None):
     if c < 2:
         raise ShapeMismatch(f"log_softmax needs >= 2 classes, got {c}")
     y, orig = _out(out, ht.shape, tout, ht.device)
-    _lib.call("ls2_log_softmax_fwd", ht.data_ptr(), y.data_ptr(), ht.numel() // c, c,
-              _lib.dtype_code(tin), _lib.dtype_code(tout), _lib.stream_handle())
+    _lib.call("ls2_log_softmax_fwd_strategy", ht.data_ptr(), y.data_ptr(), ht.numel() // c, c,
+              _strategy_code(strategy), _lib.dtype_code(tin), _lib.dtype_code(tout),
+              _lib.stream_handle())
     return _finish(y, orig)
 
 

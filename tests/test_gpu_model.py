@@ -263,28 +263,31 @@ def test_tbase_step_runs_and_is_finite():
     assert not ms[-1].skipped
 
 
-def _dp_run(force: bool, graphs: bool, steps: int, bucket_bytes=8 << 20, model=None, task=None):
+def _dp_run(force: bool, graphs: bool, steps: int, bucket_bytes=8 << 20, model=None, task=None,
+            mode="shard"):
     from paper_2110_05722_b200.dist import DataParallel
     run = RunConfig() if model is None else RunConfig(model=model,
                                                       train=TrainConfig(p_drop=0.1,
                                                                         batch_tokens=4096))
     run.train.p_drop = 0.1
     run.train.cuda_graphs = graphs
-    dp = DataParallel(bucket_bytes=bucket_bytes, force=force)
+    dp = DataParallel(bucket_bytes=bucket_bytes, force=force, mode=mode)
     eng = TrainingEngine(run, task=task, dp=dp)
     eng.setup_arena()
     ms = [eng.train_step(s) for s in range(steps)]
     return eng, ms
 
 
-@pytest.mark.parametrize("bucket_bytes", [1 << 10, 8 << 20])
-def test_dp_exchange_one_rank_matches_local_step(bucket_bytes):
-    """The overlapped exchange (per-bucket narrow + NCCL all-reduce + non-finite
-    count on the comm stream, one-rank communicator) inside the captured graph
-    gives the local step's result: losses equal, parameters equal up to the
-    embedding-scatter atomics."""
+@pytest.mark.parametrize("bucket_bytes,mode", [(1 << 10, "shard"), (8 << 20, "shard"),
+                                               (1 << 10, "allreduce"), (8 << 20, "allreduce")])
+def test_dp_exchange_one_rank_matches_local_step(bucket_bytes, mode):
+    """The overlapped exchange (per-bucket fp32 finish + NCCL reduce-scatter or
+    all-reduce + narrow + non-finite count on the comm stream, then the sharded
+    Adam and the params16 all-gather; one-rank communicator) inside the captured
+    graph gives the local step's result: losses equal, parameters equal up to
+    the embedding-scatter atomics."""
     e1, m1 = _dp_run(False, True, 8)
-    e2, m2 = _dp_run(True, True, 8, bucket_bytes)
+    e2, m2 = _dp_run(True, True, 8, bucket_bytes, mode=mode)
     assert e2._graphs and e2.dp.comm is not None
     for a, b in zip(m1, m2):
         assert a.tokens == b.tokens and a.skipped == b.skipped
@@ -309,6 +312,7 @@ def test_dp_exchange_tbase_graph_step():
     from paper_2110_05722_b200.data import FixedShapeTask
     e1, m1 = _dp_run(False, True, 4, model=transformer_base(), task=FixedShapeTask(64, 64, 32000))
     e2, m2 = _dp_run(True, True, 4, model=transformer_base(), task=FixedShapeTask(64, 64, 32000))
+    assert e2.dp.sharded and e2._shard_spans
     for a, b in zip(m1, m2):
         assert abs(a.loss - b.loss) <= 1e-3 * abs(a.loss)
     p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
