@@ -459,8 +459,12 @@ def run_ours(args):
                                        "alpha 0.1, Adam",
                            "global_batch": world * B * L, "seq_len": L,
                            "parallelism": f"dp{world}",
-                           "exchange": ("bucketed fp16 NCCL all-reduce overlapped with backward, "
-                                        "captured in the step graph") if dp.active else "none",
+                           "exchange": (("fp32 bucket reduce-scatter (NCCL), narrow + Adam on the "
+                                         "rank's 1/N chunks, in-place params16 all-gather"
+                                         if dp.sharded else
+                                         "fp32 bucket all-reduce (NCCL), narrow after the sum")
+                                        + ", overlapped with backward, captured in the step graph"
+                                        ) if dp.active else "none",
                            "l2": "inputs larger than L2 (~1.5 GB touched per step > 126 MB)"},
                 "clocks": clk.summary(),
                 "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": io.h2d_bytes,

@@ -227,7 +227,10 @@ class DataParallel:
         """Create the native communicator and the comm stream (CUDA only)."""
         if self.active and self.comm is None:
             self.comm = NcclComm(self.rank, self.world, device, self.group)
-            self.comm_stream = torch.cuda.Stream(device=device, priority=-100)
+            # high priority by default so the exchange keeps pace with backward at
+            # N > 1 (LS2_COMM_PRIORITY=low lets it fill gaps instead)
+            low = os.environ.get("LS2_COMM_PRIORITY", "high") == "low"
+            self.comm_stream = torch.cuda.Stream(device=device, priority=0 if low else -100)
         return self
 
     def buckets(self, n: int, elem_bytes: int = 2):

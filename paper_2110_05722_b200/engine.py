@@ -342,14 +342,21 @@ class TrainingEngine:
             self._buckets.append((start, stop))
             self._shard_spans.append((off, c))
 
-    def _spans_table(self, spans) -> torch.Tensor:
+    def _spans_table(self, spans):
+        """(device table, count, longest) of the rank's chunks cut into pieces of
+        near-equal length, one CTA each: the chunks differ in size (the last
+        bucket holds the whole token table), and one grid row per chunk would
+        leave most CTAs idle while the largest chunk finishes."""
         key = tuple(spans)
-        tab = self._span_tables.get(key)
-        if tab is None:
-            tab = torch.tensor([x for sp in spans for x in sp], dtype=torch.int64,
+        hit = self._span_tables.get(key)
+        if hit is None:
+            total = sum(c for _, c in spans)
+            piece = max(2048, -(-total // (148 * 8) // 2048) * 2048)
+            rows = [(o + k, min(piece, c - k)) for o, c in spans for k in range(0, c, piece)]
+            tab = torch.tensor([x for sp in rows for x in sp], dtype=torch.int64,
                                device=self.device)
-            self._span_tables[key] = tab
-        return tab
+            hit = self._span_tables[key] = (tab, len(rows), piece)
+        return hit
 
     def _dp_update(self, loss_ptr):
         """Data-parallel optimizer step on the comm stream, after the last bucket.
@@ -363,12 +370,22 @@ class TrainingEngine:
                 self._optimizer(0, ws.n_elements, loss_ptr, st)
                 return
             dp.allreduce_count(self._nonfinite, stream=cs)
-            spans = [sp for sp in self._shard_spans if sp[1] > 0]
-            if self.optim.algorithm == "adam" and spans:
+            spans = []
+            for off, c in sorted(sp for sp in self._shard_spans if sp[1] > 0):
+                if spans and spans[-1][0] + spans[-1][1] == off:      # adjacent (world 1)
+                    spans[-1] = (spans[-1][0], spans[-1][1] + c)
+                else:
+                    spans.append((off, c))
+            if len(spans) == 1:                                       # one contiguous range
+                self._optimizer(spans[0][0], spans[0][1], loss_ptr, st)
+                spans = []
+            if not spans:
+                pass
+            elif self.optim.algorithm == "adam":
+                tab, npieces, piece = self._spans_table(spans)
                 _lib.call("ls2_adam_spans", ws.params16.data_ptr(), ws.grads16.data_ptr(),
-                          ws.m32.data_ptr(), ws.v32.data_ptr(),
-                          self._spans_table(spans).data_ptr(), len(spans),
-                          max(c for _, c in spans), self._opt.hyper.data_ptr(),
+                          ws.m32.data_ptr(), ws.v32.data_ptr(), tab.data_ptr(), npieces, piece,
+                          self._opt.hyper.data_ptr(),
                           self._opt.bc.data_ptr(), bias_correction_rows(self._opt.bc), 0,
                           self._applied_dev.data_ptr(), self._nonfinite.data_ptr(), loss_ptr, st)
             else:

@@ -50,11 +50,22 @@ class _Converter:
                 setattr(y, f.name, self(getattr(x, f.name)))
             return y
         if hasattr(x, "keep") and hasattr(x, "p") and hasattr(x, "bitmask"):   # DropoutMask
-            y = copy.copy(x)
-            y.keep = self(x.keep)
-            y.bits = None
-            return y
+            return _HostMask(x, self(x.keep))
         return x
+
+
+class _HostMask:
+    """A DropoutMask seen from the test: numpy `keep`; handed back to the mirror
+    it unwraps to the device mask it came from."""
+
+    def __init__(self, dev_mask, keep):
+        self._ls2_orig = dev_mask
+        self.keep = keep
+        self.p = dev_mask.p
+
+
+def _unwrap(v):
+    return getattr(v, "_ls2_orig", v)
 
 
 def wrap(fn):
@@ -65,6 +76,8 @@ def wrap(fn):
                 t = torch.from_numpy(np.ascontiguousarray(v)).cuda()
                 kwargs[k] = t
                 back.append((v, t))
+        args = tuple(_unwrap(a) for a in args)
+        kwargs = {k: _unwrap(v) for k, v in kwargs.items()}
         res = fn(*args, **kwargs)
         conv = _Converter()
         for arr, t in back:

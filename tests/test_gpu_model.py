@@ -251,6 +251,38 @@ def test_checkpoint_resume_bit_exact(tmp_path):
     assert np.abs(pa - pb).max() <= 2e-3     # atomics only
 
 
+def test_resume_from_a_reference_written_checkpoint(tmp_path):
+    """Interop with F/checkpoint.py + F/engine.py:189-208: the reference engine's own
+    LSF2 checkpoint of the default job after 40 steps (tests/golden/make_golden_ckpt.py)
+    restores into this engine, which then continues the reference's uninterrupted
+    trajectory (same batches, same dropout masks; fp16 activations here, fp32 there);
+    and this engine's checkpoint carries the reference's tensor names, dtypes and
+    shapes, so the reference can resume from it (T/test_data_cli.py:262-282)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2110_05722_b200.checkpoint import load_checkpoint
+    ref = np.load(os.path.join(GOLDEN, "ref_ckpt_tail.npz"))
+    path = os.path.join(GOLDEN, "ref_ckpt_step40.lsf2")
+    run = RunConfig()
+    run.train.p_drop = 0.1
+    eng = TrainingEngine(run)
+    eng.setup_arena()
+    assert eng.restore(path) == 40 and eng.applied_steps == 40
+    _, want_t = load_checkpoint(path)
+    assert np.array_equal(H(eng.ws.params16).view(np.uint16), want_t["params16"].view(np.uint16))
+    losses = np.array([eng.train_step(s).loss for s in range(40, 48)])
+    assert np.abs(losses - ref["losses"]).max() <= 5e-3 * ref["losses"].max(), (losses, ref["losses"])
+    assert eng.applied_steps == int(ref["applied"][0])
+    p, q = H(eng.ws.params16).astype(np.float32), ref["params16"].astype(np.float32)
+    assert np.linalg.norm(p - q) <= 1e-2 * np.linalg.norm(q)
+    eng.save(str(tmp_path / "ours.lsf2"), 48)
+    step, ours = load_checkpoint(str(tmp_path / "ours.lsf2"))
+    assert step == 48 and list(ours) == list(want_t)
+    for k in want_t:
+        assert ours[k].dtype == want_t[k].dtype and ours[k].shape == want_t[k].shape, k
+    assert float(ours["applied_steps"][0]) == 48.0
+
+
 def test_tbase_step_runs_and_is_finite():
     from paper_2110_05722_b200.config import transformer_base
     from paper_2110_05722_b200.data import FixedShapeTask

@@ -163,6 +163,33 @@ def test_checkpoint_roundtrip(tmp_path):
         load_checkpoint(str(tmp_path / "b.bin"))
 
 
+def test_checkpoint_bytes_identical_to_the_reference_writer(tmp_path):
+    """tests/golden/ref_ckpt_format.lsf2 was written by the reference's
+    save_checkpoint (F/checkpoint.py:27-42) from fixed tensors (f16/f32, ranks 0-3,
+    an empty tensor): this writer produces the same bytes and this reader
+    recovers the same tensors; the reference engine's own checkpoint parses too."""
+    import importlib.util
+    from conftest import GOLDEN
+    from paper_2110_05722_b200.checkpoint import load_checkpoint, save_checkpoint
+    spec = importlib.util.spec_from_file_location(
+        "make_golden_ckpt", os.path.join(GOLDEN, "make_golden_ckpt.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    tensors = gen.format_tensors()
+    ref_path = os.path.join(GOLDEN, "ref_ckpt_format.lsf2")
+    save_checkpoint(str(tmp_path / "ours.lsf2"), 123456789, tensors)
+    assert (tmp_path / "ours.lsf2").read_bytes() == open(ref_path, "rb").read()
+    step, got = load_checkpoint(ref_path)
+    assert step == 123456789 and list(got) == [n for n, _ in tensors]
+    for name, arr in tensors:
+        assert got[name].dtype == arr.dtype and got[name].shape == arr.shape
+        assert got[name].tobytes() == arr.tobytes()
+    step, eng = load_checkpoint(os.path.join(GOLDEN, "ref_ckpt_step40.lsf2"))
+    assert step == 40 and list(eng) == ["params16", "moments_m", "moments_v", "applied_steps"]
+    assert eng["params16"].dtype == np.float16 and eng["moments_v"].dtype == np.float32
+    assert eng["params16"].size == eng["moments_m"].size == eng["moments_v"].size
+
+
 def test_oracle_never_imports_product():
     src = open(os.path.join(ROOT, "oracle", "lsport.py")).read()
     mods = re.findall(r"^\s*(?:from|import)\s+([\w.]+)", src, re.M)

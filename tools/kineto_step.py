@@ -22,6 +22,9 @@ def main():
     ap.add_argument("--top", type=int, default=45)
     ap.add_argument("--model", default="tbase", choices=["tbase", "tbig"])
     ap.add_argument("--shape", default=None, help="BxL batch shape (e.g. 512x8, a WMT bucket)")
+    ap.add_argument("--dp", default=None, choices=["shard", "allreduce"],
+                    help="one-rank forced data-parallel exchange in the given mode")
+    ap.add_argument("--trace", default=None, help="also write a chrome trace here")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -36,7 +39,11 @@ def main():
     run = RunConfig(model=transformer_base(V, 256) if a.model == "tbase" else
                     transformer_big(V, 256),
                     train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L))
-    eng = TrainingEngine(run, task=FixedShapeTask(B, L, V, seed=17))
+    dp = None
+    if a.dp:
+        from paper_2110_05722_b200.dist import DataParallel
+        dp = DataParallel(force=True, mode=a.dp)
+    eng = TrainingEngine(run, task=FixedShapeTask(B, L, V, seed=17), dp=dp)
     eng.setup_arena()
     for s in range(4):
         eng.train_step(s)
@@ -53,6 +60,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
     step_ms = e0.elapsed_time(e1) / a.steps
+    if a.trace:
+        os.makedirs(os.path.dirname(a.trace) or ".", exist_ok=True)
+        prof.export_chrome_trace(a.trace)
     agg = collections.defaultdict(lambda: [0, 0.0])
     for ev in prof.events():
         if ev.device_type.name != "CUDA":
