@@ -227,9 +227,11 @@ class DataParallel:
         """Create the native communicator and the comm stream (CUDA only)."""
         if self.active and self.comm is None:
             self.comm = NcclComm(self.rank, self.world, device, self.group)
-            # high priority by default so the exchange keeps pace with backward at
-            # N > 1 (LS2_COMM_PRIORITY=low lets it fill gaps instead)
-            low = os.environ.get("LS2_COMM_PRIORITY", "high") == "low"
+            # default priority: the exchange's kernels take SMs the backward leaves
+            # free instead of pre-empting it (measured on one rank: high priority
+            # slowed the backward by more than the exchange's own time;
+            # LS2_COMM_PRIORITY=high restores it)
+            low = os.environ.get("LS2_COMM_PRIORITY", "low") == "low"
             self.comm_stream = torch.cuda.Stream(device=device, priority=0 if low else -100)
         return self
 

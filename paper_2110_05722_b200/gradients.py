@@ -10,6 +10,7 @@ and the attention 1/sqrt(hd) into the same pass.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -94,7 +95,9 @@ def layernorm_backward(dy, x, w, cache: LNCache, out=None, dres=None, dw_out=Non
     m = xt.shape[-1]
     r = xt.numel() // m
     pdt = compute_dtype(dy, x, w)
-    mu, sg = cache.mu, cache.sigma
+    # host (numpy) statistics keep their precision: f64 stats stay f64
+    mu, sg = (v if isinstance(v, torch.Tensor) else torch.as_tensor(np.asarray(v))
+              for v in (cache.mu, cache.sigma))
     tstat = mu.dtype if mu.dtype in (torch.float32, torch.float64) else torch.float32
     mu = dev(mu, tstat).reshape(-1)
     sg = dev(sg, tstat).reshape(-1)
