@@ -131,6 +131,7 @@ class TrainingEngine:
         self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
         self._xplan = None
         self._span_tables: dict = {}
+        self.merge_spans = True          # tests set False to run the per-chunk update on 1 rank
         if self.dp.active:
             self.dp.setup_device(self.device)
             self._xplan = self.dp.exchange_plan(
@@ -376,7 +377,7 @@ class TrainingEngine:
                     spans[-1] = (spans[-1][0], spans[-1][1] + c)
                 else:
                     spans.append((off, c))
-            if len(spans) == 1:                                       # one contiguous range
+            if len(spans) == 1 and self.merge_spans:                  # one contiguous range
                 self._optimizer(spans[0][0], spans[0][1], loss_ptr, st)
                 spans = []
             if not spans:

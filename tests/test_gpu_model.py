@@ -296,7 +296,7 @@ def test_tbase_step_runs_and_is_finite():
 
 
 def _dp_run(force: bool, graphs: bool, steps: int, bucket_bytes=8 << 20, model=None, task=None,
-            mode="shard"):
+            mode="shard", merge=True):
     from paper_2110_05722_b200.dist import DataParallel
     run = RunConfig() if model is None else RunConfig(model=model,
                                                       train=TrainConfig(p_drop=0.1,
@@ -305,21 +305,25 @@ def _dp_run(force: bool, graphs: bool, steps: int, bucket_bytes=8 << 20, model=N
     run.train.cuda_graphs = graphs
     dp = DataParallel(bucket_bytes=bucket_bytes, force=force, mode=mode)
     eng = TrainingEngine(run, task=task, dp=dp)
+    eng.merge_spans = merge
     eng.setup_arena()
     ms = [eng.train_step(s) for s in range(steps)]
     return eng, ms
 
 
-@pytest.mark.parametrize("bucket_bytes,mode", [(1 << 10, "shard"), (8 << 20, "shard"),
-                                               (1 << 10, "allreduce"), (8 << 20, "allreduce")])
-def test_dp_exchange_one_rank_matches_local_step(bucket_bytes, mode):
+@pytest.mark.parametrize("bucket_bytes,mode,merge", [(1 << 10, "shard", True), (8 << 20, "shard", True),
+                                                     (1 << 10, "shard", False),
+                                                     (8 << 20, "shard", False),
+                                                     (1 << 10, "allreduce", True),
+                                                     (8 << 20, "allreduce", True)])
+def test_dp_exchange_one_rank_matches_local_step(bucket_bytes, mode, merge):
     """The overlapped exchange (per-bucket fp32 finish + NCCL reduce-scatter or
     all-reduce + narrow + non-finite count on the comm stream, then the sharded
     Adam and the params16 all-gather; one-rank communicator) inside the captured
     graph gives the local step's result: losses equal, parameters equal up to
     the embedding-scatter atomics."""
     e1, m1 = _dp_run(False, True, 8)
-    e2, m2 = _dp_run(True, True, 8, bucket_bytes, mode=mode)
+    e2, m2 = _dp_run(True, True, 8, bucket_bytes, mode=mode, merge=merge)
     assert e2._graphs and e2.dp.comm is not None
     for a, b in zip(m1, m2):
         assert a.tokens == b.tokens and a.skipped == b.skipped

@@ -394,6 +394,50 @@ def test_adam_bit_exact_random_states():
         assert np.array_equal(H(ws.m32), m) and np.array_equal(H(ws.v32), v), trial
 
 
+def test_adam_spans_bit_exact_and_leaves_the_rest():
+    """ls2_adam_spans (the sharded optimizer's update of this rank's chunks): on
+    random disjoint spans — ragged lengths, unaligned starts, one long span among
+    short ones — every element inside a span equals the plain Adam update bit for
+    bit and every element outside is untouched."""
+    from paper_2110_05722_b200 import _lib
+    from paper_2110_05722_b200.trainer import _state, bias_correction_rows
+    rng = np.random.default_rng(11)
+    n = 300_000
+    p0 = (rng.normal(size=n)).astype(np.float32)
+    ws = T.workspace_pack([("p", p0)], "adam")
+    g16 = O.to_half(rng.normal(size=n) * 0.1)
+    m0 = (rng.normal(size=n) * 0.1).astype(np.float32)
+    v0 = rng.uniform(0.0, 0.2, size=n).astype(np.float32)
+    ws.grads16.copy_(C(g16))
+    ws.m32.copy_(C(m0))
+    ws.v32.copy_(C(v0))
+    cuts = np.sort(rng.choice(np.arange(1, n), 40, replace=False))
+    edges = np.concatenate([[0], cuts, [n]])
+    spans = [(int(a), int(b - a)) for a, b in zip(edges[:-1], edges[1:])][::2]   # every other
+    spans.append((int(edges[-2]) if len(edges) % 2 else 0, 0))                  # an empty span
+    cfg = T.OptimConfig(lr=1e-3, weight_decay=0.01, loss_scale=4.0)
+    st = _state(ws, cfg)
+    tab = torch.tensor([x for sp in spans for x in sp], dtype=torch.int64, device="cuda")
+    longest = max(c for _, c in spans)
+    _lib.call("ls2_adam_spans", ws.params16.data_ptr(), ws.grads16.data_ptr(), ws.m32.data_ptr(),
+              ws.v32.data_ptr(), tab.data_ptr(), len(spans), longest, st.hyper.data_ptr(),
+              st.bc.data_ptr(), bias_correction_rows(st.bc), 3, None, None, None,
+              _lib.stream_handle())
+    p16, m, v = O.to_half(p0), m0.copy(), v0.copy()
+    want_p, want_m, want_v = p16.copy(), m.copy(), v.copy()
+    for o, c in spans:
+        if c:
+            O.adam_flat(want_p[o:o + c], g16[o:o + c], want_m[o:o + c], want_v[o:o + c],
+                        lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.01, loss_scale=4.0, t=3)
+    assert np.array_equal(H(ws.params16).view(np.uint16), want_p.view(np.uint16))
+    assert np.array_equal(H(ws.m32), want_m) and np.array_equal(H(ws.v32), want_v)
+    inside = np.zeros(n, bool)
+    for o, c in spans:
+        inside[o:o + c] = True
+    assert not np.array_equal(want_p[inside], p16[inside])            # the spans did move
+    assert np.array_equal(H(ws.params16)[~inside].view(np.uint16), p16[~inside].view(np.uint16))
+
+
 # --- gemm -----------------------------------------------------------------------------
 
 @pytest.mark.parametrize("dt,tol", [(np.float64, 1e-12), (np.float32, 1e-5), (np.float16, 2e-2)])
