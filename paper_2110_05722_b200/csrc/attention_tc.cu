@@ -54,6 +54,7 @@ struct Args {
   float dscale;                      // scale itself (dS = P (dP - rowsum) * scale)
   float2* stats;                     // [B][H][Lq] (row max in the log2 domain, 1 / row sum)
   uint32_t id_s, id64_km, id64_mm, id_cs;   // instruction descriptors (M, N, A / B majors)
+  uint32_t id128_pv, id128_mm;              // M = 128, N = 64: A K-major / A MN-major, B MN-major
   double *csq, *csk, *csv;
   int64_t ldcsq, ldcsk, ldcsv;
   unsigned long long* trace;         // optional phase timestamps [grid][16] (ls2_attention_tc_trace)
@@ -671,6 +672,403 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// 64 < L <= 128 (T-big, BERT-128): one (batch, head) per CTA as ONE 128-row
+// tile.  S = Q K^T and dP = dO V^T are the same M = 128 x N = 128 chains as
+// above; P, dS live in a [128 queries x 128 keys] buffer of two 64-key chunks
+// (16 KB apart), so O = P V, dQ = dS K are K = 128 chains over the chunks
+// (K-major) and dV = P^T dO, dK = dS^T Q read the same buffer MN-major.  Each
+// thread owns one row (TMEM lane) and one 64-column half of S / dP.  The
+// backward computes dV first and then reuses P's buffer for dS (96 KB of
+// shared memory: two CTAs per SM).  Bias partials: column sums of the fp32
+// dQ / dK / dV (warp reduce-scatter, then the four row quadrants in order).
+// ---------------------------------------------------------------------------
+constexpr size_t kFwd128Smem = 5 * kPair + 1024;    // Q, K, V, P (2 chunks)
+constexpr size_t kBwd128Smem = 6 * kPair + 1024;    // Q, K, V, dO, P|dS (2 chunks)
+
+// rows [L, 128) of a 128-row region: zero (no TMA box writes them)
+__device__ __forceinline__ void zero_rows128(uint8_t* pair, int L) {
+  if (L < 64) {
+    zero_tail(pair, L);
+    zero_tail(pair + kTile, 0);
+  } else {
+    zero_tail(pair + kTile, L - 64);
+  }
+}
+
+// K = 128 chain: A is the two-chunk P / dS buffer (K-major: kdesc per chunk, or
+// MN-major with its 64-wide M blocks 16 KB apart), B an MN-major 128-row tile
+template <int AM>
+__device__ __forceinline__ void mma_k128(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc) {
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint64_t da = AM == KM ? kdesc(a + (kk >> 2) * kPair, kk & 3) : mdesc_bd(a, kk);
+    const uint64_t db = mdesc(b, kk);
+    const uint32_t acc = kk ? 1u : 0u;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+
+struct Row128 {
+  int m, q, half, idx, b, h;
+  bool ok;
+  int lo, hi;     // unmasked keys relative to this thread's 64 columns
+};
+
+__device__ __forceinline__ float partner128(float* buf, const Row128& r, float v) {
+  buf[r.half * 128 + r.idx] = v;
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + r.q) : "memory");
+  return buf[(r.half ^ 1) * 128 + r.idx];
+}
+
+__device__ __forceinline__ Row128 row128(const Args& a) {
+  Row128 r;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  r.q = warp & 3;
+  r.half = warp >> 2;
+  r.idx = r.q * 32 + lane;
+  r.m = r.idx;
+  r.b = blockIdx.x / a.H;
+  r.h = blockIdx.x % a.H;
+  r.ok = r.m < a.Lq;
+  int64_t len = a.Lk;
+  if (a.mask == LS2_MASK_PADDING) len = __ldg(a.lens + r.b);
+  int n = len < a.Lk ? (int)len : a.Lk;
+  if (a.mask == LS2_MASK_CAUSAL) n = r.m + 1 < n ? r.m + 1 : n;
+  r.lo = -64 * r.half;
+  r.hi = r.ok ? n - 64 * r.half : r.lo;
+  return r;
+}
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&x)[64]) {
+  float a[32], b[32];
+  tmem_ld32(taddr, a);
+  tmem_ld32(taddr + 32, b);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] = a[i];
+    x[32 + i] = b[i];
+  }
+}
+
+// column sums over the CTA's 128 rows of a [128 x 64] fp32 TMEM result whose
+// thread holds 32 columns (half) of one row: warp reduce-scatter (lane l ends
+// with column l of its half), then the four row quadrants in order -> f64 row
+// `b` of the partial buffer
+__device__ __forceinline__ void colsum128(float (&x)[32], int q, int half, float* red,
+                                          double* out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? x[i] : x[i + o];
+      const float keep = up ? x[i + o] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  red[q * 64 + 32 * half + lane] = x[0];
+  __syncthreads();
+  if (threadIdx.x < 64 && out) {
+    const int c = threadIdx.x;
+    out[c] = (double)(((red[c] + red[64 + c]) + red[128 + c]) + red[192 + c]);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads, 2) attn_tc128_fwd_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
+    const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* Qs = sm;                  // 128 rows; doubles as the O staging
+  uint8_t* Ks = sm + kPair;
+  uint8_t* Vs = sm + 2 * kPair;
+  uint8_t* Pb = sm + 3 * kPair;      // [128 queries x 128 keys]: chunk c = keys 64c ..
+  __shared__ __align__(8) uint64_t bar_qk, bar_v, bar_s, bar_o;
+  __shared__ uint32_t tmem_base;
+  __shared__ float xm[256], xz[256];
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x / a.H, h = blockIdx.x % a.H;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mq)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
+    mbar_init(&bar_qk, 1);
+    mbar_init(&bar_v, 1);
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_qk, (uint32_t)((a.Lq + a.Lk) * 128));
+    tma_load_3d(Qs, &mq, h * 64, 0, b, &bar_qk);
+    tma_load_3d(Ks, &mk, h * 64, 0, b, &bar_qk);
+    mbar_expect_tx(&bar_v, (uint32_t)(a.Lk * 128));
+    tma_load_3d(Vs, &mv, h * 64, 0, b, &bar_v);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+        sptr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  zero_rows128(Qs, a.Lq);
+  zero_rows128(Ks, a.Lk);
+  zero_rows128(Vs, a.Lk);
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_base;
+  Row128 r = row128(a);
+  if (threadIdx.x == 0) {
+    mbar_wait(&bar_qk, 0);
+    tc_after();
+    mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Ks), a.id_s);      // S (cols 0-127)
+    commit(&bar_s);
+  }
+  __syncwarp();
+  const uint32_t tlane = tmem + ((uint32_t)(32 * r.q) << 16);
+  mbar_wait(&bar_s, 0);
+  tc_after();
+  float x[64];
+  tmem_ld64(tlane + 64 * r.half, x);
+  float m = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    x[c] = (c >= r.lo && c < r.hi) ? __fmul_rn(x[c], a.scale) : -INFINITY;
+    m = fmaxf(m, x[c]);
+  }
+  m = fmaxf(m, partner128(xm, r, m));
+  float z = 0.f;
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    x[c] = x[c] == -INFINITY ? 0.f : ex2(__fsub_rn(x[c], m));
+    z += x[c];
+  }
+  z += partner128(xz, r, z);
+  const float iz = z > 0.f ? 1.f / z : 0.f;
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      w[j] = pack_h2(__fmul_rn(x[32 * sub + 2 * j], iz), __fmul_rn(x[32 * sub + 2 * j + 1], iz));
+    st_cols(Pb + r.half * kPair, r.m, sub, w);
+  }
+  if (r.ok && r.half == 0) a.stats[((int64_t)r.b * a.H + r.h) * a.Lq + r.m] = make_float2(m, iz);
+  fence_async_smem();
+  tc_before();
+  __syncthreads();                   // P complete, S read
+  if (threadIdx.x == 0) {
+    tc_after();
+    mbar_wait(&bar_v, 0);
+    mma_k128<KM>(tmem, sptr(Pb), sptr(Vs), a.id128_pv);      // O = P V (cols 0-63)
+    commit(&bar_o);
+  }
+  __syncwarp();
+  mbar_wait(&bar_o, 0);
+  tc_after();
+  {
+    float o[32];
+    tmem_ld32(tlane + 32 * r.half, o);
+    st_cols_f(Qs, r.m, r.half, o);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mo, h * 64, 0, b, Qs);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) attn_tc128_bwd_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+    const __grid_constant__ CUtensorMap mdq, const __grid_constant__ CUtensorMap mdk,
+    const __grid_constant__ CUtensorMap mdv, const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* Qs = sm;                  // Q, K, V double as dQ, dK, dV staging
+  uint8_t* Ks = sm + kPair;
+  uint8_t* Vs = sm + 2 * kPair;
+  uint8_t* Os = sm + 3 * kPair;      // dO
+  uint8_t* Pb = sm + 4 * kPair;      // P, then dS: [128 queries x 128 keys], two chunks
+  __shared__ __align__(8) uint64_t bar_ld, bar_1, bar_2, bar_3;
+  __shared__ uint32_t tmem_base;
+  __shared__ float xr[256];
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x / a.H, h = blockIdx.x % a.H;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mq)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
+    mbar_init(&bar_ld, 1);
+    mbar_init(&bar_1, 1);
+    mbar_init(&bar_2, 1);
+    mbar_init(&bar_3, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_ld, (uint32_t)(2 * (a.Lq + a.Lk) * 128));
+    tma_load_3d(Qs, &mq, h * 64, 0, b, &bar_ld);
+    tma_load_3d(Ks, &mk, h * 64, 0, b, &bar_ld);
+    tma_load_3d(Os, &mdo, h * 64, 0, b, &bar_ld);
+    tma_load_3d(Vs, &mv, h * 64, 0, b, &bar_ld);
+  }
+  if (warp == 1) {   // S (0-127), dP (128-255); then dV (0-63), dQ (64-127), dK (128-191)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        sptr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  zero_rows128(Qs, a.Lq);
+  zero_rows128(Os, a.Lq);
+  zero_rows128(Ks, a.Lk);
+  zero_rows128(Vs, a.Lk);
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_base;
+  Row128 r = row128(a);
+  float2 st = make_float2(0.f, 0.f);
+  if (r.ok) st = __ldg(a.stats + ((int64_t)r.b * a.H + r.h) * a.Lq + r.m);
+  if (threadIdx.x == 0) {
+    mbar_wait(&bar_ld, 0);
+    tc_after();
+    mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Ks), a.id_s);          // S
+    mma128<KM, KM, 4>(tmem + 128, sptr(Os), sptr(Vs), a.id_s);    // dP
+    commit(&bar_1);
+  }
+  __syncwarp();
+  const uint32_t tlane = tmem + ((uint32_t)(32 * r.q) << 16);
+  mbar_wait(&bar_1, 0);
+  tc_after();
+  uint32_t pw[32];                   // P of this half row, fp16 pairs
+  {
+    float x[64];
+    tmem_ld64(tlane + 64 * r.half, x);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float p2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 2 * j + e;
+        p2[e] = (c >= r.lo && c < r.hi)
+                    ? __fmul_rn(ex2(__fsub_rn(__fmul_rn(x[c], a.scale), st.x)), st.y)
+                    : 0.f;
+      }
+      pw[j] = pack_h2(p2[0], p2[1]);
+    }
+  }
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = pw[16 * sub + j];
+    st_cols(Pb + r.half * kPair, r.m, sub, w);
+  }
+  uint32_t dw[32];
+  {
+    float x[64];
+    tmem_ld64(tlane + 128 + 64 * r.half, x);                  // dP
+    float rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float2 p = unpack_h2(pw[j]);
+      rs += x[2 * j] * p.x + x[2 * j + 1] * p.y;
+    }
+    rs += partner128(xr, r, rs);
+    const float ds = a.dscale;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float2 p = unpack_h2(pw[j]);
+      dw[j] = pack_h2(p.x * (x[2 * j] - rs) * ds, p.y * (x[2 * j + 1] - rs) * ds);
+    }
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();                   // P complete, S and dP read
+  if (threadIdx.x == 0) {
+    tc_after();
+    mma_k128<MN>(tmem, sptr(Pb), sptr(Os), a.id128_mm);       // dV = P^T dO (cols 0-63)
+    commit(&bar_2);
+  }
+  __syncwarp();
+  mbar_wait(&bar_2, 0);              // P no longer read: its buffer takes dS
+  tc_after();
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = dw[16 * sub + j];
+    st_cols(Pb + r.half * kPair, r.m, sub, w);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_after();
+    mma_k128<KM>(tmem + 64, sptr(Pb), sptr(Ks), a.id128_pv);  // dQ = dS K
+    mma_k128<MN>(tmem + 128, sptr(Pb), sptr(Qs), a.id128_mm); // dK = dS^T Q
+    commit(&bar_3);
+  }
+  __syncwarp();
+  __shared__ float red[256];
+  {   // dV (row = key) -> V's tile (V dead since dP), bias partial, store
+    float x[32];
+    tmem_ld32(tlane + 32 * r.half, x);
+    st_cols_f(Vs, r.m, r.half, x);
+    colsum128(x, r.q, r.half, red, a.csv ? a.csv + (int64_t)b * a.ldcsv + h * 64 : nullptr);
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mdv, h * 64, 0, b, Vs);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  mbar_wait(&bar_3, 0);              // dQ, dK done: Q, K dead
+  tc_after();
+  {
+    float x[32];
+    tmem_ld32(tlane + 64 + 32 * r.half, x);
+    st_cols_f(Qs, r.m, r.half, x);
+    colsum128(x, r.q, r.half, red, a.csq ? a.csq + (int64_t)b * a.ldcsq + h * 64 : nullptr);
+  }
+  {
+    float x[32];
+    tmem_ld32(tlane + 128 + 32 * r.half, x);
+    st_cols_f(Ks, r.m, r.half, x);
+    colsum128(x, r.q, r.half, red, a.csk ? a.csk + (int64_t)b * a.ldcsk + h * 64 : nullptr);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mdq, h * 64, 0, b, Qs);
+    tma_store_3d(&mdk, h * 64, 0, b, Ks);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
 // [B][L][ld] fp16 operand, columns [0, cols) from `base`: boxes of 64 columns x L
 // rows x G sequences, 128-byte swizzle, zero fill past L / B
 bool make_map3(CUtensorMap* m, const void* base, int64_t cols, int64_t L, int64_t B, int64_t ld,
@@ -707,7 +1105,8 @@ int fill_args(Args& a, int64_t batch, int64_t heads, int64_t lq, int64_t lk, int
   a.H = (int)heads;
   a.Lq = (int)lq;
   a.Lk = (int)lk;
-  a.G = (int)(64 / (lq > lk ? lq : lk));
+  const int64_t lmax = lq > lk ? lq : lk;
+  a.G = lmax > 64 ? 1 : (int)(64 / lmax);      // L > 64: one 128-row tile per (b, h)
   a.B = (int)batch;
   a.ntiles = (int)(heads * ((batch + a.G - 1) / a.G));
   a.mask = mask_kind;
@@ -719,6 +1118,8 @@ int fill_args(Args& a, int64_t batch, int64_t heads, int64_t lq, int64_t lk, int
   a.id64_km = idesc(false, true, 64, 64);
   a.id64_mm = idesc(true, true, 64, 64);
   a.id_cs = idesc(true, false, 16);
+  a.id128_pv = idesc(false, true, 64, 128);
+  a.id128_mm = idesc(true, true, 64, 128);
   a.csq = a.csk = a.csv = nullptr;
   a.ldcsq = a.ldcsk = a.ldcsv = 0;
   a.trace = g_trace;
@@ -744,7 +1145,7 @@ int ls2_attention_tc_supported(int64_t lq, int64_t lk, int64_t hd, int dtype) {
     const char* e = std::getenv("LS2_ATTN_TC");
     return e && e[0] == '0';
   }();
-  return !off && dtype == LS2_F16 && hd == 64 && lq >= 1 && lk >= 1 && lq <= 64 && lk <= 64;
+  return !off && dtype == LS2_F16 && hd == 64 && lq >= 1 && lk >= 1 && lq <= 128 && lk <= 128;
 }
 
 int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
@@ -752,7 +1153,7 @@ int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
                          int64_t heads, int64_t lq, int64_t lk, int64_t hd, int mask_kind,
                          const int64_t* lens, double scale, void* stream) {
   if (!ls2_attention_tc_supported(lq, lk, hd, LS2_F16))
-    return fail(LS2_ERR_SHAPE, "attention_tc_fwd: needs fp16, hd == 64, L <= 64");
+    return fail(LS2_ERR_SHAPE, "attention_tc_fwd: needs fp16, hd == 64, L <= 128");
   if (mask_kind == LS2_MASK_PADDING && !lens) return fail(LS2_ERR_SHAPE, "attention_tc: no lens");
   if (mask_kind == LS2_MASK_DENSE) return fail(LS2_ERR_SHAPE, "attention_tc: dense masks unsupported");
   if (mask_kind == LS2_MASK_CAUSAL && lq != lk) return fail(LS2_ERR_SHAPE, "attention_tc: causal needs lq == lk");
@@ -769,6 +1170,17 @@ int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
       !atc::make_map3(&mv, v, cols, lk, batch, ldv, a.G) ||
       !atc::make_map3(&mo, o, cols, lq, batch, ldo, a.G))
     return fail(LS2_ERR_CUDA, "attention_tc_fwd: cuTensorMapEncodeTiled failed");
+  if (lq > 64 || lk > 64) {
+    static bool attr128 = false;
+    if (!attr128) {
+      cudaFuncSetAttribute(atc::attn_tc128_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)atc::kFwd128Smem);
+      attr128 = true;
+    }
+    atc::attn_tc128_fwd_kernel<<<(unsigned)(batch * heads), atc::kThreads, atc::kFwd128Smem,
+                                 as_stream(stream)>>>(mq, mk, mv, mo, a);
+    return check_launch("attention_tc128_fwd");
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(atc::attn_tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -789,7 +1201,7 @@ int ls2_attention_tc_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
                          int64_t ldcsq, double* csk, int64_t ldcsk, double* csv, int64_t ldcsv,
                          void* stream) {
   if (!ls2_attention_tc_supported(lq, lk, hd, LS2_F16))
-    return fail(LS2_ERR_SHAPE, "attention_tc_bwd: needs fp16, hd == 64, L <= 64");
+    return fail(LS2_ERR_SHAPE, "attention_tc_bwd: needs fp16, hd == 64, L <= 128");
   if (mask_kind == LS2_MASK_PADDING && !lens) return fail(LS2_ERR_SHAPE, "attention_tc: no lens");
   if (mask_kind == LS2_MASK_DENSE) return fail(LS2_ERR_SHAPE, "attention_tc: dense masks unsupported");
   if (mask_kind == LS2_MASK_CAUSAL && lq != lk) return fail(LS2_ERR_SHAPE, "attention_tc: causal needs lq == lk");
@@ -813,6 +1225,17 @@ int ls2_attention_tc_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
       !atc::make_map3(&mdk, dk, cols, lk, batch, lddk, a.G) ||
       !atc::make_map3(&mdv, dv, cols, lk, batch, lddv, a.G))
     return fail(LS2_ERR_CUDA, "attention_tc_bwd: cuTensorMapEncodeTiled failed");
+  if (lq > 64 || lk > 64) {
+    static bool attr128 = false;
+    if (!attr128) {
+      cudaFuncSetAttribute(atc::attn_tc128_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)atc::kBwd128Smem);
+      attr128 = true;
+    }
+    atc::attn_tc128_bwd_kernel<<<(unsigned)(batch * heads), atc::kThreads, atc::kBwd128Smem,
+                                 as_stream(stream)>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
+    return check_launch("attention_tc128_bwd");
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(atc::attn_tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

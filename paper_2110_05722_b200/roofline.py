@@ -36,6 +36,10 @@ def algo_table(tokens: int, d: int, f: int, vocab: int, batch: int, length: int,
          4 * N * D * 2 + N * H * 8),
         (r"attn_tc_bwd_kernel", "fused attention bwd, tcgen05 (P recomputed; + bias partials)",
          7 * N * D * 2 + N * H * 8),
+        (r"attn_tc128_fwd_kernel", "fused attention fwd, tcgen05, 128-row tiles (L <= 128)",
+         4 * N * D * 2 + N * H * 8),
+        (r"attn_tc128_bwd_kernel", "fused attention bwd, tcgen05, 128-row tiles (+ bias partials)",
+         7 * N * D * 2 + N * H * 8),
         (r"attn_fwd_kernel", "fused attention fwd, mma.sync (QK^T, mask, softmax, PV)",
          4 * N * D * 2 + BHL2 * 2),
         (r"attn_bwd_kernel|attn_bwd_persist", "fused attention bwd, mma.sync",

@@ -45,7 +45,10 @@ CASES = [(64, 8, 64, 64, "padding"), (64, 8, 64, 64, "causal"), (3, 2, 37, 37, "
          # group, odd tile counts, cross-attention with Lq != Lk
          (512, 8, 8, 8, "padding"), (341, 8, 12, 12, "causal"), (3, 2, 5, 5, "none"),
          (33, 4, 16, 24, "padding"), (5, 3, 64, 64, "none"), (9, 1, 30, 31, "padding"),
-         (17, 8, 60, 60, "causal"), (1, 1, 1, 1, "none")]
+         (17, 8, 60, 60, "causal"), (1, 1, 1, 1, "none"),
+         # 64 < L <= 128: one 128-row tcgen05 tile per (batch, head)
+         (64, 16, 128, 128, "causal"), (6, 4, 65, 65, "padding"), (5, 2, 100, 77, "padding"),
+         (3, 3, 90, 128, "none"), (16, 12, 128, 128, "padding")]
 
 
 @pytest.mark.parametrize("impl", ["tc", "mma"])
@@ -69,8 +72,8 @@ def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind, impl):
     assert ATT.fused_ok(torch.float16, Lq, Lk, 64, mask)
     if impl == "tc":
         if not ATT.tc_ok(torch.float16, Lq, Lk, 64, mask):
-            assert max(Lq, Lk) > 64
-            pytest.skip("beyond the tcgen05 family (L > 64)")
+            assert kind == "causal" and Lq != Lk
+            pytest.skip("causal cross-attention (Lq != Lk) stays on the mma.sync family")
         probs = ATT.alloc_state(_Alloc(), torch.float16, B, NH, Lq, Lk, 64, mask)
         assert probs.dtype == torch.float32 and probs.shape == (B, NH, Lq, 2)
     else:
@@ -121,13 +124,14 @@ def test_fused_attention_vs_oracle(B, NH, Lq, Lk, kind, impl):
     if impl == "mma":
         assert np.abs(got_cs - want_cs).max() <= 1e-3 * max(1.0, np.abs(want_cs).max())
     else:
-        G = 64 // max(Lq, Lk)
+        G = max(1, 64 // max(Lq, Lk))      # L > 64: one 128-row tile per (b, h)
         grp = np.add.reduceat(want_cs, np.arange(0, B, G), axis=0)
         assert np.abs(got_cs[::G] - grp).max() <= 1e-3 * max(1.0, np.abs(grp).max())
         assert np.all(np.delete(got_cs, np.arange(0, B, G), axis=0) == 0)
 
 
 @pytest.mark.parametrize("B,NH,L,kind", [(64, 8, 64, "padding"), (512, 8, 8, "causal"),
+                                         (64, 16, 128, "causal"), (16, 12, 128, "padding"),
                                          (113, 8, 36, "padding"), (341, 8, 12, "none")])
 def test_tc_attention_matches_mma_kernels(B, NH, L, kind):
     """The tcgen05 and mma.sync families on the same inputs: outputs and
