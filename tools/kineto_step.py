@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--json", default=None)
     ap.add_argument("--top", type=int, default=45)
-    ap.add_argument("--model", default="tbase", choices=["tbase", "tbig"])
+    ap.add_argument("--model", default="tbase", choices=["tbase", "tbig", "bert128", "bert512"])
     ap.add_argument("--shape", default=None, help="BxL batch shape (e.g. 512x8, a WMT bucket)")
     ap.add_argument("--dp", default=None, choices=["shard", "allreduce"],
                     help="one-rank forced data-parallel exchange in the given mode")
@@ -32,18 +32,23 @@ def main():
     from paper_2110_05722_b200.data import FixedShapeTask
     from paper_2110_05722_b200.engine import TrainingEngine
 
-    from paper_2110_05722_b200.config import transformer_big
-    B, L, V = (64, 64, 32000) if a.model == "tbase" else (64, 128, 32000)
+    from paper_2110_05722_b200.config import bert_base, transformer_big
+    from paper_2110_05722_b200.data import MLMTask
+    B, L, V = {"tbase": (64, 64, 32000), "tbig": (64, 128, 32000), "bert128": (64, 128, 30522),
+               "bert512": (16, 512, 30522)}[a.model]
     if a.shape:
         B, L = (int(x) for x in a.shape.lower().split("x"))
-    run = RunConfig(model=transformer_base(V, 256) if a.model == "tbase" else
-                    transformer_big(V, 256),
-                    train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3, batch_tokens=B * L))
+    mcfg = (transformer_base(V, 256) if a.model == "tbase" else
+            transformer_big(V, 256) if a.model == "tbig" else bert_base(V, 512))
+    run = RunConfig(model=mcfg, train=TrainConfig(p_drop=0.1, alpha=0.1, lr=1e-3,
+                                                  batch_tokens=B * L))
     dp = None
     if a.dp:
         from paper_2110_05722_b200.dist import DataParallel
         dp = DataParallel(force=True, mode=a.dp)
-    eng = TrainingEngine(run, task=FixedShapeTask(B, L, V, seed=17), dp=dp)
+    task = (MLMTask(B, L, V, seed=17) if a.model.startswith("bert") else
+            FixedShapeTask(B, L, V, seed=17))
+    eng = TrainingEngine(run, task=task, dp=dp)
     eng.setup_arena()
     for s in range(4):
         eng.train_step(s)
