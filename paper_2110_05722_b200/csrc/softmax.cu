@@ -31,6 +31,16 @@ __device__ __forceinline__ bool kept(const MaskSpec& m, int64_t row, int64_t col
   }
 }
 
+// the row's kept columns are a prefix [0, limit) for every mask kind but dense:
+// evaluated once per row instead of per element (the padding length is a load)
+__device__ __forceinline__ int64_t kept_limit(const MaskSpec& m, int64_t row, int64_t cols) {
+  switch (m.kind) {
+    case LS2_MASK_CAUSAL: return row % m.lq + 1;
+    case LS2_MASK_PADDING: return m.lens[row / (m.heads * m.lq)];
+    default: return cols;
+  }
+}
+
 __device__ __forceinline__ float fexp(float x) { return __expf(x); }
 __device__ __forceinline__ double fexp(double x) { return exp(x); }
 __device__ __forceinline__ float flog(float x) { return __logf(x); }
@@ -52,6 +62,8 @@ __global__ void __launch_bounds__(256) softmax_rows(const Tin* __restrict__ x, T
   for (int64_t r0 = warp * rows_per_warp; r0 < rows; r0 += nwarps * rows_per_warp) {
     const int64_t r = r0 + lane / G;
     const bool live = r < rows;
+    const bool dense = m.kind == LS2_MASK_DENSE;
+    const int64_t lim = live && !dense ? kept_limit(m, r, cols) : cols;
     C v[ITERS][VEC];
     C mx = neg_inf<C>();
 #pragma unroll
@@ -69,7 +81,7 @@ __global__ void __launch_bounds__(256) softmax_rows(const Tin* __restrict__ x, T
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const int64_t c = c0 + e;
-        const bool ok = live && c < cols && kept(m, r, c, cols);
+        const bool ok = live && c < cols && c < lim && (!dense || kept(m, r, c, cols));
         v[it][e] = ok ? v[it][e] * sc : neg_inf<C>();
         mx = max(mx, v[it][e]);
       }
