@@ -10,6 +10,7 @@
 // sub-warp group, G = 1..32), each lane holding ITERS chunks of VEC contiguous
 // elements in registers; rows longer than 32*16*VEC use one CTA per row.
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -47,8 +48,10 @@ __device__ __forceinline__ float flog(float x) { return __logf(x); }
 __device__ __forceinline__ double flog(double x) { return log(x); }
 template <typename C> __device__ __forceinline__ C neg_inf() { return -INFINITY; }
 
-// MODE 0: softmax, MODE 1: log-softmax
-template <typename Tin, typename Tout, int VEC, int ITERS, int MODE>
+// MODE 0: softmax, MODE 1: log-softmax.  ACC64: f64 partition sum (the explicit
+// row_serial strategy, which must agree with the tree kernel to 1 ULP); the
+// default (shape-rule) path sums in fp32
+template <typename Tin, typename Tout, int VEC, int ITERS, int MODE, bool ACC64 = false>
 __global__ void __launch_bounds__(256) softmax_rows(const Tin* __restrict__ x, Tout* __restrict__ y,
                                                     int64_t rows, int64_t cols, int G, MaskSpec m,
                                                     double in_scale, int* all_masked) {
@@ -89,14 +92,15 @@ __global__ void __launch_bounds__(256) softmax_rows(const Tin* __restrict__ x, T
     mx = warp_max(mx, G);
     // the partition sum accumulates in f64 (the reference's float64 reduction), so
     // this template and the tree kernel round it identically (1-ULP agreement)
-    double zd = 0;
+    using Z = typename std::conditional<ACC64, double, C>::type;
+    Z zd = 0;
 #pragma unroll
     for (int it = 0; it < ITERS; ++it)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const C ex = (v[it][e] == neg_inf<C>()) ? (C)0 : fexp(v[it][e] - mx);
         if (MODE == 0) v[it][e] = ex;
-        zd += (double)ex;
+        zd += (Z)ex;
       }
     zd = warp_sum(zd, G);
     if (!live) continue;
@@ -309,8 +313,12 @@ int launch_rows(const void* x, void* y, int64_t rows, int64_t cols, const MaskSp
   const int grid = rows_grid(rows, s.G);
 #define LS2_SM_CASE(V, I)                                                                 \
   if (s.vec == V && s.iters == I) {                                                       \
-    softmax_rows<Tin, Tout, V, I, MODE><<<grid, 256, 0, st>>>((const Tin*)x, (Tout*)y, rows, \
-                                                             cols, s.G, m, in_scale, all_masked); \
+    if (strategy == LS2_SOFTMAX_SERIAL)                                                   \
+      softmax_rows<Tin, Tout, V, I, MODE, true><<<grid, 256, 0, st>>>(                    \
+          (const Tin*)x, (Tout*)y, rows, cols, s.G, m, in_scale, all_masked);             \
+    else                                                                                  \
+      softmax_rows<Tin, Tout, V, I, MODE><<<grid, 256, 0, st>>>((const Tin*)x, (Tout*)y, rows, \
+                                                               cols, s.G, m, in_scale, all_masked); \
     return check_launch("softmax_rows");                                                  \
   }
   LS2_SM_CASE(8, 1) LS2_SM_CASE(8, 2) LS2_SM_CASE(8, 4)
