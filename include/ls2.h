@@ -219,6 +219,18 @@ int ls2_attention_tc_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
                          int mask_kind, const int64_t* lens, double scale, double* csq,
                          int64_t ldcsq, double* csk, int64_t ldcsk, double* csv, int64_t ldcsv,
                          void* stream);
+/* the same with the forward's output O (ctx, [B, Lq, H*64] at row stride ldo): required by
+ * the flash kernels (self-attention 128 < Lq == Lk <= 512: 128-row blocks, K / V
+ * streamed through TMA rings, scores never in HBM; stats are then [B][H][Lq][4] floats
+ * (max, 1/sum, D = rowsum(dO * O), -), and the bias partials have one row per
+ * (batch, 128-row block)); shorter rows ignore O */
+int ls2_attention_tc_bwd_o(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                           int64_t ldv, const void* o, int64_t ldo, void* stats, const void* dout,
+                           int64_t lddo, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                           int64_t lddv, int64_t batch, int64_t heads, int64_t lq, int64_t lk,
+                           int64_t hd, int mask_kind, const int64_t* lens, double scale,
+                           double* csq, int64_t ldcsq, double* csk, int64_t ldcsk, double* csv,
+                           int64_t ldcsv, void* stream);
 
 /* ---- label-smoothed CE: F/kernels.py:338-360, F/gradients.py:47-74 ----
  * row_stats (double[rows*2]) receives per-row (loss, correct) partials;

@@ -71,6 +71,8 @@ _SIGS = {
     "ls2_attention_tc_fwd": [P, L, P, L, P, L, P, P, L, L, L, L, L, L, I, P, D, P],
     "ls2_attention_tc_bwd": [P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, I, P, D,
                              P, L, P, L, P, L, P],
+    "ls2_attention_tc_bwd_o": [P, L, P, L, P, L, P, L, P, P, L, P, L, P, L, P, L, L, L, L, L, L, I,
+                               P, D, P, L, P, L, P, L, P],
     "ls2_embedding_fwd": [P, P, P, P, P, P, L, L, L, L, D, I, I, U, P, U, D, I, I, P],
     "ls2_embedding_bwd": [P, P, P, P, P, I, I, L, L, L, L, D, I, D, I, P],
     "ls2_adam": [P, P, P, P, L, P, P, L, L, P, P, P, P],

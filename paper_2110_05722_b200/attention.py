@@ -33,31 +33,52 @@ from .kernels import AttentionMask, dev
 ENABLED = os.environ.get("LS2_FUSED_ATTENTION", "1") != "0"
 
 
-def fused_ok(dtype, lq: int, lk: int, hd: int, mask) -> bool:
-    if not ENABLED or dtype != torch.float16:
-        return False
-    if mask is not None and not (isinstance(mask, AttentionMask) and
-                                 mask.kind in ("none", "causal", "padding")):
+def _mask_ok(mask) -> bool:
+    return mask is None or (isinstance(mask, AttentionMask) and
+                            mask.kind in ("none", "causal", "padding"))
+
+
+def is_flash(lq: int, lk: int) -> bool:
+    """Rows past 128: the flash kernels (self-attention only, see tc_ok)."""
+    return max(lq, lk) > 128
+
+
+def fused_ok(dtype, lq: int, lk: int, hd: int, mask, flash: bool = False) -> bool:
+    """A fused kernel takes this attention.  flash=True (self-attention call sites,
+    which can hand the backward the forward's output) admits 128 < L <= 512."""
+    if not ENABLED or dtype != torch.float16 or not _mask_ok(mask):
         return False
     _lib.load_library()
-    return bool(_lib._lib.ls2_attention_supported(lq, lk, hd, _lib.F16))
+    if _lib._lib.ls2_attention_supported(lq, lk, hd, _lib.F16):
+        return True
+    return flash and is_flash(lq, lk) and tc_ok(dtype, lq, lk, hd, mask, flash=True)
 
 
-def tc_ok(dtype, lq: int, lk: int, hd: int, mask) -> bool:
+def tc_ok(dtype, lq: int, lk: int, hd: int, mask, flash: bool = False) -> bool:
     """The tcgen05 family takes this shape (implies fused_ok)."""
-    if not fused_ok(dtype, lq, lk, hd, mask):
+    if not ENABLED or dtype != torch.float16 or not _mask_ok(mask):
         return False
     if mask is not None and mask.kind == "causal" and lq != lk:
         return False
+    if is_flash(lq, lk) and not flash:
+        return False
+    _lib.load_library()
     return bool(_lib._lib.ls2_attention_tc_supported(lq, lk, hd, _lib.F16))
 
 
-def alloc_state(arena, dtype, batch, heads, lq, lk, hd, mask):
+def bias_rows(batch: int, lq: int, lk: int) -> int:
+    """Rows of the projection-bias partials the backward leaves: one per batch,
+    or one per (batch, 128-row block) for the flash kernels."""
+    return batch * ((lq + 127) // 128) if is_flash(lq, lk) else batch
+
+
+def alloc_state(arena, dtype, batch, heads, lq, lk, hd, mask, flash: bool = False):
     """The forward's saved softmax state for the fused kernels: f32 row
-    statistics [B, H, Lq, 2] (tcgen05 family) or fp16 probabilities
+    statistics [B, H, Lq, 2] (tcgen05 family; [.., 4] with room for
+    D = rowsum(dO * O) for the flash kernels) or fp16 probabilities
     [B, H, Lq, Lk] (mma.sync family)."""
-    if tc_ok(dtype, lq, lk, hd, mask):
-        return arena.alloc((batch, heads, lq, 2), torch.float32)
+    if tc_ok(dtype, lq, lk, hd, mask, flash=flash):
+        return arena.alloc((batch, heads, lq, 4 if is_flash(lq, lk) else 2), torch.float32)
     return arena.alloc((batch, heads, lq, lk), dtype)
 
 
@@ -86,9 +107,11 @@ def forward(q, ldq, k, ldk, v, ldv, probs, o, ldo, batch, heads, lq, lk, hd, mas
 
 
 def backward(q, ldq, k, ldk, v, ldv, probs, dout, lddo, dq, lddq, dk, lddk, dv, lddv, batch,
-             heads, lq, lk, hd, scale, colsums=None):
+             heads, lq, lk, hd, scale, colsums=None, o=None, ldo=0):
     """colsums: optional ((buf, col0, ld) or None) x 3 for dQ, dK, dV — f64 rows of
-    per-batch column sums (the projection biases' gradient partials)."""
+    per-batch (flash: per (batch, 128-row block), see bias_rows) column sums (the
+    projection biases' gradient partials).  o: the forward's output (required by
+    the flash kernels)."""
     cs = []
     for c in (colsums or (None, None, None)):
         if c is None:
@@ -96,6 +119,15 @@ def backward(q, ldq, k, ldk, v, ldv, probs, dout, lddo, dq, lddq, dk, lddk, dv, 
         else:
             buf, col0, ld = c
             cs += [buf.data_ptr() + 8 * col0, ld]
+    if probs.dtype == torch.float32 and probs.shape[-1] == 4:
+        if o is None:
+            raise ValueError("the flash attention backward needs the forward output o")
+        kind, lens = probs._ls2_amask
+        _lib.call("ls2_attention_tc_bwd_o", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(),
+                  ldv, o.data_ptr(), ldo, probs.data_ptr(), dout.data_ptr(), lddo, dq.data_ptr(),
+                  lddq, dk.data_ptr(), lddk, dv.data_ptr(), lddv, batch, heads, lq, lk, hd, kind,
+                  _lib.ptr(lens), float(scale), *cs, _lib.stream_handle())
+        return
     if probs.dtype == torch.float32:
         kind, lens = probs._ls2_amask
         _lib.call("ls2_attention_tc_bwd", q.data_ptr(), ldq, k.data_ptr(), ldk, v.data_ptr(),

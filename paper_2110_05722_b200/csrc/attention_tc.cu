@@ -733,6 +733,14 @@ __device__ __forceinline__ float partner128(float* buf, const Row128& r, float v
   return buf[(r.half ^ 1) * 128 + r.idx];
 }
 
+__device__ __forceinline__ float partner_pair(float* buf, int q, int half, int lane, float v) {
+  buf[half * 128 + q * 32 + lane] = v;
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+  const float o = buf[(half ^ 1) * 128 + q * 32 + lane];
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // buf reusable afterwards
+  return o;
+}
+
 __device__ __forceinline__ Row128 row128(const Args& a) {
   Row128 r;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1077,6 +1085,522 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc128_bwd_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// 128 < L <= 512 (BERT-512): flash-style kernels on the same tcgen05 blocks.
+// Work units are 128-row blocks of one (batch, head); K / V (or Q / dO) stream
+// through two-slot TMA rings in 128-row chunks (rows past L are TMA zero fill),
+// and the [B, H, L, L] scores never touch HBM.
+//  * forward (per query block): S_c = Q K_c^T for every key chunk into TMEM
+//    (4 x 128 = 512 columns), row statistics over all chunks (max, 1/sum),
+//    then P_c -> shared memory (two-slot ring) and O += P_c V_c (TMEM columns
+//    0-63, S_0's columns, free once P_0 is formed);
+//  * backward dQ (per query block): D = rowsum(dO * O), then per key chunk
+//    S_c, dP_c -> P_c, dS_c = P_c (dP_c - D) scale -> dQ += dS_c K_c;
+//  * backward dK / dV (per key block): per query chunk S, dP -> P, dS ->
+//    dV += P^T dO_i, dK += dS^T Q_i.
+// The statistics [B][H][L][4] hold (max in the log2 domain, 1/sum, D, -).
+// Bias partials: one f64 row per (batch, 128-row block).  Deterministic.
+// ---------------------------------------------------------------------------
+constexpr int kFlashMaxChunks = 4;
+constexpr size_t kFlashFwdSmem = 9 * kPair + 1024;        // Q, K[2], V[2], P[2] (2 chunks each)
+constexpr size_t kFlashDqSmem = 11 * kPair + 1024;        // Q, dO, O, K[2], V[2], dS[2]
+constexpr size_t kFlashDkvSmem = 10 * kPair + 1024;       // K, V, Q[2], dO[2], P (2), dS (2)
+
+template <int AM>
+__device__ __forceinline__ void mma_k128_acc(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc,
+                                             bool accum) {
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint64_t da = AM == KM ? kdesc(a + (kk >> 2) * kPair, kk & 3) : mdesc_bd(a, kk);
+    const uint64_t db = mdesc(b, kk);
+    const uint32_t acc = (kk || accum) ? 1u : 0u;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+
+// keys [0, n) of query row `qpos` of batch b are kept
+__device__ __forceinline__ int flash_keep_n(const Args& a, int b, int qpos) {
+  int n = a.Lk;
+  if (a.mask == LS2_MASK_PADDING) {
+    const int64_t len = __ldg(a.lens + b);
+    n = len < n ? (int)len : n;
+  }
+  if (a.mask == LS2_MASK_CAUSAL) n = qpos + 1 < n ? qpos + 1 : n;
+  return n;
+}
+
+__device__ __forceinline__ void st_row64(uint8_t* chunk_region, int m, const uint32_t (&w)[32]) {
+  uint32_t lo[16], hi[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) { lo[j] = w[j]; hi[j] = w[16 + j]; }
+  st_cols(chunk_region, m, 0, lo);
+  st_cols(chunk_region, m, 1, hi);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
+    const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* Qs = sm;                        // doubles as the O staging
+  uint8_t* Kr = sm + kPair;                // 2 slots
+  uint8_t* Vr = sm + 3 * kPair;            // 2 slots
+  uint8_t* Pr = sm + 5 * kPair;            // 2 slots x 2 chunks
+  __shared__ __align__(8) uint64_t bar_q, kfull[2], kfree[2], vfull[2], pfree[2], bar_s, bar_o;
+  __shared__ uint32_t tmem_base;
+  __shared__ float xm[256], xz[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (a.Lq + 127) / 128;
+  const int qb = blockIdx.x % nqb, bh = blockIdx.x / nqb;
+  const int b = bh / a.H, h = bh % a.H;
+  const int nk = (a.Lk + 127) / 128;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1); mbar_init(&bar_s, 1); mbar_init(&bar_o, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kfull[i], 1); mbar_init(&kfree[i], 1); mbar_init(&vfull[i], 1);
+      mbar_init(&pfree[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_q, (uint32_t)kPair);
+    tma_load_3d(Qs, &mq, h * 64, qb * 128, b, &bar_q);
+    for (int c = 0; c < nk && c < 2; ++c) {
+      mbar_expect_tx(&kfull[c], (uint32_t)kPair);
+      tma_load_3d(Kr + c * kPair, &mk, h * 64, c * 128, b, &kfull[c]);
+      mbar_expect_tx(&vfull[c], (uint32_t)kPair);
+      tma_load_3d(Vr + c * kPair, &mv, h * 64, c * 128, b, &vfull[c]);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        sptr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_base;
+  const int q = warp & 3, half = warp >> 2, m = 32 * q + lane;
+  const int qpos = qb * 128 + m;
+  const bool ok = qpos < a.Lq;
+  const int nkeep = flash_keep_n(a, b, qpos);
+  if (threadIdx.x == 0) {          // S_c for every key chunk
+    mbar_wait(&bar_q, 0);
+    for (int c = 0; c < nk; ++c) {
+      const int s = c & 1;
+      mbar_wait(&kfull[s], (uint32_t)((c >> 1) & 1));
+      tc_after();
+      mma128<KM, KM, 4>(tmem + 128 * c, sptr(Qs), sptr(Kr + s * kPair), a.id_s);
+      commit(&kfree[s]);
+      if (c + 2 < nk) {
+        mbar_wait(&kfree[s], (uint32_t)((c >> 1) & 1));
+        mbar_expect_tx(&kfull[s], (uint32_t)kPair);
+        tma_load_3d(Kr + s * kPair, &mk, h * 64, (c + 2) * 128, b, &kfull[s]);
+      }
+    }
+    commit(&bar_s);
+  }
+  __syncwarp();
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+  mbar_wait(&bar_s, 0);
+  tc_after();
+  // row statistics over every chunk (log2 domain)
+  float mx = -INFINITY, z = 0.f;
+  for (int c = 0; c < nk; ++c) {
+    float x[64];
+    tmem_ld64(tlane + 128 * c + 64 * half, x);
+    const int k0 = 128 * c + 64 * half;
+    float cm = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      x[j] = (ok && k0 + j < nkeep) ? __fmul_rn(x[j], a.scale) : -INFINITY;
+      cm = fmaxf(cm, x[j]);
+    }
+    if (cm > mx) {
+      z = mx == -INFINITY ? 0.f : z * ex2(__fsub_rn(mx, cm));
+      mx = cm;
+    }
+#pragma unroll
+    for (int j = 0; j < 64; ++j) z += x[j] == -INFINITY ? 0.f : ex2(__fsub_rn(x[j], mx));
+  }
+  {
+    const float om = partner_pair(xm, q, half, lane, mx);
+    const float oz = partner_pair(xz, q, half, lane, z);
+    const float M = fmaxf(mx, om);
+    z = (mx == -INFINITY ? 0.f : z * ex2(__fsub_rn(mx, M))) +
+        (om == -INFINITY ? 0.f : oz * ex2(__fsub_rn(om, M)));
+    mx = M;
+  }
+  const float iz = z > 0.f ? 1.f / z : 0.f;
+  if (ok && half == 0) {
+    float4* st4 = reinterpret_cast<float4*>(a.stats) + ((int64_t)b * a.H + h) * a.Lq + qpos;
+    *st4 = make_float4(mx, iz, 0.f, 0.f);
+  }
+  // P_c -> ring, O += P_c V_c
+  for (int c = 0; c < nk; ++c) {
+    const int ps = c & 1;
+    if (c >= 2) mbar_wait(&pfree[ps], (uint32_t)(((c - 2) >> 1) & 1));
+    float x[64];
+    tmem_ld64(tlane + 128 * c + 64 * half, x);
+    const int k0 = 128 * c + 64 * half;
+    uint32_t w[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float p2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kk = k0 + 2 * j + e;
+        p2[e] = (ok && kk < nkeep) ? __fmul_rn(ex2(__fsub_rn(__fmul_rn(x[2 * j + e], a.scale), mx)), iz)
+                                   : 0.f;
+      }
+      w[j] = pack_h2(p2[0], p2[1]);
+    }
+    st_row64(Pr + ps * 2 * kPair + half * kPair, m, w);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();                 // P_c complete; S_c read (and S_0 before O lands)
+    if (threadIdx.x == 0) {
+      tc_after();
+      mbar_wait(&vfull[c & 1], (uint32_t)((c >> 1) & 1));
+      mma_k128_acc<KM>(tmem, sptr(Pr + ps * 2 * kPair), sptr(Vr + (c & 1) * kPair), a.id128_pv,
+                       c > 0);
+      commit(&pfree[ps]);
+      if (c + 2 < nk) {              // the V slot is free once this MMA completes
+        mbar_wait(&pfree[ps], (uint32_t)((c >> 1) & 1));
+        mbar_expect_tx(&vfull[c & 1], (uint32_t)kPair);
+        tma_load_3d(Vr + (c & 1) * kPair, &mv, h * 64, (c + 2) * 128, b, &vfull[c & 1]);
+      }
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) commit(&bar_o);
+  __syncwarp();
+  mbar_wait(&bar_o, 0);
+  tc_after();
+  {
+    float o[32];
+    tmem_ld32(tlane + 32 * half, o);
+    st_cols_f(Qs, m, half, o);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mo, h * 64, qb * 128, b, Qs);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// the 32 fp16 columns [32 h, 32 h + 32) of row m of a 64-column swizzled tile
+__device__ __forceinline__ void ld_cols(const uint8_t* region, int m, int half, float (&f)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 u = *reinterpret_cast<const uint4*>(region + swz(m, 4 * half + c));
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 p = unpack_h2(w4[j]);
+      f[8 * c + 2 * j] = p.x;
+      f[8 * c + 2 * j + 1] = p.y;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_flash_dq_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+    const __grid_constant__ CUtensorMap mo, const __grid_constant__ CUtensorMap mdq,
+    const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* Qs = sm;                        // doubles as the dQ staging
+  uint8_t* Ds = sm + kPair;                // dO
+  uint8_t* Os = sm + 2 * kPair;            // O (for D)
+  uint8_t* Kr = sm + 3 * kPair;            // 2 slots
+  uint8_t* Vr = sm + 5 * kPair;            // 2 slots
+  uint8_t* Sr = sm + 7 * kPair;            // dS: 2 slots x 2 chunks
+  __shared__ __align__(8) uint64_t bar_ld, kvfull[2], dsfree[2], bar_sd, bar_q;
+  __shared__ uint32_t tmem_base;
+  __shared__ float xr[256];
+  __shared__ float red[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (a.Lq + 127) / 128;
+  const int qb = blockIdx.x % nqb, bh = blockIdx.x / nqb;
+  const int b = bh / a.H, h = bh % a.H;
+  const int nk = (a.Lk + 127) / 128;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_ld, 1); mbar_init(&bar_sd, 1); mbar_init(&bar_q, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&kvfull[i], 1); mbar_init(&dsfree[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_ld, (uint32_t)(3 * kPair));
+    tma_load_3d(Qs, &mq, h * 64, qb * 128, b, &bar_ld);
+    tma_load_3d(Ds, &mdo, h * 64, qb * 128, b, &bar_ld);
+    tma_load_3d(Os, &mo, h * 64, qb * 128, b, &bar_ld);
+    for (int c = 0; c < nk && c < 2; ++c) {
+      mbar_expect_tx(&kvfull[c], (uint32_t)(2 * kPair));
+      tma_load_3d(Kr + c * kPair, &mk, h * 64, c * 128, b, &kvfull[c]);
+      tma_load_3d(Vr + c * kPair, &mv, h * 64, c * 128, b, &kvfull[c]);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        sptr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_base;
+  const int q = warp & 3, half = warp >> 2, m = 32 * q + lane;
+  const int qpos = qb * 128 + m;
+  const bool ok = qpos < a.Lq;
+  const int nkeep = flash_keep_n(a, b, qpos);
+  float4* st4 = reinterpret_cast<float4*>(a.stats) + ((int64_t)b * a.H + h) * a.Lq + qpos;
+  float4 stv = ok ? *st4 : make_float4(0.f, 0.f, 0.f, 0.f);
+  mbar_wait(&bar_ld, 0);
+  float D;
+  {   // D = rowsum(dO * O) over the head's 64 columns
+    float fo[32], fd[32];
+    ld_cols(Os, m, half, fo);
+    ld_cols(Ds, m, half, fd);
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t = fmaf(fd[j], fo[j], t);
+    D = t + partner_pair(xr, q, half, lane, t);
+  }
+  if (ok && half == 0) { stv.z = D; *st4 = stv; }
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+  for (int c = 0; c < nk; ++c) {
+    const int s = c & 1;
+    if (threadIdx.x == 0) {
+      mbar_wait(&kvfull[s], (uint32_t)((c >> 1) & 1));
+      tc_after();
+      mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Kr + s * kPair), a.id_s);           // S
+      mma128<KM, KM, 4>(tmem + 128, sptr(Ds), sptr(Vr + s * kPair), a.id_s);     // dP
+      commit(&bar_sd);
+    }
+    __syncwarp();
+    mbar_wait(&bar_sd, (uint32_t)(c & 1));
+    tc_after();
+    if (c >= 2) mbar_wait(&dsfree[s], (uint32_t)(((c - 2) >> 1) & 1));
+    uint32_t w[32];
+    {
+      float x[64], dp[64];
+      tmem_ld64(tlane + 64 * half, x);
+      tmem_ld64(tlane + 128 + 64 * half, dp);
+      const int k0 = 128 * c + 64 * half;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float v2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 2 * j + e;
+          const float p = (ok && k0 + i < nkeep)
+                              ? __fmul_rn(ex2(__fsub_rn(__fmul_rn(x[i], a.scale), stv.x)), stv.y)
+                              : 0.f;
+          v2[e] = p * (dp[i] - D) * a.dscale;
+        }
+        w[j] = pack_h2(v2[0], v2[1]);
+      }
+    }
+    st_row64(Sr + s * 2 * kPair + half * kPair, m, w);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();                 // dS_c complete; S, dP read
+    if (threadIdx.x == 0) {
+      tc_after();
+      mma_k128_acc<KM>(tmem + 256, sptr(Sr + s * 2 * kPair), sptr(Kr + s * kPair), a.id128_pv,
+                       c > 0);                                                   // dQ += dS K
+      commit(&dsfree[s]);
+      if (c + 2 < nk) {
+        mbar_wait(&dsfree[s], (uint32_t)((c >> 1) & 1));
+        mbar_expect_tx(&kvfull[s], (uint32_t)(2 * kPair));
+        tma_load_3d(Kr + s * kPair, &mk, h * 64, (c + 2) * 128, b, &kvfull[s]);
+        tma_load_3d(Vr + s * kPair, &mv, h * 64, (c + 2) * 128, b, &kvfull[s]);
+      }
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) commit(&bar_q);
+  __syncwarp();
+  mbar_wait(&bar_q, 0);
+  tc_after();
+  {
+    float x[32];
+    tmem_ld32(tlane + 256 + 32 * half, x);
+    st_cols_f(Qs, m, half, x);
+    if (!ok) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = 0.f;
+    }
+    colsum128(x, q, half, red,
+              a.csq ? a.csq + ((int64_t)b * nqb + qb) * a.ldcsq + h * 64 : nullptr);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mdq, h * 64, qb * 128, b, Qs);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_flash_dkv_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+    const __grid_constant__ CUtensorMap mdk, const __grid_constant__ CUtensorMap mdv,
+    const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* Ks = sm;                        // doubles as the dK staging
+  uint8_t* Vs = sm + kPair;                // doubles as the dV staging
+  uint8_t* Qr = sm + 2 * kPair;            // 2 slots
+  uint8_t* Dr = sm + 4 * kPair;            // dO, 2 slots
+  uint8_t* Pb = sm + 6 * kPair;            // P (2 chunks)
+  uint8_t* Sb = sm + 8 * kPair;            // dS (2 chunks)
+  __shared__ __align__(8) uint64_t bar_kv, qfull[2], bar_sd, bar_mm;
+  __shared__ uint32_t tmem_base;
+  __shared__ float xr[256];
+  __shared__ float red[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = (a.Lk + 127) / 128;
+  const int kb = blockIdx.x % nkb, bh = blockIdx.x / nkb;
+  const int b = bh / a.H, h = bh % a.H;
+  const int nq = (a.Lq + 127) / 128;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_kv, 1); mbar_init(&bar_sd, 1); mbar_init(&bar_mm, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&qfull[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_kv, (uint32_t)(2 * kPair));
+    tma_load_3d(Ks, &mk, h * 64, kb * 128, b, &bar_kv);
+    tma_load_3d(Vs, &mv, h * 64, kb * 128, b, &bar_kv);
+    for (int c = 0; c < nq && c < 2; ++c) {
+      mbar_expect_tx(&qfull[c], (uint32_t)(2 * kPair));
+      tma_load_3d(Qr + c * kPair, &mq, h * 64, c * 128, b, &qfull[c]);
+      tma_load_3d(Dr + c * kPair, &mdo, h * 64, c * 128, b, &qfull[c]);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        sptr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_base;
+  const int q = warp & 3, half = warp >> 2, m = 32 * q + lane;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+  const float4* st4 = reinterpret_cast<const float4*>(a.stats) + ((int64_t)b * a.H + h) * a.Lq;
+  for (int c = 0; c < nq; ++c) {
+    const int s = c & 1;
+    const int qpos = c * 128 + m;                      // this thread's query row (S: M = query)
+    const bool ok = qpos < a.Lq;
+    const int nkeep = flash_keep_n(a, b, qpos);
+    const float4 stv = ok ? st4[qpos] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x == 0) {
+      if (c == 0) mbar_wait(&bar_kv, 0);
+      mbar_wait(&qfull[s], (uint32_t)((c >> 1) & 1));
+      tc_after();
+      mma128<KM, KM, 4>(tmem, sptr(Qr + s * kPair), sptr(Ks), a.id_s);           // S
+      mma128<KM, KM, 4>(tmem + 128, sptr(Dr + s * kPair), sptr(Vs), a.id_s);     // dP
+      commit(&bar_sd);
+    }
+    __syncwarp();
+    mbar_wait(&bar_sd, (uint32_t)(c & 1));
+    tc_after();
+    if (c >= 1) mbar_wait(&bar_mm, (uint32_t)((c - 1) & 1));   // P / dS buffers read
+    uint32_t pw[32], dw[32];
+    {
+      float x[64], dp[64];
+      tmem_ld64(tlane + 64 * half, x);
+      tmem_ld64(tlane + 128 + 64 * half, dp);
+      const int k0 = kb * 128 + 64 * half;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float p2[2], d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 2 * j + e;
+          const float p = (ok && k0 + i < nkeep)
+                              ? __fmul_rn(ex2(__fsub_rn(__fmul_rn(x[i], a.scale), stv.x)), stv.y)
+                              : 0.f;
+          p2[e] = p;
+          d2[e] = p * (dp[i] - stv.z) * a.dscale;
+        }
+        pw[j] = pack_h2(p2[0], p2[1]);
+        dw[j] = pack_h2(d2[0], d2[1]);
+      }
+    }
+    st_row64(Pb + half * kPair, m, pw);
+    st_row64(Sb + half * kPair, m, dw);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();                 // P, dS complete; S, dP read
+    if (threadIdx.x == 0) {
+      tc_after();
+      mma_k128_acc<MN>(tmem + 256, sptr(Pb), sptr(Dr + s * kPair), a.id128_mm, c > 0);  // dV
+      mma_k128_acc<MN>(tmem + 320, sptr(Sb), sptr(Qr + s * kPair), a.id128_mm, c > 0);  // dK
+      commit(&bar_mm);
+      if (c + 2 < nq) {
+        mbar_wait(&bar_mm, (uint32_t)(c & 1));
+        mbar_expect_tx(&qfull[s], (uint32_t)(2 * kPair));
+        tma_load_3d(Qr + s * kPair, &mq, h * 64, (c + 2) * 128, b, &qfull[s]);
+        tma_load_3d(Dr + s * kPair, &mdo, h * 64, (c + 2) * 128, b, &qfull[s]);
+      }
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar_mm, (uint32_t)((nq - 1) & 1));
+  tc_after();
+  const int64_t prow = (int64_t)b * nkb + kb;
+  {
+    float x[32];
+    tmem_ld32(tlane + 256 + 32 * half, x);              // dV (row = key)
+    st_cols_f(Vs, m, half, x);
+    colsum128(x, q, half, red, a.csv ? a.csv + prow * a.ldcsv + h * 64 : nullptr);
+  }
+  {
+    float x[32];
+    tmem_ld32(tlane + 320 + 32 * half, x);              // dK
+    st_cols_f(Ks, m, half, x);
+    colsum128(x, q, half, red, a.csk ? a.csk + prow * a.ldcsk + h * 64 : nullptr);
+  }
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&mdv, h * 64, kb * 128, b, Vs);
+    tma_store_3d(&mdk, h * 64, kb * 128, b, Ks);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // [B][L][ld] fp16 operand, columns [0, cols) from `base`: boxes of 64 columns x L
 // rows x G sequences, 128-byte swizzle, zero fill past L / B
 bool make_map3(CUtensorMap* m, const void* base, int64_t cols, int64_t L, int64_t B, int64_t ld,
@@ -1086,6 +1610,20 @@ bool make_map3(CUtensorMap* m, const void* base, int64_t cols, int64_t L, int64_
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)L, (cuuint64_t)B};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(L * ld * 2)};
   cuuint32_t box[3] = {64, (cuuint32_t)L, (cuuint32_t)G};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the same operand with 128-row boxes (flash kernels: one 128-row block per load)
+bool make_map3_rows(CUtensorMap* m, const void* base, int64_t cols, int64_t L, int64_t B,
+                    int64_t ld, int box_rows) {
+  auto fn = tc::encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)L, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(L * ld * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1153,7 +1691,9 @@ int ls2_attention_tc_supported(int64_t lq, int64_t lk, int64_t hd, int dtype) {
     const char* e = std::getenv("LS2_ATTN_TC");
     return e && e[0] == '0';
   }();
-  return !off && dtype == LS2_F16 && hd == 64 && lq >= 1 && lk >= 1 && lq <= 128 && lk <= 128;
+  if (off || dtype != LS2_F16 || hd != 64 || lq < 1 || lk < 1) return 0;
+  if (lq <= 128 && lk <= 128) return 1;
+  return lq == lk && lq <= 128 * atc::kFlashMaxChunks;     // flash kernels: self-attention
 }
 
 int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
@@ -1161,7 +1701,7 @@ int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
                          int64_t heads, int64_t lq, int64_t lk, int64_t hd, int mask_kind,
                          const int64_t* lens, double scale, void* stream) {
   if (!ls2_attention_tc_supported(lq, lk, hd, LS2_F16))
-    return fail(LS2_ERR_SHAPE, "attention_tc_fwd: needs fp16, hd == 64, L <= 128");
+    return fail(LS2_ERR_SHAPE, "attention_tc_fwd: needs fp16, hd == 64, L <= 128 (or Lq == Lk <= 512)");
   if (mask_kind == LS2_MASK_PADDING && !lens) return fail(LS2_ERR_SHAPE, "attention_tc: no lens");
   if (mask_kind == LS2_MASK_DENSE) return fail(LS2_ERR_SHAPE, "attention_tc: dense masks unsupported");
   if (mask_kind == LS2_MASK_CAUSAL && lq != lk) return fail(LS2_ERR_SHAPE, "attention_tc: causal needs lq == lk");
@@ -1173,6 +1713,23 @@ int ls2_attention_tc_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
   atc::fill_args(a, batch, heads, lq, lk, mask_kind, lens, scale, (float2*)stats);
   CUtensorMap mq, mk, mv, mo;
   const int64_t cols = heads * 64;
+  if (lq > 128 || lk > 128) {      // flash: stats are [B][H][Lq][4] floats
+    if (!atc::make_map3_rows(&mq, q, cols, lq, batch, ldq, 128) ||
+        !atc::make_map3_rows(&mk, k, cols, lk, batch, ldk, 128) ||
+        !atc::make_map3_rows(&mv, v, cols, lk, batch, ldv, 128) ||
+        !atc::make_map3_rows(&mo, o, cols, lq, batch, ldo, 128))
+      return fail(LS2_ERR_CUDA, "attention_flash_fwd: cuTensorMapEncodeTiled failed");
+    static bool fattr = false;
+    if (!fattr) {
+      cudaFuncSetAttribute(atc::attn_flash_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)atc::kFlashFwdSmem);
+      fattr = true;
+    }
+    const int64_t nqb = (lq + 127) / 128;
+    atc::attn_flash_fwd_kernel<<<(unsigned)(batch * heads * nqb), atc::kThreads,
+                                 atc::kFlashFwdSmem, as_stream(stream)>>>(mq, mk, mv, mo, a);
+    return check_launch("attention_flash_fwd");
+  }
   if (!atc::make_map3(&mq, q, cols, lq, batch, ldq, a.G) ||
       !atc::make_map3(&mk, k, cols, lk, batch, ldk, a.G) ||
       !atc::make_map3(&mv, v, cols, lk, batch, ldv, a.G) ||
@@ -1254,6 +1811,61 @@ int ls2_attention_tc_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
   atc::attn_tc_bwd_kernel<<<grid, atc::kThreads, atc::kBwdSmem, as_stream(stream)>>>(
       mq, mk, mv, mdo, mdq, mdk, mdv, a);
   return check_launch("attention_tc_bwd");
+}
+
+// the backward with the forward's output O (ctx): the flash kernels (Lq == Lk > 128)
+// need D = rowsum(dO * O); shorter rows ignore it and take ls2_attention_tc_bwd
+int ls2_attention_tc_bwd_o(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                           int64_t ldv, const void* o, int64_t ldo, void* stats, const void* dout,
+                           int64_t lddo, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                           int64_t lddv, int64_t batch, int64_t heads, int64_t lq, int64_t lk,
+                           int64_t hd, int mask_kind, const int64_t* lens, double scale,
+                           double* csq, int64_t ldcsq, double* csk, int64_t ldcsk, double* csv,
+                           int64_t ldcsv, void* stream) {
+  if (lq <= 128 && lk <= 128)
+    return ls2_attention_tc_bwd(q, ldq, k, ldk, v, ldv, stats, dout, lddo, dq, lddq, dk, lddk, dv,
+                                lddv, batch, heads, lq, lk, hd, mask_kind, lens, scale, csq, ldcsq,
+                                csk, ldcsk, csv, ldcsv, stream);
+  if (!ls2_attention_tc_supported(lq, lk, hd, LS2_F16))
+    return fail(LS2_ERR_SHAPE, "attention_flash_bwd: needs fp16, hd == 64, Lq == Lk <= 512");
+  if (!o) return fail(LS2_ERR_SHAPE, "attention_flash_bwd: needs the forward output O");
+  if (mask_kind == LS2_MASK_PADDING && !lens) return fail(LS2_ERR_SHAPE, "attention_tc: no lens");
+  if (mask_kind == LS2_MASK_DENSE) return fail(LS2_ERR_SHAPE, "attention_tc: dense masks unsupported");
+  if (!atc::aligned16(q, ldq) || !atc::aligned16(k, ldk) || !atc::aligned16(v, ldv) ||
+      !atc::aligned16(o, ldo) || !atc::aligned16(dout, lddo) || !atc::aligned16(dq, lddq) ||
+      !atc::aligned16(dk, lddk) || !atc::aligned16(dv, lddv))
+    return fail(LS2_ERR_SHAPE, "attention_tc: operands need 16-byte alignment");
+  if (batch <= 0 || heads <= 0) return LS2_OK;
+  atc::Args a;
+  atc::fill_args(a, batch, heads, lq, lk, mask_kind, lens, scale, (float2*)stats);
+  a.csq = csq; a.csk = csk; a.csv = csv;
+  a.ldcsq = ldcsq; a.ldcsk = ldcsk; a.ldcsv = ldcsv;
+  CUtensorMap mq, mk, mv, mo, mdo, mdq, mdk, mdv;
+  const int64_t cols = heads * 64;
+  if (!atc::make_map3_rows(&mq, q, cols, lq, batch, ldq, 128) ||
+      !atc::make_map3_rows(&mk, k, cols, lk, batch, ldk, 128) ||
+      !atc::make_map3_rows(&mv, v, cols, lk, batch, ldv, 128) ||
+      !atc::make_map3_rows(&mo, o, cols, lq, batch, ldo, 128) ||
+      !atc::make_map3_rows(&mdo, dout, cols, lq, batch, lddo, 128) ||
+      !atc::make_map3_rows(&mdq, dq, cols, lq, batch, lddq, 128) ||
+      !atc::make_map3_rows(&mdk, dk, cols, lk, batch, lddk, 128) ||
+      !atc::make_map3_rows(&mdv, dv, cols, lk, batch, lddv, 128))
+    return fail(LS2_ERR_CUDA, "attention_flash_bwd: cuTensorMapEncodeTiled failed");
+  static bool fattr = false;
+  if (!fattr) {
+    cudaFuncSetAttribute(atc::attn_flash_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)atc::kFlashDqSmem);
+    cudaFuncSetAttribute(atc::attn_flash_dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)atc::kFlashDkvSmem);
+    fattr = true;
+  }
+  const int64_t nqb = (lq + 127) / 128, nkb = (lk + 127) / 128;
+  atc::attn_flash_dq_kernel<<<(unsigned)(batch * heads * nqb), atc::kThreads, atc::kFlashDqSmem,
+                              as_stream(stream)>>>(mq, mk, mv, mdo, mo, mdq, a);
+  if (int rc = check_launch("attention_flash_dq")) return rc;
+  atc::attn_flash_dkv_kernel<<<(unsigned)(batch * heads * nkb), atc::kThreads, atc::kFlashDkvSmem,
+                               as_stream(stream)>>>(mq, mk, mv, mdo, mdk, mdv, a);
+  return check_launch("attention_flash_dkv");
 }
 
 }  // extern "C"

@@ -887,8 +887,8 @@ def _self_attention_fwd(x, w, mask, p_drop, seed, site, n_heads, eps, arena, sta
     qkv = arena.alloc((b, l, 3 * d), dt)
     _linear(u1.view(r, d), w.wqkv, w.bqkv, qkv.view(r, 3 * d))
     stash.push(p + "qkv", qkv)
-    if ATT.fused_ok(dt, l, l, hd, mask):
-        scores = ATT.alloc_state(arena, dt, b, n_heads, l, l, hd, mask)
+    if ATT.fused_ok(dt, l, l, hd, mask, flash=True):
+        scores = ATT.alloc_state(arena, dt, b, n_heads, l, l, hd, mask, flash=True)
         ctxm = arena.alloc((b, l, d), dt)
         ATT.forward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
                     scores, ctxm, d, b, n_heads, l, l, hd, mask, 1.0 / math.sqrt(hd))
@@ -1103,19 +1103,21 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dpro
     dctxm = arena.alloc((b, l, d), dt)
     K.gemm(dproj.view(r, d), _as_dt(w.wo, dt), out=dctxm.view(r, d))
     _wgrad(sink, pp + "attn.wo", dproj.view(r, d), ctxm.view(r, d))
-    arena.free(dproj); arena.free(ctxm)
+    arena.free(dproj)
     bias_done = False
-    if ATT.fused_ok(dt, l, l, hd, AttentionMask("none")):
+    if ATT.fused_ok(dt, l, l, hd, AttentionMask("none"), flash=True):
         dqkv = arena.alloc((b, l, 3 * d), dt)
-        # the qkv bias gradient leaves the kernel as per-batch column partials
-        part = _defer(sink, [pp + "attn.bqkv"], b, 1, 3 * d)
+        # the qkv bias gradient leaves the kernel as per-batch (flash: per 128-row
+        # block) column partials
+        part = _defer(sink, [pp + "attn.bqkv"], ATT.bias_rows(b, l, l), 1, 3 * d)
         ATT.backward(qkv[..., :d], 3 * d, qkv[..., d:2 * d], 3 * d, qkv[..., 2 * d:], 3 * d,
                      probs, dctxm, d, dqkv[..., :d], 3 * d, dqkv[..., d:2 * d], 3 * d,
                      dqkv[..., 2 * d:], 3 * d, b, n_heads, l, l, hd, 1.0 / math.sqrt(hd),
                      colsums=None if part is None else
-                     ((part, 0, 3 * d), (part, d, 3 * d), (part, 2 * d, 3 * d)))
+                     ((part, 0, 3 * d), (part, d, 3 * d), (part, 2 * d, 3 * d)),
+                     o=ctxm, ldo=d)
         bias_done = part is not None
-        arena.free(probs); arena.free(dctxm); arena.free(qkv)
+        arena.free(probs); arena.free(dctxm); arena.free(qkv); arena.free(ctxm)
     else:
         dctx = _heads(dctxm, n_heads)
         qh, kh, vh = _qkv_heads(qkv, n_heads)
@@ -1129,6 +1131,7 @@ def _self_attention_bwd(dy1, w, stash, sink, n_heads, p_drop, arena, p, pp, dpro
         K.gemm(dscores, qh, trans_a=True, out=dk)
         K.gemm(probs, dctx, trans_a=True, out=dv)
         arena.free(dscores); arena.free(probs); arena.free(dctxm); arena.free(qkv)
+        arena.free(ctxm)
     du1 = arena.alloc((b, l, d), dt)
     K.gemm(dqkv.view(r, 3 * d), _as_dt(w.wqkv, dt), out=du1.view(r, d))
     _wgrad(sink, pp + "attn.wqkv", dqkv.view(r, 3 * d), u1.view(r, d))

@@ -162,3 +162,54 @@ def test_fused_attention_gates():
     assert not ATT.fused_ok(torch.float16, 64, 200, 64, None)
     assert not ATT.fused_ok(torch.float16, 64, 64, 32, None)
     assert not ATT.fused_ok(torch.float16, 64, 64, 64, torch.ones(64, 64, dtype=torch.bool))
+
+
+@pytest.mark.parametrize("B,NH,L,kind", [(4, 4, 512, "padding"), (3, 2, 256, "none"),
+                                         (2, 3, 200, "causal"), (5, 2, 129, "padding"),
+                                         (2, 12, 384, "padding"), (16, 12, 512, "padding")])
+def test_flash_attention_vs_oracle(B, NH, L, kind):
+    """128 < L <= 512 self-attention (BERT-512): the flash kernels (128-row blocks,
+    K / V streamed, scores never in HBM; backward = dQ pass + dK/dV pass with
+    D = rowsum(dO * O)) against the f32 oracle, and the bias partials (one row per
+    (batch, 128-row block)) against the column sums of the stored gradients."""
+    rng = np.random.default_rng(B * 1000 + L)
+    d = 64 * NH
+    qkv_h = (rng.normal(size=(B, L, 3 * d)) * 0.8).astype(np.float16)
+    qkv_h[..., 2 * d:] = rng.normal(size=(B, L, d)).astype(np.float16)
+    dod = rng.normal(size=(B, L, d)).astype(np.float16)
+    lens = rng.integers(1, L + 1, B)
+    lens[0] = L
+    mask = AttentionMask(kind, torch.tensor(lens, device="cuda")) if kind == "padding" else \
+        AttentionMask(kind)
+    keep = {"padding": O.pad_keep(lens, L, L), "causal": O.causal_keep(L, L), "none": None}[kind]
+    assert ATT.fused_ok(torch.float16, L, L, 64, mask, flash=True)
+    assert not ATT.fused_ok(torch.float16, L, L, 64, mask)          # cross-attention sites
+    qkv = torch.tensor(qkv_h, device="cuda")
+    q, k, v = qkv[..., :d], qkv[..., d:2 * d], qkv[..., 2 * d:]
+    st = ATT.alloc_state(_Alloc(), torch.float16, B, NH, L, L, 64, mask, flash=True)
+    assert st.dtype == torch.float32 and st.shape == (B, NH, L, 4)
+    o = torch.empty((B, L, d), dtype=torch.float16, device="cuda")
+    scale = 1.0 / math.sqrt(64)
+    ATT.forward(q, 3 * d, k, 3 * d, v, 3 * d, st, o, d, B, NH, L, L, 64, mask, scale)
+    dqkv = torch.empty_like(qkv)
+    nrow = ATT.bias_rows(B, L, L)
+    assert nrow == B * ((L + 127) // 128)
+    cs = torch.full((nrow, 3 * d), float("nan"), dtype=torch.float64, device="cuda")
+    dout = torch.tensor(dod, device="cuda")
+    ATT.backward(q, 3 * d, k, 3 * d, v, 3 * d, st, dout, d, dqkv[..., :d], 3 * d,
+                 dqkv[..., d:2 * d], 3 * d, dqkv[..., 2 * d:], 3 * d, B, NH, L, L, 64, scale,
+                 colsums=((cs, 0, 3 * d), (cs, d, 3 * d), (cs, 2 * d, 3 * d)), o=o, ldo=d)
+    hs = lambda x: x.astype(np.float32).reshape(B, L, NH, 64).transpose(0, 2, 1, 3)  # noqa
+    merge = lambda x: x.transpose(0, 2, 1, 3).reshape(B, L, d)  # noqa
+    _, oo, dqq, dkk, dvv = _ref(hs(qkv_h[..., :d]), hs(qkv_h[..., d:2 * d]),
+                                hs(qkv_h[..., 2 * d:]), keep, hs(dod), scale)
+    got_dqkv = H(dqkv).astype(np.float32)
+    for got, want in ((H(o).astype(np.float32), merge(oo)), (got_dqkv[..., :d], merge(dqq)),
+                      (got_dqkv[..., d:2 * d], merge(dkk)), (got_dqkv[..., 2 * d:], merge(dvv))):
+        assert np.abs(got - want).max() <= 2e-2 * max(1.0, np.abs(want).max())
+        assert np.linalg.norm(got - want) <= 1e-2 * max(1e-6, np.linalg.norm(want))
+    got_cs = H(cs)
+    assert np.isfinite(got_cs).all()
+    want_cs = H(dqkv).astype(np.float64).sum(1)                     # [B, 3d]
+    per_b = got_cs.reshape(B, -1, 3 * d).sum(1)
+    assert np.abs(per_b - want_cs).max() <= 1e-3 * max(1.0, np.abs(want_cs).max())
