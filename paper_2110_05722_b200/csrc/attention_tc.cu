@@ -1102,8 +1102,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc128_bwd_kernel(
 // Bias partials: one f64 row per (batch, 128-row block).  Deterministic.
 // ---------------------------------------------------------------------------
 constexpr int kFlashMaxChunks = 4;
-constexpr size_t kFlashFwdSmem = 9 * kPair + 1024;        // Q, K[2], V[2], P[2] (2 chunks each)
-constexpr size_t kFlashDqSmem = 11 * kPair + 1024;        // Q, dO, O, K[2], V[2], dS[2]
+constexpr size_t kFlashFwdSmem = 13 * kPair + 1024;       // Q, K[4], V[4], P[2] (2 chunks each)
+constexpr size_t kFlashDqSmem = 13 * kPair + 1024;        // Q, dO, O, K[4], V[4], dS (2 chunks)
 constexpr size_t kFlashDkvSmem = 10 * kPair + 1024;       // K, V, Q[2], dO[2], P (2), dS (2)
 
 template <int AM>
@@ -1149,10 +1149,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* Qs = sm;                        // doubles as the O staging
-  uint8_t* Kr = sm + kPair;                // 2 slots
-  uint8_t* Vr = sm + 3 * kPair;            // 2 slots
-  uint8_t* Pr = sm + 5 * kPair;            // 2 slots x 2 chunks
-  __shared__ __align__(8) uint64_t bar_q, kfull[2], kfree[2], vfull[2], pfree[2], bar_s, bar_o;
+  uint8_t* Kr = sm + kPair;                // one slot per key chunk (<= 4)
+  uint8_t* Vr = sm + 5 * kPair;            // one slot per key chunk
+  uint8_t* Pr = sm + 9 * kPair;            // 2 slots x 2 chunks
+  __shared__ __align__(8) uint64_t bar_q, kfull[kFlashMaxChunks], vfull[kFlashMaxChunks],
+      pfree[2], bar_s, bar_o;
   __shared__ uint32_t tmem_base;
   __shared__ float xm[256], xz[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1162,14 +1163,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
   const int nk = (a.Lk + 127) / 128;
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1); mbar_init(&bar_s, 1); mbar_init(&bar_o, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kfull[i], 1); mbar_init(&kfree[i], 1); mbar_init(&vfull[i], 1);
-      mbar_init(&pfree[i], 1);
-    }
+    for (int i = 0; i < kFlashMaxChunks; ++i) { mbar_init(&kfull[i], 1); mbar_init(&vfull[i], 1); }
+    for (int i = 0; i < 2; ++i) mbar_init(&pfree[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_expect_tx(&bar_q, (uint32_t)kPair);
     tma_load_3d(Qs, &mq, h * 64, qb * 128, b, &bar_q);
-    for (int c = 0; c < nk && c < 2; ++c) {
+    for (int c = 0; c < nk; ++c) {
       mbar_expect_tx(&kfull[c], (uint32_t)kPair);
       tma_load_3d(Kr + c * kPair, &mk, h * 64, c * 128, b, &kfull[c]);
       mbar_expect_tx(&vfull[c], (uint32_t)kPair);
@@ -1192,16 +1191,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
   if (threadIdx.x == 0) {          // S_c for every key chunk
     mbar_wait(&bar_q, 0);
     for (int c = 0; c < nk; ++c) {
-      const int s = c & 1;
-      mbar_wait(&kfull[s], (uint32_t)((c >> 1) & 1));
+      mbar_wait(&kfull[c], 0);
       tc_after();
-      mma128<KM, KM, 4>(tmem + 128 * c, sptr(Qs), sptr(Kr + s * kPair), a.id_s);
-      commit(&kfree[s]);
-      if (c + 2 < nk) {
-        mbar_wait(&kfree[s], (uint32_t)((c >> 1) & 1));
-        mbar_expect_tx(&kfull[s], (uint32_t)kPair);
-        tma_load_3d(Kr + s * kPair, &mk, h * 64, (c + 2) * 128, b, &kfull[s]);
-      }
+      mma128<KM, KM, 4>(tmem + 128 * c, sptr(Qs), sptr(Kr + c * kPair), a.id_s);
     }
     commit(&bar_s);
   }
@@ -1266,15 +1258,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
     __syncthreads();                 // P_c complete; S_c read (and S_0 before O lands)
     if (threadIdx.x == 0) {
       tc_after();
-      mbar_wait(&vfull[c & 1], (uint32_t)((c >> 1) & 1));
-      mma_k128_acc<KM>(tmem, sptr(Pr + ps * 2 * kPair), sptr(Vr + (c & 1) * kPair), a.id128_pv,
+      mbar_wait(&vfull[c], 0);
+      mma_k128_acc<KM>(tmem, sptr(Pr + ps * 2 * kPair), sptr(Vr + c * kPair), a.id128_pv,
                        c > 0);
       commit(&pfree[ps]);
-      if (c + 2 < nk) {              // the V slot is free once this MMA completes
-        mbar_wait(&pfree[ps], (uint32_t)((c >> 1) & 1));
-        mbar_expect_tx(&vfull[c & 1], (uint32_t)kPair);
-        tma_load_3d(Vr + (c & 1) * kPair, &mv, h * 64, (c + 2) * 128, b, &vfull[c & 1]);
-      }
     }
     __syncwarp();
   }
@@ -1328,10 +1315,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_dq_kernel(
   uint8_t* Qs = sm;                        // doubles as the dQ staging
   uint8_t* Ds = sm + kPair;                // dO
   uint8_t* Os = sm + 2 * kPair;            // O (for D)
-  uint8_t* Kr = sm + 3 * kPair;            // 2 slots
-  uint8_t* Vr = sm + 5 * kPair;            // 2 slots
-  uint8_t* Sr = sm + 7 * kPair;            // dS: 2 slots x 2 chunks
-  __shared__ __align__(8) uint64_t bar_ld, kvfull[2], dsfree[2], bar_sd, bar_q;
+  uint8_t* Kr = sm + 3 * kPair;            // one slot per key chunk (<= 4)
+  uint8_t* Vr = sm + 7 * kPair;            // one slot per key chunk
+  uint8_t* Sr = sm + 11 * kPair;           // dS (2 chunks)
+  __shared__ __align__(8) uint64_t bar_ld, kvfull[kFlashMaxChunks], dsfree, bar_sd, bar_q;
   __shared__ uint32_t tmem_base;
   __shared__ float xr[256];
   __shared__ float red[256];
@@ -1341,14 +1328,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_dq_kernel(
   const int b = bh / a.H, h = bh % a.H;
   const int nk = (a.Lk + 127) / 128;
   if (threadIdx.x == 0) {
-    mbar_init(&bar_ld, 1); mbar_init(&bar_sd, 1); mbar_init(&bar_q, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&kvfull[i], 1); mbar_init(&dsfree[i], 1); }
+    mbar_init(&bar_ld, 1); mbar_init(&bar_sd, 1); mbar_init(&bar_q, 1); mbar_init(&dsfree, 1);
+    for (int i = 0; i < kFlashMaxChunks; ++i) mbar_init(&kvfull[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_expect_tx(&bar_ld, (uint32_t)(3 * kPair));
     tma_load_3d(Qs, &mq, h * 64, qb * 128, b, &bar_ld);
     tma_load_3d(Ds, &mdo, h * 64, qb * 128, b, &bar_ld);
     tma_load_3d(Os, &mo, h * 64, qb * 128, b, &bar_ld);
-    for (int c = 0; c < nk && c < 2; ++c) {
+    for (int c = 0; c < nk; ++c) {
       mbar_expect_tx(&kvfull[c], (uint32_t)(2 * kPair));
       tma_load_3d(Kr + c * kPair, &mk, h * 64, c * 128, b, &kvfull[c]);
       tma_load_3d(Vr + c * kPair, &mv, h * 64, c * 128, b, &kvfull[c]);
@@ -1383,18 +1370,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_dq_kernel(
   if (ok && half == 0) { stv.z = D; *st4 = stv; }
   const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
   for (int c = 0; c < nk; ++c) {
-    const int s = c & 1;
     if (threadIdx.x == 0) {
-      mbar_wait(&kvfull[s], (uint32_t)((c >> 1) & 1));
+      mbar_wait(&kvfull[c], 0);
       tc_after();
-      mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Kr + s * kPair), a.id_s);           // S
-      mma128<KM, KM, 4>(tmem + 128, sptr(Ds), sptr(Vr + s * kPair), a.id_s);     // dP
+      mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Kr + c * kPair), a.id_s);           // S
+      mma128<KM, KM, 4>(tmem + 128, sptr(Ds), sptr(Vr + c * kPair), a.id_s);     // dP
       commit(&bar_sd);
     }
     __syncwarp();
     mbar_wait(&bar_sd, (uint32_t)(c & 1));
     tc_after();
-    if (c >= 2) mbar_wait(&dsfree[s], (uint32_t)(((c - 2) >> 1) & 1));
+    if (c >= 1) mbar_wait(&dsfree, (uint32_t)((c - 1) & 1));   // dS buffer read
     uint32_t w[32];
     {
       float x[64], dp[64];
@@ -1415,21 +1401,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_dq_kernel(
         w[j] = pack_h2(v2[0], v2[1]);
       }
     }
-    st_row64(Sr + s * 2 * kPair + half * kPair, m, w);
+    st_row64(Sr + half * kPair, m, w);
     fence_async_smem();
     tc_before();
     __syncthreads();                 // dS_c complete; S, dP read
     if (threadIdx.x == 0) {
       tc_after();
-      mma_k128_acc<KM>(tmem + 256, sptr(Sr + s * 2 * kPair), sptr(Kr + s * kPair), a.id128_pv,
+      mma_k128_acc<KM>(tmem + 256, sptr(Sr), sptr(Kr + c * kPair), a.id128_pv,
                        c > 0);                                                   // dQ += dS K
-      commit(&dsfree[s]);
-      if (c + 2 < nk) {
-        mbar_wait(&dsfree[s], (uint32_t)((c >> 1) & 1));
-        mbar_expect_tx(&kvfull[s], (uint32_t)(2 * kPair));
-        tma_load_3d(Kr + s * kPair, &mk, h * 64, (c + 2) * 128, b, &kvfull[s]);
-        tma_load_3d(Vr + s * kPair, &mv, h * 64, (c + 2) * 128, b, &kvfull[s]);
-      }
+      commit(&dsfree);
     }
     __syncwarp();
   }

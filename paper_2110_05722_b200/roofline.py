@@ -40,6 +40,14 @@ def algo_table(tokens: int, d: int, f: int, vocab: int, batch: int, length: int,
          4 * N * D * 2 + N * H * 8),
         (r"attn_tc128_bwd_kernel", "fused attention bwd, tcgen05, 128-row tiles (+ bias partials)",
          7 * N * D * 2 + N * H * 8),
+        (r"attn_flash_fwd_kernel", "flash attention fwd, tcgen05 (L <= 512; scores in TMEM only)",
+         4 * N * D * 2 + N * H * 16),
+        (r"attn_flash_dq_kernel", "flash attention bwd, dQ pass (+ D = rowsum(dO*O))",
+         6 * N * D * 2 + N * H * 16),
+        (r"attn_flash_dkv_kernel", "flash attention bwd, dK/dV pass",
+         6 * N * D * 2 + N * H * 16),
+        (r"softmax_rows", "attention softmax fwd (unfused path)", 2 * B * H * L * L * 2),
+        (r"softmax_bwd_rows", "attention softmax bwd (unfused path)", 3 * B * H * L * L * 2),
         (r"attn_fwd_kernel", "fused attention fwd, mma.sync (QK^T, mask, softmax, PV)",
          4 * N * D * 2 + BHL2 * 2),
         (r"attn_bwd_kernel|attn_bwd_persist", "fused attention bwd, mma.sync",
