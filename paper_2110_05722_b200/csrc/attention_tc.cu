@@ -1201,38 +1201,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
   const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
   mbar_wait(&bar_s, 0);
   tc_after();
-  // row statistics over every chunk (log2 domain)
-  float mx = -INFINITY, z = 0.f;
+  // pass 1: the row maximum over every chunk (log2 domain; no exponentials)
+  float mx = -INFINITY;
   for (int c = 0; c < nk; ++c) {
     float x[64];
     tmem_ld64(tlane + 128 * c + 64 * half, x);
     const int k0 = 128 * c + 64 * half;
-    float cm = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      x[j] = (ok && k0 + j < nkeep) ? __fmul_rn(x[j], a.scale) : -INFINITY;
-      cm = fmaxf(cm, x[j]);
-    }
-    if (cm > mx) {
-      z = mx == -INFINITY ? 0.f : z * ex2(__fsub_rn(mx, cm));
-      mx = cm;
-    }
-#pragma unroll
-    for (int j = 0; j < 64; ++j) z += x[j] == -INFINITY ? 0.f : ex2(__fsub_rn(x[j], mx));
+    for (int j = 0; j < 64; ++j)
+      if (ok && k0 + j < nkeep) mx = fmaxf(mx, __fmul_rn(x[j], a.scale));
   }
-  {
-    const float om = partner_pair(xm, q, half, lane, mx);
-    const float oz = partner_pair(xz, q, half, lane, z);
-    const float M = fmaxf(mx, om);
-    z = (mx == -INFINITY ? 0.f : z * ex2(__fsub_rn(mx, M))) +
-        (om == -INFINITY ? 0.f : oz * ex2(__fsub_rn(om, M)));
-    mx = M;
-  }
-  const float iz = z > 0.f ? 1.f / z : 0.f;
-  if (ok && half == 0) {
-    float4* st4 = reinterpret_cast<float4*>(a.stats) + ((int64_t)b * a.H + h) * a.Lq + qpos;
-    *st4 = make_float4(mx, iz, 0.f, 0.f);
-  }
+  mx = fmaxf(mx, partner_pair(xm, q, half, lane, mx));
+  // pass 2 (below): P = exp2(s - max) unnormalised (<= 1) into the ring, its row
+  // sum on the side; O is divided by the sum when it leaves TMEM, so every score
+  // takes ONE exponential
+  float z = 0.f;
   // P_c -> ring, O += P_c V_c
   for (int c = 0; c < nk; ++c) {
     const int ps = c & 1;
@@ -1247,10 +1230,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int kk = k0 + 2 * j + e;
-        p2[e] = (ok && kk < nkeep) ? __fmul_rn(ex2(__fsub_rn(__fmul_rn(x[2 * j + e], a.scale), mx)), iz)
-                                   : 0.f;
+        p2[e] = (ok && kk < nkeep) ? ex2(__fsub_rn(__fmul_rn(x[2 * j + e], a.scale), mx)) : 0.f;
       }
       w[j] = pack_h2(p2[0], p2[1]);
+      // the sum of the STORED (fp16-rounded) probabilities normalises O = P V
+      const float2 pr = unpack_h2(w[j]);
+      z += pr.x + pr.y;
     }
     st_row64(Pr + ps * 2 * kPair + half * kPair, m, w);
     fence_async_smem();
@@ -1267,11 +1252,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_flash_fwd_kernel(
   }
   if (threadIdx.x == 0) commit(&bar_o);
   __syncwarp();
+  z += partner_pair(xz, q, half, lane, z);
+  const float iz = z > 0.f ? 1.f / z : 0.f;
+  if (ok && half == 0) {
+    float4* st4 = reinterpret_cast<float4*>(a.stats) + ((int64_t)b * a.H + h) * a.Lq + qpos;
+    *st4 = make_float4(mx, iz, 0.f, 0.f);
+  }
   mbar_wait(&bar_o, 0);
   tc_after();
   {
     float o[32];
     tmem_ld32(tlane + 32 * half, o);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = __fmul_rn(o[j], iz);
     st_cols_f(Qs, m, half, o);
   }
   fence_async_smem();
