@@ -206,7 +206,7 @@ class DataParallel:
     communicator), so the overlapped step can be tested on a single GPU."""
 
     def __init__(self, group=None, bucket_bytes: int = 16 << 20, force: bool = False,
-                 mode: str | None = None):
+                 mode: str | None = None, native: bool = True):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -216,6 +216,10 @@ class DataParallel:
         if mode not in MODES:
             raise ValueError(f"data-parallel mode must be one of {MODES}, got {mode!r}")
         self.mode = mode
+        # native=False: the collectives go through torch.distributed (e.g. gloo on
+        # CUDA tensors, several ranks sharing one GPU in the tests) instead of the
+        # NCCL binding; the step then runs eagerly (no CUDA graph)
+        self.native = bool(native)
         self.comm: NcclComm | None = None
         self.comm_stream = None
 
@@ -225,8 +229,9 @@ class DataParallel:
 
     def setup_device(self, device):
         """Create the native communicator and the comm stream (CUDA only)."""
-        if self.active and self.comm is None:
-            self.comm = NcclComm(self.rank, self.world, device, self.group)
+        if self.active and self.comm is None and self.comm_stream is None:
+            if self.native:
+                self.comm = NcclComm(self.rank, self.world, device, self.group)
             # default priority: the exchange's kernels take SMs the backward leaves
             # free instead of pre-empting it (measured on one rank: high priority
             # slowed the backward by more than the exchange's own time;
@@ -269,10 +274,13 @@ class DataParallel:
             self.comm.reduce_scatter(flat, start, stop, stream=stream)
         elif self.world > 1:
             c = (stop - start) // self.world
+            o = start + self.rank * c
+            if flat.is_cuda:      # gloo on CUDA tensors: a sum of the whole span, keep our chunk
+                dist.all_reduce(flat[start:stop], op=dist.ReduceOp.SUM, group=self.group)
+                return
             out = torch.empty(c, dtype=flat.dtype, device=flat.device)
             dist.reduce_scatter_tensor(out, flat[start:stop].contiguous(), op=dist.ReduceOp.SUM,
                                        group=self.group)
-            o = start + self.rank * c
             flat[o:o + c].copy_(out)
 
     def all_gather_span(self, flat: torch.Tensor, start: int, stop: int, stream=None):
@@ -281,6 +289,12 @@ class DataParallel:
         elif self.world > 1:
             c = (stop - start) // self.world
             o = start + self.rank * c
+            if flat.is_cuda:      # gloo on CUDA tensors: everyone else's chunks zeroed, summed
+                buf = torch.zeros(stop - start, dtype=flat.dtype, device=flat.device)
+                buf[o - start:o - start + c].copy_(flat[o:o + c])
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+                flat[start:stop].copy_(buf)
+                return
             out = torch.empty(stop - start, dtype=flat.dtype, device=flat.device)
             dist.all_gather_into_tensor(out, flat[o:o + c].contiguous(), group=self.group)
             flat[start:stop].copy_(out)
