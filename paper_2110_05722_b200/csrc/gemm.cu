@@ -76,6 +76,17 @@ __global__ void fill_ptrs_kernel(const char* A, const char* B, char* C, int64_t 
   }
 }
 
+// pointer lists of ls2_gemm_list travel by value in the kernel's parameters (so
+// a captured graph replays them without any host memory)
+constexpr int kMaxList = 64;
+struct PtrList {
+  const void* p[3 * kMaxList];
+};
+
+__global__ void fill_list_kernel(PtrList l, int n, const void** out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = l.p[i];
+}
+
 inline int blas_fail(cublasStatus_t s, const char* what) {
   return fail(LS2_ERR_CUBLAS, std::string(what) + ": cublas status " + std::to_string((int)s));
 }
@@ -468,6 +479,43 @@ int ls2_gemm(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k
                           (void* const*)(ptrs + 2 * total), tC, (int)ldc, (int)total, ct,
                           CUBLAS_GEMM_DEFAULT);
   return s == CUBLAS_STATUS_SUCCESS ? LS2_OK : blas_fail(s, "cublasGemmBatchedEx");
+}
+
+int ls2_gemm_list(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                  double alpha, const void* const* a_list, int64_t lda, const void* const* b_list,
+                  int64_t ldb, double beta, void* const* c_list, int64_t ldc, int count, int tab,
+                  int tc, void* ptr_scratch, void* stream) {
+  Blas* b = reinterpret_cast<Blas*>(hp);
+  if (!b) return fail(LS2_ERR_CUBLAS, "gemm_list: null blas handle");
+  if (count <= 0 || m <= 0 || n <= 0) return LS2_OK;
+  if (count > kMaxList) return fail(LS2_ERR_SHAPE, "gemm_list: at most 64 products per call");
+  if (!a_list || !b_list || !c_list) return fail(LS2_ERR_SHAPE, "gemm_list: null pointer list");
+  if (tab == LS2_F64 || tc == LS2_F64) return fail(LS2_ERR_DTYPE, "gemm_list: f64 not batched");
+  if (!(tc == tab || tc == LS2_F32)) return fail(LS2_ERR_DTYPE, "gemm_list: bad output dtype");
+  if (count == 1)
+    return lt_matmul(b, trans_a, trans_b, m, n, k, alpha, a_list[0], lda, b_list[0], ldb, beta,
+                     c_list[0], ldc, nullptr, tab, tc, as_stream(stream));
+  if (!ptr_scratch) return fail(LS2_ERR_SHAPE, "gemm_list: needs pointer scratch");
+  PtrList l;
+  for (int i = 0; i < count; ++i) {
+    l.p[i] = a_list[i];
+    l.p[count + i] = b_list[i];
+    l.p[2 * count + i] = c_list[i];
+  }
+  const void** ptrs = reinterpret_cast<const void**>(ptr_scratch);
+  fill_list_kernel<<<1, 256, 0, as_stream(stream)>>>(l, 3 * count, ptrs);
+  int rc = check_launch("gemm_fill_list");
+  if (rc) return rc;
+  cublasSetStream(b->h, as_stream(stream));
+  const float af = (float)alpha, bf = (float)beta;
+  const cublasOperation_t opA = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cublasOperation_t opB = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cudaDataType_t tAB = cuda_type(tab), tC = cuda_type(tc);
+  cublasStatus_t s = cublasGemmBatchedEx(
+      b->h, opB, opA, (int)n, (int)m, (int)k, &af, (const void* const*)(ptrs + count), tAB,
+      (int)ldb, (const void* const*)ptrs, tAB, (int)lda, &bf, (void* const*)(ptrs + 2 * count),
+      tC, (int)ldc, count, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  return s == CUBLAS_STATUS_SUCCESS ? LS2_OK : blas_fail(s, "cublasGemmBatchedEx(list)");
 }
 
 }  // extern "C"

@@ -149,6 +149,13 @@ class TrainingEngine:
         # by default: measured 1% slower at T-base, because the one-wave fused
         # kernels cannot co-reside with a concurrent GEMM's CTAs
         self.use_lane = os.environ.get("LS2_WGRAD_LANE", "0") == "1"
+        # weight-gradient GEMMs batched across layers (model._WgradBatch):
+        # LS2_WGRAD_BATCH=0 off, =k flush every k layers, =end once at the end of
+        # backward; default: at the end, every 2 layers under data parallelism
+        # (so the bucket exchange still overlaps the rest of backward)
+        wb = os.environ.get("LS2_WGRAD_BATCH", "auto")
+        self.wgrad_group = None if wb == "0" else 0 if wb == "end" else \
+            ((2 if self.dp.active else 0) if wb == "auto" else int(wb))
         # every forward dropout site of a step drawn by one launch (model.MaskBank)
         self.masks = MaskBank(self.device) if os.environ.get("LS2_MASK_BANK", "1") != "0" else None
         # next step's site seeds: the bank draws step t+1's bits beside step t's Adam
@@ -173,7 +180,8 @@ class TrainingEngine:
 
     def _record_shape(self, batch: Batch, compute_grads: bool):
         rec = RecordingArena(self.device)
-        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane) if compute_grads else None
+        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane,
+                         wgrad_group=self.wgrad_group) if compute_grads else None
         self.model.forward_backward(self.pviews, batch,
                                     p_drop=self.cfg.train.p_drop if compute_grads else 0.0,
                                     alpha=self.cfg.train.alpha, seed=self.cfg.train.seed,
@@ -242,7 +250,7 @@ class TrainingEngine:
                 nx.dev[:n].copy_(nx.host[:n], non_blocking=True)
             self._consumed.record()
         self.arena.begin(key)
-        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane)
+        sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane, wgrad_group=self.wgrad_group)
         self._bank_done = None
         if self.masks is not None and self._early_masks and t.p_drop > 0.0:
             # the next step's dropout bits, layer by layer as backward releases them

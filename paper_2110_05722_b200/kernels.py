@@ -12,6 +12,7 @@ materializes the dense 0/1 tensor on demand.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from dataclasses import dataclass, field
@@ -636,6 +637,44 @@ def _joint_levels(views):
     while len(dims) < 2:
         dims.insert(0, (1, [0] * len(views)))
     return dims
+
+
+def gemm_list(a_list, b_list, outs, trans_a: bool = False, trans_b: bool = False,
+              alpha: float = 1.0, beta: float = 0.0):
+    """outs[i] = alpha * op(a_list[i]) @ op(b_list[i]) + beta * outs[i] for products
+    of ONE shape and layout at unrelated addresses, as cuBLAS pointer-array
+    batches of up to 64 (ls2_gemm_list).  Contiguous 2-D CUDA operands only."""
+    ctx = _lib.context()
+    if not (len(a_list) == len(b_list) == len(outs)) or not a_list:
+        raise ShapeMismatch("gemm_list: operand lists differ in length or are empty")
+    a0, b0, c0 = a_list[0], b_list[0], outs[0]
+    for group in (a_list, b_list, outs):
+        for t in group:
+            if t.dim() != 2 or not t.is_contiguous() or not t.is_cuda:
+                raise ShapeMismatch("gemm_list: contiguous 2-D CUDA operands only")
+            if t.shape != group[0].shape or t.dtype != group[0].dtype:
+                raise ShapeMismatch("gemm_list: every product must have one shape and dtype")
+    if a0.dtype != b0.dtype:
+        raise ShapeMismatch("gemm_list: A and B dtypes differ")
+    m, k = (a0.shape[1], a0.shape[0]) if trans_a else tuple(a0.shape)
+    kb, n = (b0.shape[1], b0.shape[0]) if trans_b else tuple(b0.shape)
+    if k != kb or tuple(c0.shape) != (m, n):
+        raise ShapeMismatch(f"gemm_list: op(A) {m}x{k}, op(B) {kb}x{n}, C {tuple(c0.shape)}")
+    for lo in range(0, len(a_list), 64):
+        A, B, C = a_list[lo:lo + 64], b_list[lo:lo + 64], outs[lo:lo + 64]
+        cnt = len(A)
+        key = ("list",) + tuple(t.data_ptr() for t in A + B + C)
+        scratch = ctx.ptr_cache.get(key)
+        if scratch is None:
+            scratch = torch.empty(3 * cnt, dtype=torch.int64, device=ctx.device)
+            ctx.ptr_cache[key] = scratch
+        arr = ctypes.c_void_p * cnt
+        _lib.call("ls2_gemm_list", ctx.blas_handle(), int(trans_a), int(trans_b), m, n, k,
+                  float(alpha), arr(*[t.data_ptr() for t in A]), a0.shape[1],
+                  arr(*[t.data_ptr() for t in B]), b0.shape[1], float(beta),
+                  arr(*[t.data_ptr() for t in C]), n, cnt, _lib.dtype_code(a0),
+                  _lib.dtype_code(c0), scratch.data_ptr(), _lib.stream_handle())
+    return outs
 
 
 def gemm(a, b, trans_a: bool = False, trans_b: bool = False, accumulate_into=None, out=None,

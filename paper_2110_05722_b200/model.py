@@ -351,9 +351,13 @@ class _ViewSink(GradSink):
     """Writes into preallocated views of the fp32 gradient workspace; the first
     producer of a name overwrites (beta=0), later producers accumulate."""
 
-    def __init__(self, store: dict, defer: bool = False, lane: bool = False):
+    def __init__(self, store: dict, defer: bool = False, lane: bool = False,
+                 wgrad_group: int | None = None):
         super().__init__(store)
         self.use_lane = bool(lane)
+        # weight-gradient GEMMs batched across layers (_WgradBatch): flushed every
+        # `wgrad_group` layers (0: only at the end of backward); None: off
+        self.wgrad_group = wgrad_group
         self.written: set = set()
         # deferred column sums: the producer leaves per-block partials in an arena
         # buffer and the engine finishes them all inside the fp16 narrow pass
@@ -376,7 +380,14 @@ class _ViewSink(GradSink):
                 [n for n in self.store if any(n.startswith(p) for p in prefixes)]
             self.on_ready(names)
 
+    def _settle(self, name: str):
+        """A second producer of `name` writes now: issue its pending batched GEMM."""
+        lane = self.lane
+        if lane is not None and name in getattr(lane, "pending", ()):
+            lane.flush()
+
     def add(self, name: str, value):
+        self._settle(name)
         if name in self.written:
             self.store[name] += value
         else:
@@ -384,12 +395,15 @@ class _ViewSink(GradSink):
             self.written.add(name)
 
     def target(self, name: str):
+        self._settle(name)
         beta = 1 if name in self.written else 0
         self.written.add(name)
         return self.store[name], beta
 
     def defer_buffer(self, names, nblk: int, np_: int, cols: int):
         """Arena buffer for nblk x np_ x cols partials of `names`, or None."""
+        for n in names:
+            self._settle(n)
         if not self.defer_enabled or self.arena is None or nblk <= 0 or \
                 any(n in self.written for n in names):
             return None
@@ -427,6 +441,12 @@ class _Lane:
         self.deferred: list = []
         self.pending = False
 
+    def wgrad(self, name, dy2d, x2d, out2d, beta):
+        self.run(lambda: K.gemm(dy2d, x2d, trans_a=True, out=out2d, beta=float(beta)), dy2d, x2d)
+
+    def postpone(self, prefixes) -> bool:
+        return False
+
     def run(self, fn, *reads):
         ev = torch.cuda.Event()
         ev.record(self.main)
@@ -454,6 +474,104 @@ class _Lane:
             self.arena.free(t)
         self.deferred.clear()
 
+    flush = join
+
+
+class _WgradBatch:
+    """Weight-gradient GEMMs batched across layers (engine path).
+
+    dW = dy^T x is consumed only by the optimizer (or by the data-parallel
+    exchange of its bucket), so `_wgrad` enqueues it here and `flush()` issues
+    every pending product of one shape as ONE cuBLAS pointer-array batch
+    (K.gemm_list): the Transformer-base step's 24 [512 x 512] x 4096 weight
+    gradients take ~55 us as one batch against ~215 us one by one, the FFN ones
+    84 vs 153 us per 12 (profiles/r3a_wgrad_batch.jsonl).  The engine flushes
+    every `group` layers (0: once, at the end of backward).  Like the lane, the
+    arena buffers a pending GEMM reads are held (their frees wait for the
+    flush, in the planner's dry run too), and the readiness of the layers whose
+    gradients are pending (`_ready`: the DP exchange of their buckets) is
+    postponed to the flush.  Products with large outputs (the vocabulary
+    projection) gain nothing from batching and run at once."""
+
+    MAX_OUT = 1 << 22          # outputs of more elements run immediately
+
+    def __init__(self, arena, group: int):
+        self.arena, self.group = arena, int(group)
+        self.items: list = []          # (name, dy2d, x2d, out2d, beta)
+        self.pending: set = set()
+        self.held: set = set()
+        self.deferred: list = []
+        self.ready_q: list = []
+        self.sink = None
+        self.layers = 0
+
+    def wgrad(self, name, dy2d, x2d, out2d, beta):
+        if out2d.numel() > self.MAX_OUT or not all(t.is_contiguous() for t in (dy2d, x2d, out2d)):
+            K.gemm(dy2d, x2d, trans_a=True, out=out2d, beta=float(beta))
+            return
+        self.items.append((name, dy2d, x2d, out2d, float(beta)))
+        self.pending.add(name)
+        self.held.add(dy2d.data_ptr())
+        self.held.add(x2d.data_ptr())
+
+    def free(self, t):
+        if t.data_ptr() in self.held:
+            self.deferred.append(t)
+        else:
+            self.arena.free(t)
+
+    def postpone(self, prefixes) -> bool:
+        if not self.items:
+            return False
+        self.ready_q.append(prefixes)
+        return True
+
+    def join(self):
+        self.layers += 1
+        if self.group > 0 and self.layers >= self.group:
+            self.flush()
+
+    def flush(self):
+        groups: dict = {}
+        for name, dy, x, out, beta in self.items:
+            key = (tuple(dy.shape), tuple(x.shape), dy.dtype, out.dtype, beta)
+            groups.setdefault(key, []).append((dy, x, out))
+        for (_, _, _, _, beta), its in groups.items():
+            K.gemm_list([i[0] for i in its], [i[1] for i in its], [i[2] for i in its],
+                        trans_a=True, beta=beta)
+        self.items.clear()
+        self.pending.clear()
+        self.layers = 0
+        self.held.clear()
+        for t in self.deferred:
+            self.arena.free(t)
+        self.deferred.clear()
+        q, self.ready_q = self.ready_q, []
+        for prefixes in q:
+            _ready_now(self.sink, prefixes)
+
+
+def _open_lane(sink, arena, dt):
+    """(lane, arena facade, join) for the backward pass: the side-stream lane
+    (LS2_WGRAD_LANE=1), the cross-layer weight-gradient batch, or neither."""
+    if dt == torch.float64:
+        return None, arena, (lambda: None)
+    if getattr(sink, "use_lane", False):
+        lane = _Lane(arena)
+    elif getattr(sink, "wgrad_group", None) is not None:
+        lane = _WgradBatch(arena, sink.wgrad_group)
+        lane.sink = sink
+    else:
+        return None, arena, (lambda: None)
+    sink.lane = lane
+    return lane, _LaneArena(arena, lane), lane.join
+
+
+def _close_lane(sink, lane):
+    if lane is not None:
+        lane.flush()
+        sink.lane = None
+
 
 class _LaneArena:
     """Arena facade whose frees respect the lane's holds."""
@@ -472,9 +590,17 @@ class _LaneArena:
 
 
 def _ready(sink, *prefixes):
+    pre = list(prefixes) if prefixes != (None,) else None
+    lane = getattr(sink, "lane", None)
+    if lane is not None and lane.postpone(pre):
+        return                       # its weight gradients are still pending
+    _ready_now(sink, pre)
+
+
+def _ready_now(sink, prefixes):
     fn = getattr(sink, "ready", None)
     if fn is not None:
-        fn(list(prefixes) if prefixes != (None,) else None)
+        fn(prefixes)
 
 
 def _defer(sink, names, nblk, np_, cols):
@@ -493,20 +619,19 @@ def _colsum_nblk(rows, cols, t) -> int:
 
 
 def _wgrad(sink, name, dy2d, x2d):
-    """dW = dy^T x straight into the sink (cuBLAS, fp32 output); on the sink's
-    side lane when it has one."""
+    """dW = dy^T x straight into the sink (cuBLAS, fp32 output); through the
+    sink's lane (side stream or cross-layer batch) when it has one."""
     tgt = sink.target(name)
     if tgt is None:
         sink.add(name, K.gemm(dy2d, x2d, trans_a=True))
         return
     v, beta = tgt
-    go = lambda: K.gemm(dy2d, x2d, trans_a=True, out=v.view(dy2d.shape[1], x2d.shape[1]),  # noqa: E731
-                        beta=float(beta))
+    out2d = v.view(dy2d.shape[1], x2d.shape[1])
     lane = getattr(sink, "lane", None)
     if lane is not None:
-        lane.run(go, dy2d, x2d)
+        lane.wgrad(name, dy2d, x2d, out2d, beta)
     else:
-        go()
+        K.gemm(dy2d, x2d, trans_a=True, out=out2d, beta=float(beta))
 
 
 def _colsum_grad(sink, name, x2d):
@@ -1645,15 +1770,10 @@ class Transformer:
             return out
 
         # --- backward: output projection ---
-        # weight-gradient GEMMs go to the side lane (engine path); frees of the
-        # buffers they read are held until the lane joins after each layer
-        lane = None
+        # weight-gradient GEMMs go through the sink's lane (engine path: batched
+        # across layers); frees of the buffers they read are held until it flushes
         main_arena = arena
-        if getattr(sink, "use_lane", False) and dt != torch.float64:
-            lane = _Lane(arena)
-            sink.lane = lane
-            arena = _LaneArena(arena, lane)
-        join = lane.join if lane is not None else (lambda: None)
+        lane, arena, join = _open_lane(sink, arena, dt)
         dlogits = logits
         dec_out = stash.pop("dec_out")
         ddec = arena.alloc((b, lt, d), dt)
@@ -1739,9 +1859,8 @@ class Transformer:
         self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
         arena.free(dh); arena.free(keep_src)
         join()
+        _close_lane(sink, lane)
         _ready(sink, None)
-        if lane is not None:
-            sink.lane = None
         arena = main_arena
         if len(stash):
             raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")
@@ -1930,13 +2049,8 @@ class EncoderMLM(Transformer):
             return out
 
         # --- backward ---
-        lane = None
         main_arena = arena
-        if getattr(sink, "use_lane", False) and dt != torch.float64:
-            lane = _Lane(arena)
-            sink.lane = lane
-            arena = _LaneArena(arena, lane)
-        join = lane.join if lane is not None else (lambda: None)
+        lane, arena, join = _open_lane(sink, arena, dt)
         denc = arena.alloc((b, ls, d), dt)
         K.gemm(logits_buf[:, :va], tok_emb[:va], out=denc.view(rt, d))   # K-split as above
         if va != v:
@@ -1967,9 +2081,8 @@ class EncoderMLM(Transformer):
         self._embedding_grads(sink, dh, src, keep_src, p_drop, emb_cfg)
         arena.free(dh); arena.free(keep_src)
         join()
+        _close_lane(sink, lane)
         _ready(sink, None)
-        if lane is not None:
-            sink.lane = None
         arena = main_arena
         if len(stash):
             raise ShapeMismatch(f"activation stash leaked {len(stash)} entries")

@@ -417,3 +417,33 @@ def test_engine_file_task(tmp_path):
     ms = [eng.train_step(s) for s in range(60)]
     assert all(np.isfinite(m.loss) for m in ms)
     assert np.mean([m.loss for m in ms[-8:]]) < np.mean([m.loss for m in ms[:8]])
+
+
+@pytest.mark.parametrize("group", ["0", "3"])
+def test_wgrad_batch_matches_per_layer_gemms(monkeypatch, group):
+    """Weight gradients batched across layers (model._WgradBatch: pointer-array
+    cuBLAS batches, flushed at the end of backward or every 3 layers, the
+    readiness of their layers postponed) vs one GEMM per weight (LS2_WGRAD_BATCH=0):
+    the same products, so losses agree and parameters agree up to fp32 summation
+    order and the embedding atomics; T-base shapes, captured graphs."""
+    from paper_2110_05722_b200.config import transformer_base
+    from paper_2110_05722_b200.data import FixedShapeTask
+
+    def run(env):
+        monkeypatch.setenv("LS2_WGRAD_BATCH", env)
+        cfg = RunConfig(model=transformer_base(), train=TrainConfig(p_drop=0.1, batch_tokens=4096))
+        eng = TrainingEngine(cfg, task=FixedShapeTask(64, 64, 32000))
+        eng.setup_arena()
+        return eng, [eng.train_step(s) for s in range(4)]
+
+    e1, m1 = run("0")
+    e2, m2 = run("auto" if group == "0" else group)
+    assert e1.wgrad_group is None and e2.wgrad_group == int(group)
+    for a, b in zip(m1, m2):
+        assert abs(a.loss - b.loss) <= 1e-4 * abs(a.loss), (a.step, a.loss, b.loss)
+        assert not b.skipped
+    g1, g2 = H(e1.ws.grads16).astype(np.float32), H(e2.ws.grads16).astype(np.float32)
+    assert np.linalg.norm(g1 - g2) <= 1e-3 * np.linalg.norm(g1)
+    p1, p2 = H(e1.ws.params16).astype(np.float32), H(e2.ws.params16).astype(np.float32)
+    assert np.abs(p1 - p2).max() <= 2e-3
+    assert e2.arena.realloc_count == 0 and e2.arena.high_water <= e2.capacity

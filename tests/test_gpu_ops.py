@@ -476,6 +476,29 @@ def test_gemm_known_and_errors():
         K.gemm(C(np.zeros((2, 3))), C(np.zeros((4, 2))))
 
 
+
+@pytest.mark.parametrize("count,m,n,k,beta", [(24, 512, 512, 4096, 0.0), (3, 64, 96, 200, 1.0),
+                                              (70, 32, 48, 64, 0.0), (1, 128, 64, 256, 1.0)])
+def test_gemm_list_pointer_batches_vs_torch(count, m, n, k, beta):
+    """K.gemm_list / ls2_gemm_list: dW_i = dy_i^T x_i (+ beta dW_i) for operands at
+    unrelated addresses (pointer-array batches of <= 64, the list travelling in a
+    kernel's parameters); fp16 in, fp32 out, vs torch fp32.  count 70 spans two
+    batches, count 1 takes the single-GEMM cuBLASLt plan."""
+    g = torch.Generator(device="cuda").manual_seed(count)
+    dys = [torch.randn(k, m, device="cuda", generator=g).half() for _ in range(count)]
+    xs = [torch.randn(k, n, device="cuda", generator=g).half() for _ in range(count)]
+    outs = [torch.randn(m, n, device="cuda", generator=g) for _ in range(count)]
+    before = [o.clone() for o in outs]
+    K.gemm_list(dys, xs, outs, trans_a=True, beta=beta)
+    for dy, x, o, o0 in zip(dys, xs, outs, before):
+        want = dy.float().t() @ x.float() + beta * o0
+        assert ((o - want).abs().max() / want.abs().max()).item() <= 1e-5
+    with pytest.raises(ShapeMismatch):
+        K.gemm_list(dys[:1], xs[:1], [], trans_a=True)
+    with pytest.raises(ShapeMismatch):     # one shape per call
+        K.gemm_list([dys[0], dys[0][:-1]], [xs[0], xs[0][:-1]], [outs[0], outs[0]], trans_a=True)
+
+
 # --- mask bank: every site of a step in one launch ------------------------------------
 
 def test_dropout_bits_multi_matches_reference_rng():
