@@ -80,6 +80,13 @@ int ls2_dropout_bits(uint8_t* bits, int64_t n, uint64_t seed, const uint64_t* se
 int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
                            const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
                            const int64_t* want, void* stream);
+/* the same with at most ctas_per_sm resident CTAs of 256 per SM (0: full
+ * occupancy): the engine draws the next step's bank with 1 CTA per SM beside
+ * the HBM-bound optimizer, so the two kernels share every SM */
+int ls2_dropout_bits_multi_ex(const int64_t* desc, int nsites, int64_t total_words,
+                              uint8_t* base, const uint64_t* seeds, uint64_t thresh,
+                              const int64_t* stamp, const int64_t* want, int ctas_per_sm,
+                              void* stream);
 int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream);
 int ls2_dense_to_bits(const void* dense, int dtype, uint8_t* bits, int64_t n, void* stream);
 

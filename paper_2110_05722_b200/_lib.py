@@ -38,6 +38,7 @@ _SIGS = {
     "ls2_rand_uniform": [P, U, L, L, P],
     "ls2_dropout_bits": [P, L, U, P, U, P],
     "ls2_dropout_bits_multi": [P, I, L, P, P, U, P, P, P],
+    "ls2_dropout_bits_multi_ex": [P, I, L, P, P, U, P, P, I, P],
     "ls2_bits_to_dense": [P, P, I, L, P],
     "ls2_dense_to_bits": [P, I, P, L, P],
     "ls2_bias_dropout_residual_fwd": [P, P, P, P, P, L, L, I, I, U, P, U, D, I, I, P],

@@ -163,23 +163,31 @@ int ls2_dropout_bits(uint8_t* bits, int64_t n, uint64_t seed, const uint64_t* se
   return check_launch("dropout_bits");
 }
 
-int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
-                           const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
-                           const int64_t* want, void* stream) {
+int ls2_dropout_bits_multi_ex(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
+                              const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
+                              const int64_t* want, int ctas_per_sm, void* stream) {
   if (total_words <= 0 || nsites <= 0) return LS2_OK;
   if (nsites > 64) return fail(LS2_ERR_SHAPE, "dropout_bits_multi: at most 64 sites");
   if ((reinterpret_cast<uintptr_t>(base) & 3) != 0)
     return fail(LS2_ERR_SHAPE, "dropout_bits_multi: base must be 4-byte aligned");
-  static int grid = 0;
-  if (!grid) {
+  static int occ = 0;
+  if (!occ) {
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dropout_bits_multi_kernel, 256, 0);
-    grid = kNumSMs * (per > 0 ? per : 8);
+    occ = per > 0 ? per : 8;
   }
-  const int g = (int)std::min<int64_t>(grid, ceil_div(total_words, (int64_t)256));
+  const int per = ctas_per_sm > 0 ? std::min(ctas_per_sm, occ) : occ;
+  const int g = (int)std::min<int64_t>((int64_t)kNumSMs * per, ceil_div(total_words, (int64_t)256));
   dropout_bits_multi_kernel<<<g, 256, 0, as_stream(stream)>>>(
       desc, nsites, total_words, reinterpret_cast<uint32_t*>(base), seeds, thresh, stamp, want);
   return check_launch("dropout_bits_multi");
+}
+
+int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words, uint8_t* base,
+                           const uint64_t* seeds, uint64_t thresh, const int64_t* stamp,
+                           const int64_t* want, void* stream) {
+  return ls2_dropout_bits_multi_ex(desc, nsites, total_words, base, seeds, thresh, stamp, want, 0,
+                                   stream);
 }
 
 int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream) {

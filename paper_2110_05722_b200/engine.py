@@ -161,7 +161,11 @@ class TrainingEngine:
         # next step's site seeds: the bank draws step t+1's bits beside step t's Adam
         self._seeds_next = SeedTable(self.device)
         # LS2_EARLY_MASKS=1: draw the next step's bits layer by layer during backward
-        self._early_masks = os.environ.get("LS2_EARLY_MASKS", "0") == "1"
+        #   =opt (default): the whole bank at once beside this step's narrow pass and
+        #   optimizer (HBM-bound), capped at one CTA per SM so both share every SM;
+        #   =0: in-step draw only
+        self._early_mode = os.environ.get("LS2_EARLY_MASKS", "opt")
+        self._early_masks = self._early_mode in ("1", "opt")
         # host/device overlap: once a step's inputs are on the device (an event
         # recorded inside the graph), the host stages the next step's batch and
         # seeds while the device still runs this one (LS2_OVERLAP_HOST=0: off)
@@ -255,7 +259,8 @@ class TrainingEngine:
         if self.masks is not None and self._early_masks and t.p_drop > 0.0:
             # the next step's dropout bits, layer by layer as backward releases them
             self._bank_table = self._seeds_next if upload else self.model.seed_table(self.device)
-            sink.on_layer_done = self._bank_layer_done
+            if self._early_mode == "1":
+                sink.on_layer_done = self._bank_layer_done
         if self.dp.active:
             # buckets are narrowed / all-reduced on the comm stream while the
             # backward pass is still running (dist.py)
@@ -447,6 +452,24 @@ class TrainingEngine:
             self._bank_done = torch.cuda.Event()
             self._bank_done.record(side)
 
+    def _draw_next_bank(self):
+        """The next step's dropout bits on the side stream, beside this step's
+        narrow pass and optimizer: those are HBM-bound and the draw is integer-ALU
+        bound, so with the draw capped at one CTA per SM the two share every SM
+        (alone: Adam 236 us + draw 167 us; together 274 us,
+        profiles/r3d_overlap.jsonl).  Every read of this step's bits is enqueued
+        before this point; the next step finds the stamp and skips its draw."""
+        bank = self.masks
+        side = _lib.context().side_stream
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            bank.generate(self._bank_table.dev, ctas_per_sm=1)
+            bank.stamp.copy_(self._bank_table.step_slot())
+        self._bank_done = torch.cuda.Event()
+        self._bank_done.record(side)
+
     def _finish_deferred(self, sink, out3, nonfinite_ptr, entries=None):
         """One launch finishing every deferred bias / LayerNorm gradient (partials
         left by their producers) straight into the fp16 workspace."""
@@ -480,6 +503,9 @@ class TrainingEngine:
         t = self.cfg.train
         ws = self.ws
         loss_ptr = out3.data_ptr()
+        if self._early_mode == "opt" and self.masks is not None and \
+                self.masks.desc is not None and t.p_drop > 0.0 and sink is not None:
+            self._draw_next_bank()
         joined = getattr(self, "_bank_done", None)
         if self.dp.active:
             # every bucket was reduced + narrowed + checked on the comm stream;

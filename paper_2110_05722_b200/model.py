@@ -877,12 +877,13 @@ class MaskBank:
         _lib.call("ls2_dropout_bits_multi", desc.data_ptr(), ns, words, self.buf.data_ptr() + off,
                   seeds_dev.data_ptr(), self.thresh, None, None, _lib.stream_handle())
 
-    def generate(self, seeds_dev: torch.Tensor, stamp=None, want=None):
+    def generate(self, seeds_dev: torch.Tensor, stamp=None, want=None, ctas_per_sm: int = 0):
         """Draw every site with the seeds in seeds_dev (skipped on the device
-        when *stamp == *want)."""
-        _lib.call("ls2_dropout_bits_multi", self.desc.data_ptr(), self.nsites, self.words,
+        when *stamp == *want); ctas_per_sm > 0 caps the draw's residency so a
+        concurrent kernel keeps the rest of every SM."""
+        _lib.call("ls2_dropout_bits_multi_ex", self.desc.data_ptr(), self.nsites, self.words,
                   self.buf.data_ptr(), seeds_dev.data_ptr(), self.thresh, _lib.ptr(stamp),
-                  _lib.ptr(want), _lib.stream_handle())
+                  _lib.ptr(want), int(ctas_per_sm), _lib.stream_handle())
 
     def bits(self, seed, n: int):
         """Bank view for the site whose seed is the table slot `seed`, else None."""

@@ -364,7 +364,8 @@ def _run_steps(steps, graphs=True):
     return eng, [eng.train_step(s) for s in steps]
 
 
-@pytest.mark.parametrize("graphs,early", [(True, "1"), (False, "1"), (True, "0")])
+@pytest.mark.parametrize("graphs,early", [(True, "1"), (False, "1"), (True, "0"), (True, "opt"),
+                                          (False, "opt")])
 def test_mask_bank_step_equals_inline_masks(monkeypatch, graphs, early):
     """Engine with the mask bank (every site drawn by one launch, step t+1's bits
     drawn beside step t's Adam) vs inline drawing: same masks, so the same
