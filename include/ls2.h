@@ -337,13 +337,15 @@ int ls2_gemm(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
 /* count (<= 64) independent products of one shape, C_i = alpha op(A_i) op(B_i)
  * + beta C_i, as ONE cuBLAS pointer-array batch.  a_list / b_list / c_list are
  * HOST arrays of device pointers; they reach the device through a kernel's
- * parameters (graph-capturable), ptr_scratch: >= 3*count device pointers.
+ * parameters (graph-capturable), ptr_scratch: >= 3*count device pointers;
+ * ptrs_ready=1: ptr_scratch already holds this list (cached per address list).
  * Used to issue a step's weight-gradient GEMMs batched across layers
  * (replaces the per-layer dW = dy^T x of F/model.py:451,461,479,500,678,688,706). */
 int ls2_gemm_list(void* h, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
                   double alpha, const void* const* a_list, int64_t lda,
                   const void* const* b_list, int64_t ldb, double beta, void* const* c_list,
-                  int64_t ldc, int count, int tab, int tc, void* ptr_scratch, void* stream);
+                  int64_t ldc, int count, int tab, int tc, void* ptr_scratch,
+                  int ptrs_ready, void* stream);
 /* bytes of device scratch ls2_gemm needs for pointer-array batches
  * (ptrs_ready=1: the caller guarantees ptr_scratch already holds this call's
  *  A/B/C pointer arrays, e.g. cached per static arena address) */

@@ -90,7 +90,7 @@ _SIGS = {
     "ls2_blas_create": [],
     "ls2_blas_destroy": [P],
     "ls2_gemm": [P, I, I, L, L, L, D, P, L, L, L, P, L, L, L, D, P, L, L, L, L, L, I, I, P, I, P],
-    "ls2_gemm_list": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, I, I, I, P, P],
+    "ls2_gemm_list": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, I, I, I, P, I, P],
     "ls2_gemm_lt": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, P],
     "ls2_gemm_lt_bgrad": [P, I, I, L, L, L, D, P, L, P, L, D, P, L, P, I, I, I, P],
     "ls2_gemm_scratch_bytes": [L, L],

@@ -484,7 +484,7 @@ int ls2_gemm(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k
 int ls2_gemm_list(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
                   double alpha, const void* const* a_list, int64_t lda, const void* const* b_list,
                   int64_t ldb, double beta, void* const* c_list, int64_t ldc, int count, int tab,
-                  int tc, void* ptr_scratch, void* stream) {
+                  int tc, void* ptr_scratch, int ptrs_ready, void* stream) {
   Blas* b = reinterpret_cast<Blas*>(hp);
   if (!b) return fail(LS2_ERR_CUBLAS, "gemm_list: null blas handle");
   if (count <= 0 || m <= 0 || n <= 0) return LS2_OK;
@@ -496,16 +496,18 @@ int ls2_gemm_list(void* hp, int trans_a, int trans_b, int64_t m, int64_t n, int6
     return lt_matmul(b, trans_a, trans_b, m, n, k, alpha, a_list[0], lda, b_list[0], ldb, beta,
                      c_list[0], ldc, nullptr, tab, tc, as_stream(stream));
   if (!ptr_scratch) return fail(LS2_ERR_SHAPE, "gemm_list: needs pointer scratch");
-  PtrList l;
-  for (int i = 0; i < count; ++i) {
-    l.p[i] = a_list[i];
-    l.p[count + i] = b_list[i];
-    l.p[2 * count + i] = c_list[i];
-  }
   const void** ptrs = reinterpret_cast<const void**>(ptr_scratch);
-  fill_list_kernel<<<1, 256, 0, as_stream(stream)>>>(l, 3 * count, ptrs);
-  int rc = check_launch("gemm_fill_list");
-  if (rc) return rc;
+  if (!ptrs_ready) {   // callers cache the table per address list: filled once
+    PtrList l;
+    for (int i = 0; i < count; ++i) {
+      l.p[i] = a_list[i];
+      l.p[count + i] = b_list[i];
+      l.p[2 * count + i] = c_list[i];
+    }
+    fill_list_kernel<<<1, 256, 0, as_stream(stream)>>>(l, 3 * count, ptrs);
+    int rc = check_launch("gemm_fill_list");
+    if (rc) return rc;
+  }
   cublasSetStream(b->h, as_stream(stream));
   const float af = (float)alpha, bf = (float)beta;
   const cublasOperation_t opA = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;

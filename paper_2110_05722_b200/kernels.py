@@ -664,16 +664,20 @@ def gemm_list(a_list, b_list, outs, trans_a: bool = False, trans_b: bool = False
         A, B, C = a_list[lo:lo + 64], b_list[lo:lo + 64], outs[lo:lo + 64]
         cnt = len(A)
         key = ("list",) + tuple(t.data_ptr() for t in A + B + C)
+        # the table is filled by the first call (the eager first step of a bucket,
+        # before its graph is captured) and reused: planned-arena addresses are static
         scratch = ctx.ptr_cache.get(key)
+        ready = 1
         if scratch is None:
             scratch = torch.empty(3 * cnt, dtype=torch.int64, device=ctx.device)
             ctx.ptr_cache[key] = scratch
+            ready = 0
         arr = ctypes.c_void_p * cnt
         _lib.call("ls2_gemm_list", ctx.blas_handle(), int(trans_a), int(trans_b), m, n, k,
                   float(alpha), arr(*[t.data_ptr() for t in A]), a0.shape[1],
                   arr(*[t.data_ptr() for t in B]), b0.shape[1], float(beta),
                   arr(*[t.data_ptr() for t in C]), n, cnt, _lib.dtype_code(a0),
-                  _lib.dtype_code(c0), scratch.data_ptr(), _lib.stream_handle())
+                  _lib.dtype_code(c0), scratch.data_ptr(), ready, _lib.stream_handle())
     return outs
 
 
