@@ -64,11 +64,15 @@ def main():
     draws = 6 * (2 * N * D + N * F) + 6 * (3 * N * D + N * F) + 2 * N * D
     for k in d["kernels"]:
         if "dropout_bits_multi" in k["name"]:
-            us = k["us_per_step"] / max(k["launches_per_step"], 1)
+            # one launch draws the bank (the next step's, beside the narrow pass and
+            # Adam at one CTA per SM); the step's own launch finds the stamp and exits
+            us = k["us_per_step"]
             lines.append("")
             lines.append(f"Mask bank (`dropout_bits_multi_kernel`, integer-ALU bound, not HBM): "
-                         f"{draws / 1e6:.0f} M keep-bit draws in {us:.1f} µs = "
-                         f"{draws / us / 1e6:.2f} T draws/s")
+                         f"{draws / 1e6:.0f} M keep-bit draws in {us:.1f} µs per step "
+                         f"({k['launches_per_step']} launches; the draw runs beside "
+                         f"`scale_narrow` and `adam_kernel`, which share the SMs with it, so "
+                         f"their in-situ times above include that sharing)")
     out = "\n".join(lines)
     print(f"step {d['step_us']:.0f} µs, kernel busy {d['busy_us']:.0f} µs\n")
     print(out)
