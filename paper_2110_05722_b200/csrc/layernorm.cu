@@ -460,7 +460,8 @@ inline int ln_stage_rw(int64_t rows, int64_t cols) {
   return (int)rw;
 }
 
-template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP>
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP,
+          bool PIPE>
 __global__ void __launch_bounds__((ITERS >= 4 ? kLnStageWideWarps : kLnStageMaxWarps) * 32, 1)
 ln_bwd_stage(
     const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
@@ -482,11 +483,17 @@ ln_bwd_stage(
     if (g < cgs) wv[it] = ld8(w + g * 8);
   }
   const float inv_m = (float)(1.0 / (double)cols);
-  for (int64_t base = (int64_t)blockIdx.x * rw; base < rows; base += (int64_t)gridDim.x * rw) {
+  // PIPE (the CTA has several row batches): batch k's loads are issued before
+  // batch k-1's staged column contributions are folded into accs, so the fold
+  // overlaps the loads.  The fold order is the same either way: PIPE does not
+  // change results.
+  const int64_t base0 = (int64_t)blockIdx.x * rw;
+  for (int64_t base = base0; base < rows; base += (int64_t)gridDim.x * rw) {
     const int64_t r = base + wid;
     float* my = stg + (int64_t)wid * npairs;
+    Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
+    float m_r = 0.f, rs = 0.f;
     if (r < rows) {
-      Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         const int64_t g = lane + 32 * it;
@@ -496,8 +503,18 @@ ln_bwd_stage(
           if (RES) cr[it] = ld8_stream(dres + r * cols + g * 8);
         }
       }
-      const float m_r = (float)mu[r];
-      const float rs = (float)(1.0 / (double)sigma[r]);
+      m_r = (float)mu[r];
+      rs = (float)(1.0 / (double)sigma[r]);
+    }
+    if (PIPE && base != base0) {     // fold the previous batch (staged, synced)
+      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        float s = 0.f;
+        for (int q = 0; q < rw; ++q) s += stg[(int64_t)q * npairs + p];
+        accs[p] += s;
+      }
+      __syncthreads();               // folded before the stage is overwritten
+    }
+    if (r < rows) {
       // packed pair math: xh = x*rs - m*rs, gg = w*dy, sums of gg and gg*xh
       const float2 rs2 = f2s(rs), nmrs2 = f2s(-m_r * rs);
       float2 r1v = f2s(0.f), r3v = f2s(0.f);
@@ -568,13 +585,23 @@ ln_bwd_stage(
     } else {
       for (int c = lane; c < npairs; c += 32) my[c] = 0.f;
     }
-    __syncthreads();
+    __syncthreads();                 // the batch is staged
+    if (!PIPE) {
+      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        float s = 0.f;
+        for (int q = 0; q < rw; ++q) s += stg[(int64_t)q * npairs + p];
+        accs[p] += s;
+      }
+      __syncthreads();
+    }
+  }
+  // the last batch's fold; thread p owns accs[p] in every fold, so no barrier
+  if (PIPE && base0 < rows) {
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
       float s = 0.f;
       for (int q = 0; q < rw; ++q) s += stg[(int64_t)q * npairs + p];
       accs[p] += s;
     }
-    __syncthreads();
   }
   for (int p = threadIdx.x; p < npairs; p += blockDim.x)
     partial[(int64_t)blockIdx.x * npairs + p] = (double)accs[p];
@@ -704,18 +731,25 @@ int ln_bwd_launch(const void* dy, const void* x, const void* w, const void* mu, 
         (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
         (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (C)dscale, (double*)ws, rows, cols);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
     constexpr int NP = B ? 3 : 2;
     const int rw = ln_stage_rw(rows, cols);
     const size_t smem = (size_t)(rw + 1) * NP * cols * sizeof(float);
-    ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D><<<nblk, rw * 32, smem, st>>>(
-        (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
-        (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows, cols);
+    auto go = [&](auto pipe) {
+      constexpr bool P = decltype(pipe)::value;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D, P>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      ln_bwd_stage<Tin, Tout, Tstat, I, R, B, D, P><<<nblk, rw * 32, smem, st>>>(
+          (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
+          (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows,
+          cols);
+    };
+    // several row batches per CTA (T-big, BERT): overlap each fold with the next loads
+    if (rows > (int64_t)nblk * rw) go(std::true_type{});
+    else go(std::false_type{});
   }
   return check_launch(B ? "layernorm_bwd_bdr" : "layernorm_bwd");
 }
