@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
   uint8_t* Pt = sm + 4 * kPair;      // [P0 | P1]
   uint8_t* St = sm + 5 * kPair;      // [dS0 | dS1]
   uint8_t* Ib = sm + 6 * kPair;      // slot indicator [16 x 128] (4 KB), the column-sum B operand
-  __shared__ __align__(8) uint64_t bar_ld, bar_1, bar_2, bar_cs;
+  __shared__ __align__(8) uint64_t bar_ld, bar_ov, bar_1, bar_1b, bar_dv, bar_2, bar_cs;
   __shared__ uint32_t tmem_base;
   __shared__ float xr[256];
   const int warp = threadIdx.x >> 5;
@@ -479,17 +479,25 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdo)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
     mbar_init(&bar_ld, 1);
+    mbar_init(&bar_ov, 1);
     mbar_init(&bar_1, 1);
+    mbar_init(&bar_1b, 1);
+    mbar_init(&bar_dv, 1);
     mbar_init(&bar_2, 1);
     mbar_init(&bar_cs, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&bar_ld, (uint32_t)(nb * 2 * (qrows + krows) * 128));
+    // Q, K first (S = Q K^T starts on them), then dO, V (dP = dO V^T)
+    mbar_expect_tx(&bar_ld, (uint32_t)(nb * (qrows + krows) * 128));
     for (int s = 0; s < nb; ++s) {
       const int t = tile0 + s, h = t % a.H, b0 = (t / a.H) * a.G;
       tma_load_3d(Qs + s * kTile, &mq, h * 64, 0, b0, &bar_ld);
       tma_load_3d(Ks + s * kTile, &mk, h * 64, 0, b0, &bar_ld);
-      tma_load_3d(Os + s * kTile, &mdo, h * 64, 0, b0, &bar_ld);
-      tma_load_3d(Vs + s * kTile, &mv, h * 64, 0, b0, &bar_ld);
+    }
+    mbar_expect_tx(&bar_ov, (uint32_t)(nb * (qrows + krows) * 128));
+    for (int s = 0; s < nb; ++s) {
+      const int t = tile0 + s, h = t % a.H, b0 = (t / a.H) * a.G;
+      tma_load_3d(Os + s * kTile, &mdo, h * 64, 0, b0, &bar_ov);
+      tma_load_3d(Vs + s * kTile, &mv, h * 64, 0, b0, &bar_ov);
     }
     stamp(a, 8);
   }
@@ -527,8 +535,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
     stamp(a, 2);
     tc_after();
     mma128<KM, KM, 4>(tmem, sptr(Qs), sptr(Ks), a.id_s);          // S
-    mma128<KM, KM, 4>(tmem + 128, sptr(Os), sptr(Vs), a.id_s);    // dP
     commit(&bar_1);
+    mbar_wait(&bar_ov, 0);
+    tc_after();
+    mma128<KM, KM, 4>(tmem + 128, sptr(Os), sptr(Vs), a.id_s);    // dP
+    commit(&bar_1b);
   }
   __syncwarp();
 
@@ -552,6 +563,21 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
     pw[j] = pack_h2(p2[0], p2[1]);
   }
   st_cols(Pt, r.m, r.half, pw);
+  // P complete, S read: dV = P^T dO (M = 64 per slot, TMEM columns 0-63, which
+  // S no longer needs) runs while the threads form dS
+  fence_async_smem();
+  tc_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_after();
+    for (int s2 = 0; s2 < nb; ++s2)
+      mma64<MN, MN>(tmem + ((uint32_t)(16 * s2) << 16), sptr(Pt + s2 * kTile), sptr(Os + s2 * kTile),
+                    a.id64_mm);
+    commit(&bar_dv);
+  }
+  __syncwarp();
+  mbar_wait(&bar_1b, 0);
+  tc_after();
   tmem_ld32(tlane + 128 + 64 * r.slot + 32 * r.half, x);    // dP
   float rs = 0.f;
 #pragma unroll
@@ -570,31 +596,38 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
     }
     st_cols(St, r.m, r.half, dw);
   }
+  // dV (done while dS was formed) -> fp16 staging in V's tile (dP has been read)
+  const int mr = m64_row();
+  mbar_wait(&bar_dv, 0);
+  tc_after();
+  tmem_ld32(tlane + 32 * r.half, x);
+  st_cols_f(Vs, mr, r.half, x);      // dV
   fence_async_smem();
   tc_before();
-  __syncthreads();                   // P and dS complete, S and dP read
+  __syncthreads();                   // dS and the dV staging complete, dP read
   stamp(a, 4);
   if (threadIdx.x == 0) {
     tc_after();
     for (int s2 = 0; s2 < nb; ++s2) {   // per-slot M = 64 products, slot s at lane offset 16 s
       const uint32_t d = tmem + ((uint32_t)(16 * s2) << 16);
-      mma64<MN, MN>(d, sptr(Pt + s2 * kTile), sptr(Os + s2 * kTile), a.id64_mm);       // dV = P^T dO
       mma64<KM, MN>(d + 64, sptr(St + s2 * kTile), sptr(Ks + s2 * kTile), a.id64_km);  // dQ = dS K
       mma64<MN, MN>(d + 128, sptr(St + s2 * kTile), sptr(Qs + s2 * kTile), a.id64_mm); // dK = dS^T Q
     }
     commit(&bar_2);
+    for (int s = 0; s < nb; ++s) {       // dV leaves while dQ, dK run
+      const int t = tile0 + s, h = t % a.H, b0 = (t / a.H) * a.G;
+      tma_store_3d(&mdv, h * 64, 0, b0, Vs + s * kTile);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   __syncwarp();
   mbar_wait(&bar_2, 0);
   stamp(a, 5);
   tc_after();
-  const int mr = m64_row();
   tmem_ld32(tlane + 64 + 32 * r.half, x);
   st_cols_f(Qs, mr, r.half, x);      // dQ (row = query)
   tmem_ld32(tlane + 128 + 32 * r.half, x);
   st_cols_f(Ks, mr, r.half, x);      // dK (row = key)
-  tmem_ld32(tlane + 32 * r.half, x);
-  st_cols_f(Vs, mr, r.half, x);      // dV
   fence_async_smem();
   tc_before();
   __syncthreads();
@@ -604,7 +637,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_bwd_kernel(
       const int t = tile0 + s, h = t % a.H, b0 = (t / a.H) * a.G;
       tma_store_3d(&mdq, h * 64, 0, b0, Qs + s * kTile);
       tma_store_3d(&mdk, h * 64, 0, b0, Ks + s * kTile);
-      tma_store_3d(&mdv, h * 64, 0, b0, Vs + s * kTile);
     }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
