@@ -211,6 +211,14 @@ __device__ __forceinline__ uint32_t keep_bits_n(uint64_t seed, uint64_t first, u
   return b;
 }
 
+// bit e of w as 0 or 1 in type C: a select, not an integer->float conversion
+// (I2FP on the conversion pipe was a throttle in the mask-applying kernels);
+// the value, and so every product with it, is unchanged
+template <typename C>
+__device__ __forceinline__ C bitval(uint32_t w, int e) {
+  return ((w >> e) & 1u) ? (C)1 : (C)0;
+}
+
 __device__ __forceinline__ uint32_t keep_byte(uint64_t seed, uint64_t first, uint64_t thresh) {
   return keep_bits_n<8>(seed, first, thresh);
 }

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(1024) bdr_fwd_vec(const Tin* __restrict__ x, c
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       C a = add_rn(xv[e], b[e]);
-      if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), scale);
+      if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), scale);
       o[e] = add_rn(a, rv[e]);
     }
     store_row_group(y + g * 8, o);
@@ -227,7 +227,7 @@ __global__ void bdr_fwd_flat(const Tin* __restrict__ x, const Tin* __restrict__ 
       const int64_t i = g * 8 + e;
       if (i >= n) break;
       C a = add_rn(cvt<C>(x[i]), cvt<C>(bias[i % cols]));
-      if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), scale);
+      if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), scale);
       y[i] = cvt<Tout>(add_rn(a, cvt<C>(res[i])));
     }
   }
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(1024) bdr_bwd_vec(const Tin* __restrict__ dy, 
       const uint32_t kb = DROP ? bits[g] : 0xFF;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        if (DROP) d[e] = mul_rn(mul_rn(d[e], (C)((kb >> e) & 1)), scale);
+        if (DROP) d[e] = mul_rn(mul_rn(d[e], bitval<C>(kb, e)), scale);
         acc[e] += d[e];
       }
       store_row_group(dx + g * 8, d);
@@ -268,7 +268,7 @@ __global__ void bdr_bwd_flat(const Tin* __restrict__ dy, const uint8_t* __restri
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     C d = cvt<C>(dy[i]);
-    if (DROP) d = mul_rn(mul_rn(d, (C)((bits[i >> 3] >> (i & 7)) & 1)), scale);
+    if (DROP) d = mul_rn(mul_rn(d, bitval<C>(bits[i >> 3], (int)(i & 7))), scale);
     dx[i] = cvt<Tout>(d);
   }
 }
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(1024) brd_fwd_vec(const Tin* __restrict__ x, c
       const bool pos = a > (C)0;
       rb |= (uint32_t)pos << e;
       a = mul_rn(a, (C)(pos ? 1 : 0));
-      if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), scale);
+      if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), scale);
       o[e] = a;
     }
     if (rbits) rbits[g] = (uint8_t)rb;
@@ -346,7 +346,7 @@ __global__ void brd_fwd_flat(const Tin* __restrict__ x, const Tin* __restrict__ 
       const bool pos = a > (C)0;
       rb |= (uint32_t)pos << e;
       a = mul_rn(a, (C)(pos ? 1 : 0));
-      if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), scale);
+      if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), scale);
       y[i] = cvt<Tout>(a);
     }
     if (rbits) rbits[g] = (uint8_t)rb;
@@ -390,8 +390,10 @@ __global__ void __launch_bounds__(1024) brd_bwd_vec(const Tin* __restrict__ dy, 
           C d[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            d[e] = mul_rn(cvt<C>(pd[u].v[e]), (C)((rb[u] >> e) & 1));
-            if (DROP) d[e] = mul_rn(mul_rn(d[e], (C)((kb[u] >> e) & 1)), scale);
+            // (d * relu) * keep == d * (relu & keep) for 0/1 factors, signed zeros
+            // and NaN included: one multiply by the combined bit
+            d[e] = mul_rn(cvt<C>(pd[u].v[e]), bitval<C>(DROP ? rb[u] & kb[u] : rb[u], e));
+            if (DROP) d[e] = mul_rn(d[e], scale);
             acc[e] += d[e];
           }
           store_row_group(dx + g * 8, d);
@@ -409,8 +411,8 @@ __global__ void brd_bwd_flat(const Tin* __restrict__ dy, const uint8_t* __restri
   using C = typename CompOf<Tin>::type;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    C d = mul_rn(cvt<C>(dy[i]), (C)((rbits[i >> 3] >> (i & 7)) & 1));
-    if (DROP) d = mul_rn(mul_rn(d, (C)((kbits[i >> 3] >> (i & 7)) & 1)), scale);
+    C d = mul_rn(cvt<C>(dy[i]), bitval<C>(rbits[i >> 3], (int)(i & 7)));
+    if (DROP) d = mul_rn(mul_rn(d, bitval<C>(kbits[i >> 3], (int)(i & 7))), scale);
     dx[i] = cvt<Tout>(d);
   }
 }
@@ -447,8 +449,8 @@ __global__ void masked_colsum_stage1(const Tin* __restrict__ dy, const uint8_t* 
     for (int64_t r = r0; r < r1; ++r) {
       const int64_t i = r * cols + c;
       C d = cvt<C>(dy[i]);
-      if (rbits) d = mul_rn(d, (C)((rbits[i >> 3] >> (i & 7)) & 1));
-      if (use_drop) d = mul_rn(mul_rn(d, (C)((kbits[i >> 3] >> (i & 7)) & 1)), scale);
+      if (rbits) d = mul_rn(d, bitval<C>(rbits[i >> 3], (int)(i & 7)));
+      if (use_drop) d = mul_rn(mul_rn(d, bitval<C>(kbits[i >> 3], (int)(i & 7))), scale);
       s += (double)d;
     }
     partial[(int64_t)blockIdx.x * cols + c] = s;

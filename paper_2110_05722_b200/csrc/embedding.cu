@@ -44,7 +44,7 @@ __global__ void emb_fwd_vec(const Tin* __restrict__ E, const Tin* __restrict__ P
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         C a = add_rn(mul_rn(cvt<C>(ev.v[e]), es), cvt<C>(pv.v[e]));
-        if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), ds);
+        if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), ds);
         o.v[e] = cvt<Tout>(a);
       }
     }
@@ -83,7 +83,7 @@ __global__ void emb_fwd_flat(const Tin* __restrict__ E, const Tin* __restrict__ 
         if (bad) *bad = 1;
       } else {
         a = add_rn(mul_rn(cvt<C>(E[tok * d + j]), es), cvt<C>(P[(r % len) * d + j]));
-        if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), ds);
+        if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), ds);
       }
       y[i] = cvt<Tout>(a);
     }

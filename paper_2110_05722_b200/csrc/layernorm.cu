@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             C a = add_rn(cvt<C>(px.v[e]), cvt<C>(cq.v[e]));
-            if (DROP) a = mul_rn(mul_rn(a, (C)((kb >> e) & 1)), dscale);
+            if (DROP) a = mul_rn(mul_rn(a, bitval<C>(kb, e)), dscale);
             q.v[e] = cvt<Tout>(add_rn(a, cvt<C>(pr.v[e])));
           }
         }
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32) ln_bwd_warp(
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             C v = cvt<C>(o.v[e]);
-            if (DROP) v = mul_rn(mul_rn(v, (C)((kb >> e) & 1)), dscale);
+            if (DROP) v = mul_rn(mul_rn(v, bitval<C>(kb, e)), dscale);
             acc[NP - 1][it][e] += v;
             pj.v[e] = cvt<Tout>(v);
           }
@@ -570,7 +570,7 @@ ln_bwd_stage(
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               float v = cvt<float>(o.v[e]);
-              if (DROP) v = mul_rn(mul_rn(v, (float)((kb >> e) & 1)), dscale);
+              if (DROP) v = mul_rn(mul_rn(v, bitval<float>(kb, e)), dscale);
               c2[e] = v;
               pj.v[e] = cvt<Tout>(v);
             }
