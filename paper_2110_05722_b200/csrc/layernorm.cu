@@ -178,20 +178,31 @@ __global__ void __launch_bounds__(kLnWarps * 32, 7) ln_fwd_bdr_warp(
   for (int64_t r = (int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5); r < rows;
        r += (int64_t)gridDim.x * kLnWarps) {
     Pack8<Tout> v[ITERS];   // the stored yres, packed; LN statistics read it back
+    // every load of the row first (x, residual and the bank's keep bits of all
+    // ITERS groups), so one memory round trip covers the row: issued inside the
+    // compute loop, the next group's loads queued behind this group's store
+    Pack8<Tin> pxs[ITERS], prs[ITERS];
+    uint32_t kbs[ITERS];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t g = lane + 32 * it;
+      kbs[it] = 0xFF;
+      if (g < cgs) {
+        pxs[it] = ld8(x + r * cols + g * 8);
+        prs[it] = ld8(res + r * cols + g * 8);
+        if (DROP && !GEN) kbs[it] = bits[r * cgs + g];      // precomputed by the mask bank
+      }
+    }
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int64_t g = lane + 32 * it;
       if (g < cgs) {
-        const Pack8<Tin> px = ld8(x + r * cols + g * 8);
-        const Pack8<Tin> pr = ld8(res + r * cols + g * 8);
-        uint32_t kb = 0xFF;
-        if (DROP) {
-          if (GEN) {
-            kb = keep_byte(seed, (uint64_t)(r * cgs + g) * 8, thresh);
-            bits[r * cgs + g] = (uint8_t)kb;
-          } else {
-            kb = bits[r * cgs + g];      // precomputed by the mask bank
-          }
+        const Pack8<Tin>& px = pxs[it];
+        const Pack8<Tin>& pr = prs[it];
+        uint32_t kb = kbs[it];
+        if (DROP && GEN) {
+          kb = keep_byte(seed, (uint64_t)(r * cgs + g) * 8, thresh);
+          bits[r * cgs + g] = (uint8_t)kb;
         }
         Pack8<Tout> q;
         const Pack8<Tin> cq = sc[g];
@@ -492,15 +503,18 @@ ln_bwd_stage(
     const int64_t r = base + wid;
     float* my = stg + (int64_t)wid * npairs;
     Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
+    uint32_t kbs[ITERS];   // keep bits loaded with the row (not after the reductions)
     float m_r = 0.f, rs = 0.f;
     if (r < rows) {
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         const int64_t g = lane + 32 * it;
+        kbs[it] = 0xFF;
         if (g < cgs) {
           cd[it] = ld8_stream(dy + r * cols + g * 8);
           cx[it] = ld8_stream(x + r * cols + g * 8);
           if (RES) cr[it] = ld8_stream(dres + r * cols + g * 8);
+          if (BDR && DROP) kbs[it] = bits[r * cgs + g];
         }
       }
       m_r = (float)mu[r];
@@ -564,7 +578,7 @@ ln_bwd_stage(
           }
           st8(dx + r * cols + g * 8, o);
           if (BDR) {
-            const uint32_t kb = DROP ? bits[r * cgs + g] : 0xFF;
+            const uint32_t kb = kbs[it];
             Pack8<Tout> pj;
             float c2[8];
 #pragma unroll
