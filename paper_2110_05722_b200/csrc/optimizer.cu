@@ -154,7 +154,7 @@ __global__ void step_commit_kernel(int64_t* applied, const int* nonfinite, const
 __global__ void step_report_kernel(int64_t* applied, const int* nonfinite, const double* totals,
                                    double* report) {
   const bool ok = !skip_step(nonfinite, totals);
-  if (ok) *applied += 1;
+  if (ok && applied) *applied += 1;   // applied == NULL: report only (before the update)
   report[0] = totals[0];
   report[1] = totals[1];
   report[2] = totals[2];

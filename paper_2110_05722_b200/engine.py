@@ -128,7 +128,15 @@ class TrainingEngine:
         self._nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._dev_out = torch.zeros(5, dtype=torch.float64, device=self.device)
+        self._dev_early = torch.zeros(5, dtype=torch.float64, device=self.device)
         self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
+        # the step's metrics reach the host BEFORE the optimizer runs (they are known
+        # once the non-finite count is): train_step waits on this event, not on the
+        # stream, so the host returns and enqueues the next step while Adam (and the
+        # next step's mask draw) still run; the next replay is stream-ordered after
+        # them.  Data parallelism keeps the end-of-step copy.
+        self._metrics_ev = torch.cuda.Event(external=True)
+        self._early_report = os.environ.get("LS2_EARLY_REPORT", "1") != "0"
         self._xplan = None
         self._span_tables: dict = {}
         self.merge_spans = True          # tests set False to run the per-chunk update on 1 rank
@@ -507,6 +515,7 @@ class TrainingEngine:
                 self.masks.desc is not None and t.p_drop > 0.0 and sink is not None:
             self._draw_next_bank()
         joined = getattr(self, "_bank_done", None)
+        reported = False
         if self.dp.active:
             # every bucket was reduced + narrowed + checked on the comm stream;
             # the optimizer (sharded or whole) follows there, then the join
@@ -520,13 +529,22 @@ class TrainingEngine:
                       ws.n_elements, float(t.loss_scale), out3.data_ptr(), -1,
                       float(1.0 / t.act_grad_scale), self._nonfinite.data_ptr(), st)
             self._finish_deferred(sink, out3, self._nonfinite.data_ptr())
+            if host_copy and self._early_report:
+                # the metrics are final here (the skip decision needs only the
+                # non-finite count and the loss): report them before the update
+                _lib.call("ls2_step_report", None, self._nonfinite.data_ptr(), loss_ptr,
+                          self._dev_early.data_ptr(), st)
+                self._host_out.copy_(self._dev_early, non_blocking=True)
+                self._metrics_ev.record()
+                reported = True
             self._optimizer(0, ws.n_elements, loss_ptr, st)
         _lib.call("ls2_step_report", self._applied_dev.data_ptr(), self._nonfinite.data_ptr(),
                   loss_ptr, self._dev_out.data_ptr(), st)
         if joined is not None:
             torch.cuda.current_stream().wait_event(joined)
-        if host_copy:
+        if host_copy and not reported:
             self._host_out.copy_(self._dev_out, non_blocking=True)
+            self._metrics_ev.record()
 
     def _run(self, io, key, step, graphed: bool):
         if graphed:
@@ -604,7 +622,13 @@ class TrainingEngine:
         else:
             io.stage(batch)
             self._run(io, key, step, graphed=False)
-        torch.cuda.current_stream().synchronize()
+        if graphed:
+            # the metrics copy (issued before the optimizer) has landed; the update
+            # and the next step's mask draw may still run, and everything enqueued
+            # after this call is stream-ordered behind them
+            self._metrics_ev.synchronize()
+        else:
+            torch.cuda.current_stream().synchronize()
         loss, count, correct, applied, nonfinite = self._host_out.tolist()
         if self.use_graphs and key not in self._graphs:
             self._capture(io, key, step + 1)
