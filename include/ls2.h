@@ -64,6 +64,12 @@ enum {
 
 const char* ls2_last_error(void);
 int ls2_version(void);
+/* dst[i] <- src[i] (nbytes[i] bytes, multiples of 8, 8-byte aligned), i < n <= 8, in ONE
+ * launch; src may be pinned host memory (UVA).  The engine's per-step H2D inputs (batch
+ * + dropout seed tables) enter a captured step as one kernel node.  Replaces the
+ * reference's per-array host->device hand-off of a step's batch (F/engine.py:130-148). */
+int ls2_copy_spans(void* const* dst, const void* const* src, const int64_t* nbytes, int n,
+                   void* stream);
 int ls2_num_kernels_launched(int64_t* out);   /* launches since load (host counter) */
 
 /* ---- counter RNG / dropout masks: F/numerics.py:139-163, F/kernels.py:155-166 ----

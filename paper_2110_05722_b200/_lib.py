@@ -34,6 +34,7 @@ Fl = ctypes.c_float
 _SIGS = {
     "ls2_last_error": [],
     "ls2_version": [],
+    "ls2_copy_spans": [P, P, P, I, P],
     "ls2_num_kernels_launched": [P],
     "ls2_rand_uniform": [P, U, L, L, P],
     "ls2_dropout_bits": [P, L, U, P, U, P],

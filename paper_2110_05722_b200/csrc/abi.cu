@@ -141,6 +141,27 @@ __global__ void dense_to_bits_kernel(const T* dense, uint8_t* bits, int64_t n) {
 
 using namespace ls2;
 
+// Up to kMaxSpans copies of 8-byte words in ONE launch (the step's batch and seed
+// tables, read straight from pinned host memory through UVA): one kernel node in a
+// captured step instead of one copy-engine node per buffer.  Thread w copies word
+// w of the concatenation, so every word crosses the bus in one round trip.
+constexpr int kMaxSpans = 8;
+struct CopySpans {
+  uint64_t* dst[kMaxSpans];
+  const uint64_t* src[kMaxSpans];
+  int64_t start[kMaxSpans + 1];   // word offsets of each span in the concatenation
+  int n;
+};
+
+__global__ void copy_spans_kernel(CopySpans s) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= s.start[s.n]) return;
+  int i = 0;
+  while (i + 1 < s.n && w >= s.start[i + 1]) ++i;
+  const int64_t k = w - s.start[i];
+  s.dst[i][k] = s.src[i][k];
+}
+
 extern "C" {
 
 const char* ls2_last_error(void) { return t_err.c_str(); }
@@ -188,6 +209,27 @@ int ls2_dropout_bits_multi(const int64_t* desc, int nsites, int64_t total_words,
                            const int64_t* want, void* stream) {
   return ls2_dropout_bits_multi_ex(desc, nsites, total_words, base, seeds, thresh, stamp, want, 0,
                                    stream);
+}
+
+int ls2_copy_spans(void* const* dst, const void* const* src, const int64_t* nbytes, int n,
+                   void* stream) {
+  if (n < 0 || n > kMaxSpans) return fail(LS2_ERR_SHAPE, "copy_spans: 0..8 spans");
+  CopySpans s{};
+  s.n = n;
+  int64_t words = 0;
+  for (int i = 0; i < n; ++i) {
+    if ((nbytes[i] & 7) || (reinterpret_cast<uintptr_t>(dst[i]) & 7) ||
+        (reinterpret_cast<uintptr_t>(src[i]) & 7))
+      return fail(LS2_ERR_SHAPE, "copy_spans: 8-byte sizes and alignment");
+    s.dst[i] = static_cast<uint64_t*>(dst[i]);
+    s.src[i] = static_cast<const uint64_t*>(src[i]);
+    s.start[i] = words;
+    words += nbytes[i] / 8;
+  }
+  s.start[n] = words;
+  if (words == 0) return LS2_OK;
+  copy_spans_kernel<<<(unsigned)ceil_div(words, 256), 256, 0, as_stream(stream)>>>(s);
+  return check_launch("copy_spans");
 }
 
 int ls2_bits_to_dense(const uint8_t* bits, void* dense, int dtype, int64_t n, void* stream) {

@@ -12,6 +12,7 @@ on the device, so a skipped step needs no extra host round trip.
 
 from __future__ import annotations
 
+import ctypes
 import gc
 import os
 import time
@@ -88,6 +89,12 @@ class _StaticIO:
                      (self.len, self.h_len)):
             d.copy_(h, non_blocking=True)
 
+    def spans(self) -> list:
+        """(dst, src, nbytes) of the batch's H2D copies."""
+        return [(d.data_ptr(), h.data_ptr(), 8 * d.numel())
+                for d, h in ((self.src, self.h_src), (self.tin, self.h_tin),
+                             (self.tout, self.h_tout), (self.len, self.h_len))]
+
     def batch(self) -> Batch:
         return Batch(self.src, self.tin, self.tout, self.len, self.pad_id)
 
@@ -137,6 +144,7 @@ class TrainingEngine:
         # them.  Data parallelism keeps the end-of-step copy.
         self._metrics_ev = torch.cuda.Event(external=True)
         self._early_report = os.environ.get("LS2_EARLY_REPORT", "1") != "0"
+        self._one_copy = os.environ.get("LS2_COPY_SPANS", "1") != "0"
         self._xplan = None
         self._span_tables: dict = {}
         self.merge_spans = True          # tests set False to run the per-chunk update on 1 rank
@@ -249,17 +257,32 @@ class TrainingEngine:
             # every host->device input of the step first: the batch, this step's
             # site seeds, (the next step's seeds); then mark them consumed so the
             # host can stage the next step while this one runs (train_step)
-            io.upload()
+            # all of them as ONE kernel reading the pinned buffers (ls2_copy_spans)
+            # instead of one copy-engine node each (LS2_COPY_SPANS=0: the copies)
+            spans = io.spans()
+            seeds = None
             if t.p_drop > 0.0:
                 seeds = self.model.seed_table(self.device)
                 self.model.register_seeds(seeds, t.seed, step, t.p_drop)
-                seeds.upload()
+                spans.append(seeds.stage_span())
             if self.masks is not None and self._early_masks and t.p_drop > 0.0:
                 if not torch.cuda.is_current_stream_capturing():
                     self._stage_next_seeds(step)
                 nx = self._seeds_next
-                n = len(nx.values)
-                nx.dev[:n].copy_(nx.host[:n], non_blocking=True)
+                spans.append((nx.dev.data_ptr(), nx.host.data_ptr(), 8 * len(nx.values)))
+            if self._one_copy:
+                n = len(spans)
+                _lib.call("ls2_copy_spans", (ctypes.c_void_p * n)(*[s[0] for s in spans]),
+                          (ctypes.c_void_p * n)(*[s[1] for s in spans]),
+                          (ctypes.c_int64 * n)(*[s[2] for s in spans]), n, _lib.stream_handle())
+            else:
+                io.upload()
+                for tab in ([seeds] if seeds is not None else []) + \
+                        ([self._seeds_next] if len(spans) > 4 + (seeds is not None) else []):
+                    n = len(tab.values)
+                    tab.dev[:n].copy_(tab.host[:n], non_blocking=True)
+            if seeds is not None:
+                seeds.uploaded()
             self._consumed.record()
         self.arena.begin(key)
         sink = _ViewSink(self.gviews, defer=True, lane=self.use_lane, wgrad_group=self.wgrad_group)

@@ -775,13 +775,23 @@ class SeedTable:
         return self.dev[i:i + 1]
 
     def upload(self):
+        span = self.stage_span()
+        self.dev[:len(self.values)].copy_(self.host[:len(self.values)], non_blocking=True)
+        self.uploaded()
+        return span
+
+    def stage_span(self):
+        """Fill the pinned staging buffer; (dst, src, nbytes) of the H2D copy the
+        caller issues (engine: one ls2_copy_spans launch for every step input)."""
         n = len(self.values)
         if n > self.host.numel():
             raise ShapeMismatch("seed table overflow")
-        capturing = torch.cuda.is_current_stream_capturing()
-        self.write_host(sync=not capturing)
-        self.dev[:n].copy_(self.host[:n], non_blocking=True)
-        if not capturing:
+        self.write_host(sync=not torch.cuda.is_current_stream_capturing())
+        return (self.dev.data_ptr(), self.host.data_ptr(), 8 * n)
+
+    def uploaded(self):
+        """After the copy is enqueued: the next write_host waits for it (eager)."""
+        if not torch.cuda.is_current_stream_capturing():
             self._evt = torch.cuda.Event()
             self._evt.record()
 
