@@ -307,7 +307,8 @@ int ls2_step_commit(int64_t* applied, const int* nonfinite, const double* loss,
 /* step_commit and the step report {loss sum, tokens, correct, applied, non-finite}
  * (f64 x 5, the train-step D2H source) in one launch; totals = (loss, count, correct).
  * applied == NULL: the report alone (the engine issues it before the optimizer, so the
- * host reads the step's metrics while the update still runs) */
+ * host reads the step's metrics while the update still runs); report may be pinned host
+ * memory (UVA), written directly by the kernel */
 int ls2_step_report(int64_t* applied, const int* nonfinite, const double* totals, double* report,
                     void* stream);
 /* g16 = RNE(acc32 * f32(loss_scale / max(count,1)) * post), count = out3[1] (device) or

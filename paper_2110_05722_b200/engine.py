@@ -135,7 +135,6 @@ class TrainingEngine:
         self._nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._dev_out = torch.zeros(5, dtype=torch.float64, device=self.device)
-        self._dev_early = torch.zeros(5, dtype=torch.float64, device=self.device)
         self._host_out = torch.zeros(5, dtype=torch.float64).pin_memory()
         # the step's metrics reach the host BEFORE the optimizer runs (they are known
         # once the non-finite count is): train_step waits on this event, not on the
@@ -555,9 +554,10 @@ class TrainingEngine:
             if host_copy and self._early_report:
                 # the metrics are final here (the skip decision needs only the
                 # non-finite count and the loss): report them before the update
+                # written by the report kernel straight into the pinned host
+                # buffer (UVA): no D2H copy node ahead of the optimizer
                 _lib.call("ls2_step_report", None, self._nonfinite.data_ptr(), loss_ptr,
-                          self._dev_early.data_ptr(), st)
-                self._host_out.copy_(self._dev_early, non_blocking=True)
+                          self._host_out.data_ptr(), st)
                 self._metrics_ev.record()
                 reported = True
             self._optimizer(0, ws.n_elements, loss_ptr, st)
