@@ -750,3 +750,41 @@ def test_gemm_tc_two_sm_persistent_all_majors(ta, tb, m, n, k, variant):
     tol = (6e-5 if k > 8192 else 1e-5) if odt == torch.float32 else \
         (8e-3 if dt == torch.bfloat16 else 1e-3)
     assert err <= tol, err
+
+
+# ---------------------------------------------------------------------------
+# ls2_copy_spans: the engine's one-launch step inputs (pinned host -> device)
+# ---------------------------------------------------------------------------
+def test_copy_spans_pinned_and_device_sources():
+    import ctypes
+    from paper_2110_05722_b200 import _lib
+    from paper_2110_05722_b200.errors import ShapeMismatch
+    g = torch.Generator().manual_seed(5)
+    sizes = [64 * 64, 64 * 64, 64 * 64, 64, 0, 37, 1, 3000]
+    srcs = [torch.randint(-2**62, 2**62, (n,), generator=g, dtype=torch.int64) for n in sizes]
+    srcs = [s.pin_memory() if i % 2 == 0 else s.cuda() for i, s in enumerate(srcs)]
+    dsts = [torch.full((n,), -1, dtype=torch.int64, device="cuda") for n in sizes]
+    P8 = ctypes.c_void_p * 8
+    _lib.call("ls2_copy_spans", P8(*[d.data_ptr() for d in dsts]), P8(*[s.data_ptr() for s in srcs]),
+              (ctypes.c_int64 * 8)(*[8 * n for n in sizes]), 8, None)
+    torch.cuda.synchronize()
+    for d, s in zip(dsts, srcs):
+        assert torch.equal(d.cpu(), s.cpu())
+    # graph-captured with pinned sources: a replay reads the CURRENT host contents
+    h = torch.arange(100, dtype=torch.int64).pin_memory()
+    d = torch.zeros(100, dtype=torch.int64, device="cuda")
+    st = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        _lib.call("ls2_copy_spans", (ctypes.c_void_p * 1)(d.data_ptr()),
+                  (ctypes.c_void_p * 1)(h.data_ptr()), (ctypes.c_int64 * 1)(800), 1,
+                  _lib.stream_handle())
+    h.copy_(torch.arange(100, 200, dtype=torch.int64))
+    gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(d.cpu(), torch.arange(100, 200, dtype=torch.int64))
+    with pytest.raises(ShapeMismatch):
+        _lib.call("ls2_copy_spans", (ctypes.c_void_p * 1)(d.data_ptr()),
+                  (ctypes.c_void_p * 1)(h.data_ptr()), (ctypes.c_int64 * 1)(12), 1, None)
+    with pytest.raises(ShapeMismatch):
+        _lib.call("ls2_copy_spans", P8(), P8(), (ctypes.c_int64 * 8)(), 9, None)
