@@ -7,7 +7,7 @@ TAG=${1:-r2}
 OUT=gpurun_out/sanitize_${TAG}
 mkdir -p "$OUT"
 CS="compute-sanitizer --print-limit 20 --error-exitcode 99"
-SEL_OPS='fused_criterion_vs_oracle and (37-29 or 2-250000 or 300-64000 or 257-100008 or 40-500000) or embedding_fp16_tbase_shape or dropout_bits_multi or bdr_layernorm_read_bits or (gemm_tc_two_sm_vs_torch and 4068-1536-512 and plain) or (wgrad_tc_vs_torch and 512-512-4096) or (layernorm_fp16_storage_vs_oracle)'
+SEL_OPS='fused_criterion_vs_oracle and (37-29 or 2-250000 or 300-64000 or 257-100008 or 40-500000) or embedding_fp16_tbase_shape or dropout_bits_multi or bdr_layernorm_read_bits or (gemm_tc_two_sm_vs_torch and 4068-1536-512 and plain) or (wgrad_tc_vs_torch and 512-512-4096) or (layernorm_fp16_storage_vs_oracle) or elementwise_fp16_storage_vs_oracle or copy_spans'
 SEL_ATT='test_tc_attention_matches_mma_kernels and (padding or causal)'
 for TOOL in memcheck racecheck synccheck; do
   echo "== $TOOL smoke" > "$OUT/$TOOL.log"
