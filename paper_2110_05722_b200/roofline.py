@@ -69,6 +69,16 @@ def algo_table(tokens: int, d: int, f: int, vocab: int, batch: int, length: int,
     ]
 
 
+def tensor_flops(batch: int, length: int, heads: int, d: int):
+    """[(regex, FLOPs per launch)] of the kernels bound by the tensor cores and
+    their issue chain rather than by HBM: the flash attention passes at
+    128 < L <= 512, 2·L²·hd FLOPs per (batch, head) and product (forward S, PV;
+    dQ pass S, dP, dQ; dK/dV pass S, dP, dV, dK)."""
+    per = 2 * batch * heads * length * length * (d // heads)
+    return [(r"attn_flash_fwd_kernel", 2 * per), (r"attn_flash_dq_kernel", 3 * per),
+            (r"attn_flash_dkv_kernel", 4 * per)]
+
+
 def profile_graph(graph, steps: int = 5) -> dict:
     """CUPTI kernel durations over `steps` replays of a captured step graph:
     {name: [launches per step, us per step]}."""
@@ -90,10 +100,13 @@ def profile_graph(graph, steps: int = 5) -> dict:
     return {k: [v[0] / steps, v[1] / steps] for k, v in agg.items()}
 
 
-def kernel_table(times: dict, algo, peak_gbs: float) -> list:
+def kernel_table(times: dict, algo, peak_gbs: float, flops=None, peak_tflops=None) -> list:
     """Rows for the hand-written kernels of `times` (profile_graph output),
     largest step share first: name, what, launches/step, us/launch, us/step,
-    algorithmic bytes/launch, achieved GB/s, fraction of peak."""
+    algorithmic bytes/launch, achieved GB/s, fraction of peak.  Kernels listed in
+    `flops` (tensor_flops) are bound by the tensor cores: their `frac` is achieved
+    TFLOP/s over `peak_tflops` (`bound` "tensor"; the HBM fraction stays as
+    `hbm_frac`)."""
     rows = []
     for name, (n, us_step) in times.items():
         for pat, what, nbytes in algo:
@@ -106,7 +119,15 @@ def kernel_table(times: dict, algo, peak_gbs: float) -> list:
                        "bytes_per_launch": nbytes}
                 if nbytes is not None:
                     gbs = nbytes / (us * 1e-6) / 1e9
-                    row.update(achieved_gbs=round(gbs, 1), frac=round(gbs / peak_gbs, 3))
+                    row.update(bound="hbm", achieved_gbs=round(gbs, 1),
+                               frac=round(gbs / peak_gbs, 3))
+                for fpat, nflop in (flops or []):
+                    if peak_tflops and re.search(fpat, name):
+                        tf = nflop / (us * 1e-6) / 1e12
+                        row.update(bound="tensor", flops_per_launch=nflop,
+                                   achieved_tflops=round(tf, 1), hbm_frac=row.get("frac"),
+                                   frac=round(tf / peak_tflops, 3))
+                        break
                 rows.append(row)
                 break
     rows.sort(key=lambda r: -r["us_per_step"])
