@@ -621,6 +621,128 @@ ln_bwd_stage(
     partial[(int64_t)blockIdx.x * npairs + p] = (double)accs[p];
 }
 
+// Several row batches per CTA (d >= 768: T-big, BERT): each warp keeps its column
+// partials in registers over all of its rows and the CTA folds them ONCE at the
+// end (warp order, fp32), instead of staging every batch in shared memory and
+// folding it behind a barrier.  Per-row math is ln_bwd_stage's, so dx / dproj
+// are identical; the partials differ only in fp32 summation order.
+constexpr int kLnRegWarps = 8;
+template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP>
+__global__ void __launch_bounds__(kLnRegWarps * 32, 1) ln_bwd_reg(
+    const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
+    const Tstat* __restrict__ mu, const Tstat* __restrict__ sigma, const Tin* __restrict__ dres,
+    Tout* __restrict__ dx, const uint8_t* __restrict__ bits, Tout* __restrict__ dproj,
+    float dscale, double* __restrict__ partial, int64_t rows, int64_t cols) {
+  constexpr int NP = BDR ? 3 : 2;
+  extern __shared__ __align__(16) float red[];   // [warps][NP][cols], the final fold
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t cgs = cols / 8;
+  const int npairs = NP * (int)cols;
+  float acc[NP][ITERS][8];
+#pragma unroll
+  for (int k = 0; k < NP; ++k)
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[k][it][e] = 0.f;
+  Pack8<Tin> wv[ITERS];
+#pragma unroll
+  for (int it = 0; it < ITERS; ++it) {
+    const int64_t g = lane + 32 * it;
+    if (g < cgs) wv[it] = ld8(w + g * 8);
+  }
+  const float inv_m = (float)(1.0 / (double)cols);
+  for (int64_t r = (int64_t)blockIdx.x * nw + wid; r < rows; r += (int64_t)gridDim.x * nw) {
+    Pack8<Tin> cd[ITERS], cx[ITERS], cr[ITERS];
+    uint32_t kbs[ITERS];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t g = lane + 32 * it;
+      kbs[it] = 0xFF;
+      if (g < cgs) {
+        cd[it] = ld8_stream(dy + r * cols + g * 8);
+        cx[it] = ld8_stream(x + r * cols + g * 8);
+        if (RES) cr[it] = ld8_stream(dres + r * cols + g * 8);
+        if (BDR && DROP) kbs[it] = bits[r * cgs + g];
+      }
+    }
+    const float m_r = (float)mu[r];
+    const float rs = (float)(1.0 / (double)sigma[r]);
+    const float2 rs2 = f2s(rs), nmrs2 = f2s(-m_r * rs);
+    float2 r1v = f2s(0.f), r3v = f2s(0.f);
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      if (lane + 32 * it < cgs) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 dv = pair_f2(cd[it], e);
+          const float2 xh = f2fma(pair_f2(cx[it], e), rs2, nmrs2);
+          const float2 gg = f2mul(pair_f2(wv[it], e), dv);
+          r1v = f2add(r1v, gg);
+          r3v = f2fma(gg, xh, r3v);
+          const float2 c0 = f2mul(dv, xh);
+          acc[0][it][2 * e] += c0.x;
+          acc[0][it][2 * e + 1] += c0.y;
+          acc[1][it][2 * e] += dv.x;
+          acc[1][it][2 * e + 1] += dv.y;
+        }
+      }
+    }
+    const float r1 = warp_sum(r1v.x + r1v.y) * inv_m;
+    const float r3 = warp_sum(r3v.x + r3v.y) * inv_m;
+    const float2 nr1 = f2s(-r1), nr3 = f2s(-r3);
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t g = lane + 32 * it;
+      if (g < cgs) {
+        Pack8<Tout> o;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 dv = pair_f2(cd[it], e);
+          const float2 xh = f2fma(pair_f2(cx[it], e), rs2, nmrs2);
+          const float2 gg = f2mul(pair_f2(wv[it], e), dv);
+          float2 v = f2mul(f2fma(xh, nr3, f2add(gg, nr1)), rs2);
+          if (RES) v = f2add(v, pair_f2(cr[it], e));
+          o.v[2 * e] = cvt<Tout>(v.x);
+          o.v[2 * e + 1] = cvt<Tout>(v.y);
+        }
+        st8(dx + r * cols + g * 8, o);
+        if (BDR) {
+          const uint32_t kb = kbs[it];
+          Pack8<Tout> pj;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float v = cvt<float>(o.v[e]);
+            if (DROP) v = mul_rn(mul_rn(v, bitval<float>(kb, e)), dscale);
+            acc[NP - 1][it][e] += v;
+            pj.v[e] = cvt<Tout>(v);
+          }
+          st8(dproj + r * cols + g * 8, pj);
+        }
+      }
+    }
+  }
+  float* my = red + (int64_t)wid * npairs;
+#pragma unroll
+  for (int it = 0; it < ITERS; ++it) {
+    const int64_t g = lane + 32 * it;
+    if (g < cgs) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        float4* d = reinterpret_cast<float4*>(my + k * cols + g * 8);
+        d[0] = make_float4(acc[k][it][0], acc[k][it][1], acc[k][it][2], acc[k][it][3]);
+        d[1] = make_float4(acc[k][it][4], acc[k][it][5], acc[k][it][6], acc[k][it][7]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    float t = 0.f;
+    for (int q = 0; q < nw; ++q) t += red[(int64_t)q * npairs + p];
+    partial[(int64_t)blockIdx.x * npairs + p] = (double)t;
+  }
+}
+
 // generic backward: CTA per row for dx; param partials by a column-parallel kernel
 template <typename Tin, typename Tout, typename Tstat>
 __global__ void ln_bwd_block(const Tin* __restrict__ dy, const Tin* __restrict__ x,
@@ -761,9 +883,30 @@ int ln_bwd_launch(const void* dy, const void* x, const void* w, const void* mu, 
           (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows,
           cols);
     };
-    // several row batches per CTA (T-big, BERT): overlap each fold with the next loads
-    if (rows > (int64_t)nblk * rw) go(std::true_type{});
-    else go(std::false_type{});
+    // several row batches per CTA at d > 512 (T-big, BERT): register partials, one
+    // fold (LS2_LN_BWD_REG=0: the staged kernel with each fold overlapping the next
+    // batch's loads)
+    static const bool reg_ok = [] {
+      const char* e = getenv("LS2_LN_BWD_REG");
+      return !(e && e[0] == '0');
+    }();
+    if (reg_ok && I >= 4 && rows > (int64_t)nblk * rw) {
+      const size_t rsm = (size_t)kLnRegWarps * NP * cols * sizeof(float);
+      static bool rattr = false;
+      if (!rattr) {
+        cudaFuncSetAttribute(ln_bwd_reg<Tin, Tout, Tstat, I, R, B, D>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        rattr = true;
+      }
+      ln_bwd_reg<Tin, Tout, Tstat, I, R, B, D><<<nblk, kLnRegWarps * 32, rsm, st>>>(
+          (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
+          (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows,
+          cols);
+    } else if (rows > (int64_t)nblk * rw) {
+      go(std::true_type{});
+    } else {
+      go(std::false_type{});
+    }
   }
   return check_launch(B ? "layernorm_bwd_bdr" : "layernorm_bwd");
 }

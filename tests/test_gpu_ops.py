@@ -89,7 +89,9 @@ def test_layernorm_known_answers_and_errors(golden_ops):
     assert rel_err(H(cs.sigma), g["ln_shift_sigma"]) < 1e-9
 
 
-@pytest.mark.parametrize("rows,cols", [(4096, 512), (1000, 1024), (333, 48), (64, 2048), (7, 13)])
+# (8192, 1024) and (4096, 768): several row batches per CTA -> ln_bwd_reg
+@pytest.mark.parametrize("rows,cols", [(4096, 512), (1000, 1024), (8192, 1024), (4096, 768), (333, 48),
+                                       (64, 2048), (7, 13)])
 def test_layernorm_fp16_storage_vs_oracle(rows, cols):
     rng = np.random.default_rng(rows + cols)
     x = (rng.normal(size=(rows, cols)) * 2 + 0.5).astype(np.float16)
