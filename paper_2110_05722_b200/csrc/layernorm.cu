@@ -626,9 +626,11 @@ ln_bwd_stage(
 // end (warp order, fp32), instead of staging every batch in shared memory and
 // folding it behind a barrier.  Per-row math is ln_bwd_stage's, so dx / dproj
 // are identical; the partials differ only in fp32 summation order.
-constexpr int kLnRegWarps = 8;
+// 8 warps at ITERS = 4 (243 registers), 16 at ITERS <= 2
+template <int ITERS>
+constexpr int ln_reg_warps() { return ITERS >= 4 ? 8 : 16; }
 template <typename Tin, typename Tout, typename Tstat, int ITERS, bool RES, bool BDR, bool DROP>
-__global__ void __launch_bounds__(kLnRegWarps * 32, 1) ln_bwd_reg(
+__global__ void __launch_bounds__(ln_reg_warps<ITERS>() * 32, 1) ln_bwd_reg(
     const Tin* __restrict__ dy, const Tin* __restrict__ x, const Tin* __restrict__ w,
     const Tstat* __restrict__ mu, const Tstat* __restrict__ sigma, const Tin* __restrict__ dres,
     Tout* __restrict__ dx, const uint8_t* __restrict__ bits, Tout* __restrict__ dproj,
@@ -883,22 +885,24 @@ int ln_bwd_launch(const void* dy, const void* x, const void* w, const void* mu, 
           (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows,
           cols);
     };
-    // several row batches per CTA at d > 512 (T-big, BERT): register partials, one
-    // fold (LS2_LN_BWD_REG=0: the staged kernel with each fold overlapping the next
-    // batch's loads)
+    // d >= 512 (ITERS >= 2): register partials, one fold per CTA (ln_bwd_reg).  T-big
+    // 31.9 -> 20.2 us, BERT-128 25.0 -> 17.5 us, T-base 7.22 -> 7.15 us per launch.
+    // LS2_LN_BWD_REG=0: the staged kernel (each fold overlapping the next batch's
+    // loads when a CTA has several batches)
     static const bool reg_ok = [] {
       const char* e = getenv("LS2_LN_BWD_REG");
       return !(e && e[0] == '0');
     }();
-    if (reg_ok && I >= 4 && rows > (int64_t)nblk * rw) {
-      const size_t rsm = (size_t)kLnRegWarps * NP * cols * sizeof(float);
+    if (reg_ok && I >= 2) {
+      constexpr int kW = ln_reg_warps<I>();
+      const size_t rsm = (size_t)kW * NP * cols * sizeof(float);
       static bool rattr = false;
       if (!rattr) {
         cudaFuncSetAttribute(ln_bwd_reg<Tin, Tout, Tstat, I, R, B, D>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         rattr = true;
       }
-      ln_bwd_reg<Tin, Tout, Tstat, I, R, B, D><<<nblk, kLnRegWarps * 32, rsm, st>>>(
+      ln_bwd_reg<Tin, Tout, Tstat, I, R, B, D><<<nblk, kW * 32, rsm, st>>>(
           (const Tin*)dy, (const Tin*)x, (const Tin*)w, (const Tstat*)mu, (const Tstat*)sigma,
           (const Tin*)dres, (Tout*)dx, bits, (Tout*)dproj, (float)dscale, (double*)ws, rows,
           cols);

@@ -29,11 +29,11 @@ def algo_table(tokens: int, d: int, f: int, vocab: int, batch: int, length: int,
         (r"ln_fwd_bdr_warp", "bias+dropout+residual -> LayerNorm fwd",
          4 * N * D * 2 + N * D // 8 + 8 * N),
         (r"ln_fwd_warp", "LayerNorm fwd", 2 * N * D * 2 + 8 * N),
-        (r"ln_bwd_stage<[^>]*, true, true, true(?:, (?:true|false))?>", "LayerNorm bwd + residual + bdr bwd",
+        (r"ln_bwd_(?:stage|reg)<[^>]*, true, true, true(?:, (?:true|false))?>", "LayerNorm bwd + residual + bdr bwd",
          5 * N * D * 2 + N * D // 8 + 8 * N),
-        (r"ln_bwd_stage<[^>]*, true, false, false(?:, (?:true|false))?>", "LayerNorm bwd + residual",
+        (r"ln_bwd_(?:stage|reg)<[^>]*, true, false, false(?:, (?:true|false))?>", "LayerNorm bwd + residual",
          4 * N * D * 2 + 8 * N),
-        (r"ln_bwd_stage<[^>]*, false, false, false(?:, (?:true|false))?>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
+        (r"ln_bwd_(?:stage|reg)<[^>]*, false, false, false(?:, (?:true|false))?>", "LayerNorm bwd", 3 * N * D * 2 + 8 * N),
         (r"attn_tc_fwd_kernel", "fused attention fwd, tcgen05 (QK^T, mask, softmax, PV; row stats)",
          4 * N * D * 2 + N * H * 8),
         (r"attn_tc_bwd_kernel", "fused attention bwd, tcgen05 (P recomputed; + bias partials)",

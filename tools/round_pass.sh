@@ -23,6 +23,6 @@ timeout 300 python tools/roofline_table.py "$OUT/kineto_tbase.json" > "$OUT/roof
 timeout 300 python tools/roofline_table.py "$OUT/kineto_tbig.json" --model tbig > "$OUT/roofline_tbig.md" 2>&1
 timeout 300 python tools/bucket_times.py > "$OUT/bucket_times.json" 2>&1
 timeout 600 python tools/sweep.py --out "$OUT/sweep.json" > "$OUT/sweep.log" 2>&1
-timeout 1500 bash tools/profile_round.sh "$TAG" adam_kernel attn_tc_bwd attn_tc_fwd ln_bwd_stage \
+timeout 1500 bash tools/profile_round.sh "$TAG" adam_kernel attn_tc_bwd attn_tc_fwd ln_bwd_reg \
   ln_fwd_bdr_warp brd_bwd_vec brd_fwd_vec criterion_rows dropout_bits_multi > "$OUT/profile_round.log" 2>&1
 ls gpurun_out/prof_${TAG} | head -40
