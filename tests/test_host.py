@@ -252,3 +252,27 @@ def test_wmt_shaped_task_buckets_and_budget():
         b2 = t.batch(s)
         assert np.array_equal(np.asarray(b2.src), src)      # pure function of step
     assert len(seen) > 4
+
+
+def test_roofline_table_kernel_names_and_bounds():
+    """bench.py's per-kernel roofline rows: the LayerNorm backward is matched under
+    both kernel names, and the flash attention passes are reported against the
+    tensor peak with their HBM fraction kept (paper_2110_05722_b200/roofline.py)."""
+    from paper_2110_05722_b200 import roofline as RL
+    algo = RL.algo_table(4096, 512, 2048, 32000, 64, 64, 8, 60_655_616)
+    times = {
+        "void ls2::ln_bwd_reg<__half, __half, float, 2, true, true, true>(a)": [28, 200.0],
+        "void ls2::ln_bwd_stage<__half, __half, float, 2, true, true, true, false>(a)": [28, 210.0],
+        "ls2::atc::attn_flash_dkv_kernel(a)": [12, 960.0],
+        "nvjet_hsh_128x128_64x8_2x2_2cta_v_bz_NNT": [49, 340.0],
+    }
+    rows = RL.kernel_table(times, algo, 6545.0, flops=RL.tensor_flops(16, 512, 12, 768),
+                           peak_tflops=1419.7)
+    by = {r["kernel"].split("<")[0]: r for r in rows}
+    assert set(by) == {"ln_bwd_reg", "ln_bwd_stage", "atc::attn_flash_dkv_kernel"}  # no cuBLAS rows
+    assert by["ln_bwd_reg"]["bound"] == "hbm" and by["ln_bwd_reg"]["bytes_per_launch"] == \
+        5 * 4096 * 512 * 2 + 4096 * 512 // 8 + 8 * 4096
+    fl = by["atc::attn_flash_dkv_kernel"]
+    assert fl["bound"] == "tensor" and fl["flops_per_launch"] == 4 * 2 * 16 * 12 * 512 * 512 * 64
+    assert abs(fl["frac"] - fl["achieved_tflops"] / 1419.7) < 1e-3 and fl["hbm_frac"] < fl["frac"]
+    assert [r["us_per_step"] for r in rows] == sorted((r["us_per_step"] for r in rows), reverse=True)
